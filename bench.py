@@ -1,0 +1,414 @@
+#!/usr/bin/env python3
+"""Decode benchmark of the B200 DeepSpeed-Inference hot path (BASELINE.json configs[1]: GPT-J-6B shape).
+
+One "step" = one greedy decode step (one token per sequence) through every layer, the LM head and
+the argmax, replayed from a CUDA graph.  Default: N=1, GPT-J-6B fp16, batch 1, 128-token prompt.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config gptj-6b] [--dtype fp16|int8] [--batch 1]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL over NVLink): tensor parallel TP=N of the
+same model (strong scaling), timed on the device as the max over ranks.
+`--impl reference` times the reference's own CPU implementation of the path (exec_reference from
+the reference headers, oracle/_ref) on the host cores, for the same metric and config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20220701
+METRIC = "decode_tokens_per_s"
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference path (exec_reference)
+
+def gemm_shapes(preset, tp):
+    h = preset.hidden
+    vpad = (preset.vocab + 128 * tp - 1) // (128 * tp) * (128 * tp)
+    layer = [("qkv", 3 * h // tp, h), ("attn_out", h, h // tp), ("mlp_up", 4 * h // tp, h), ("mlp_down", h, 4 * h // tp)]
+    return layer, ("lm_head", vpad // tp, h)
+
+
+def reference_ms_per_token(preset, tp, batch, dtype_bytes, budget_s, threads):
+    """exec_reference (gemm.hpp:147-202, compiled from the reference headers) on a row sample of every
+    per-rank GEMM of one decode step; per-token time = L * sum(layer GEMMs) + LM head, each scaled
+    from its row sample (every output row costs the same).  Returns (ms_per_token, kind, sample)."""
+    from oracle import oracle as O
+
+    layer, lm = gemm_shapes(preset, tp)
+    shapes = layer + [lm]
+    ref = O.ref_lib()
+    kind = "reference" if ref is not None else "port"
+    per_shape = budget_s / len(shapes)
+    total_ms = 0.0
+    rows_used = {}
+    for name, N, K in shapes:
+        # calibrate: time a small sample, then size the real sample to the per-shape budget
+        rows = max(threads, 64)
+        t = _time_rows(O, ref, N, K, batch, dtype_bytes, rows, threads)
+        rate = t / rows
+        rows = int(min(N, max(threads, per_shape / max(rate, 1e-9))))
+        t = _time_rows(O, ref, N, K, batch, dtype_bytes, rows, threads)
+        ms_full = t * (N / rows) * 1e3
+        rows_used[name] = rows
+        total_ms += ms_full * (preset.layers if name != "lm_head" else 1)
+    sample = "exec_reference on row samples " + ", ".join(f"{k}:{v}" for k, v in rows_used.items()) + \
+             f" of each per-rank GEMM (B={batch}), x{threads} threads, extrapolated to L={preset.layers} layers + LM head"
+    return total_ms, kind, sample
+
+
+def _time_rows(O, ref, N, K, B, dtype_bytes, rows, threads):
+    import ctypes as C
+
+    if ref is not None:
+        cs = C.c_double()
+        return float(ref.ref_time_exec(N, K, B, dtype_bytes, 148, rows, threads, SEED, C.byref(cs)))
+    # port: the oracle's same-order restatement (multi-threaded)
+    W = np.random.default_rng(0).standard_normal((rows, K)).astype(np.float32)
+    x = np.random.default_rng(1).standard_normal((B, K))
+    s = O.derive_schedule(N, K, B, dtype_bytes)
+    t0 = time.perf_counter()
+    O.gemm_f64(W, x, s)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, preset, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    dtype_bytes = 1 if args.dtype == "int8" else 2
+    vals = []
+    for i in range(args.warmup + args.steps):
+        ms, kind, sample = reference_ms_per_token(preset, world, args.batch, dtype_bytes, args.ref_step_budget, threads)
+        if i >= args.warmup:
+            vals.append(ms)
+    ms = statistics.median(vals)
+    value = args.batch * 1e3 / ms
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, preset, world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, preset, world):
+    return {"workload": f"{preset.name} {args.dtype} greedy decode, batch {args.batch}, {args.prompt}-token prompt, "
+                        f"TP={world}", "model": args.config, "global_batch": args.batch, "seq_len": args.prompt,
+            "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------- our path
+
+def kernel_roofline(E, torch, preset, tp, batch, dtype, peak_gbs, stream):
+    """Times each SBI-GeMM shape of one layer (+ LM head) alone with CUDA events on the launching
+    stream; 4 rotating weight copies (> L2) per shape.  Returns the per-kernel list and the byte-weighted
+    aggregate for the dominant kernel family (sbi_gemm_kernel)."""
+    layer, lm = gemm_shapes(preset, tp)
+    dev = torch.device("cuda")
+    res = []
+    tot_b, tot_t = 0.0, 0.0
+    for name, N, K in layer + [lm]:
+        int8 = dtype == "int8" and name != "lm_head"
+        copies = []
+        for c in range(4):
+            w = (torch.randn(N, K, device=dev) * 0.02).half()
+            if int8:
+                copies.append(E.quantize_weights_int8(w))
+            else:
+                copies.append((E.pack_weights_device(w, 2), None))
+            del w
+        x = torch.randn(batch, K, device=dev).half()
+        out = torch.empty(batch, N, device=dev, dtype=torch.float32)
+        for i in range(3):
+            wq, ws = copies[i % 4]
+            E.gemm(wq, x, N, K, w_scales=ws, out=out, stream=stream)
+        n = 20
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        st.record(stream)
+        for i in range(n):
+            wq, ws = copies[i % 4]
+            E.gemm(wq, x, N, K, w_scales=ws, out=out, stream=stream)
+        en.record(stream)
+        en.synchronize()
+        ms = st.elapsed_time(en) / n
+        wbytes = N * K * (1 if int8 else 2) + (N * 4 if int8 else 0)
+        algo = wbytes + batch * K * 2 + batch * N * 4
+        gbs = algo / (ms * 1e-3) / 1e9
+        res.append({"kernel": f"sbi_gemm[{name}] N={N} K={K}", "us": round(ms * 1e3, 2), "bytes": algo,
+                    "gbs": round(gbs, 1), "frac": round(gbs / peak_gbs, 3)})
+        mult = preset.layers if name != "lm_head" else 1
+        tot_b += algo * mult
+        tot_t += ms * 1e-3 * mult
+        del copies
+        torch.cuda.empty_cache()
+    agg = tot_b / tot_t / 1e9
+    return res, agg
+
+
+def run_ours(args, preset, rank, world, local_rank):
+    import torch
+
+    from paper_2207_00032_b200 import _capi as capi
+    from paper_2207_00032_b200 import engine as E
+
+    torch.cuda.set_device(local_rank)
+    stream = torch.cuda.Stream()
+    peak_gbs, peak_kind = measured_peaks()
+    dtype_bytes = 1 if args.dtype == "int8" else 2
+    comm = None
+    if world > 1:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            capi.check(capi.lib.dsinf_nccl_get_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_uint8 * 128)(*obj[0])
+        h = C.c_void_p()
+        capi.check(capi.lib.dsinf_nccl_comm_create(uid, world, rank, local_rank, C.byref(h)))
+        comm = h.value
+    max_ctx = args.prompt + 2 * (args.warmup + args.steps) + 8
+    model = E.DecoderModel(preset.hidden, preset.layers, preset.heads, preset.vocab, dtype_bytes=dtype_bytes,
+                           batch=args.batch, max_ctx=max_ctx, tp_size=world, tp_rank=rank,
+                           tp_mode=capi.TP_NCCL if world > 1 else capi.TP_NONE, nccl_comm=comm,
+                           use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank)
+    rng = np.random.default_rng(SEED)
+    prompt = rng.integers(0, preset.vocab, (args.batch, args.prompt)).astype(np.int32)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # ---- device-timed decode (inputs resident in HBM)
+    model.set_prompt(prompt, stream=stream)
+    t0 = time.perf_counter()
+    model.step(args.prompt, stream=stream)  # prefill: prompt tokens through the same step graph
+    stream.synchronize()
+    prefill_s = time.perf_counter() - t0
+    model.step(args.warmup, stream=stream)
+    pos0 = args.prompt + args.warmup
+    barrier()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        st.record(stream)
+        model.step(args.steps, stream=stream)
+        en.record(stream)
+        en.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = args.batch * args.steps * 1e3 / ms  # whole-job tokens/s (every rank serves the same tokens)
+    info = model.get_info()
+    step_bytes = sum(model.bytes_per_step(p) for p in range(pos0, pos0 + args.steps))
+    step_gbs = step_bytes / (ms * 1e-3) / 1e9
+    _, hist = model.read_tokens(stream=stream)
+    gen_sample = hist[0, args.prompt: args.prompt + 8].tolist()
+
+    # ---- end to end through the C ABI with host buffers (H2D tokens in, D2H tokens out each step)
+    import ctypes as C
+
+    model.set_prompt(prompt, stream=stream)
+    model.step(args.prompt, stream=stream)
+    stream.synchronize()
+    tin = torch.empty(args.batch, dtype=torch.int32, pin_memory=True)
+    tout = torch.empty(args.batch, dtype=torch.int32, pin_memory=True)
+    nxt, _ = model.read_tokens(stream=stream)
+    tin.numpy()[:] = nxt
+    pin = C.cast(tin.data_ptr(), C.POINTER(C.c_int32))
+    pout = C.cast(tout.data_ptr(), C.POINTER(C.c_int32))
+    sp = stream.cuda_stream
+    for _ in range(args.warmup):
+        capi.check(capi.lib.dsinf_decode_step_host(model._h, pin, pout, sp))
+        tin.copy_(tout)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        capi.check(capi.lib.dsinf_decode_step_host(model._h, pin, pout, sp))
+        tin.copy_(tout)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch
+
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = args.batch * args.steps / e2e_s
+
+    # ---- dominant-kernel roofline (SBI-GeMM launches timed alone) and the CPU baseline: rank 0
+    roof = None
+    cpu = None
+    if rank == 0:
+        per_kernel, agg = kernel_roofline(E, torch, preset, world, args.batch, args.dtype, peak_gbs, stream)
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(f"{args.config}-{args.dtype}-b{args.batch}")
+        roof = {"bound": "hbm", "achieved": round(agg, 1), "peak": peak_gbs, "unit": "GB/s",
+                "frac": round(agg / peak_gbs, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "sbi_gemm_kernel (byte-weighted over one step's GEMM launches, timed alone)",
+                "per_kernel": per_kernel,
+                "step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak_gbs, 4),
+                         "bytes_per_step": int(step_bytes / args.steps)}}
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            cms, kind, sample = reference_ms_per_token(preset, 1, args.batch, dtype_bytes, args.cpu_budget, threads)
+            cpu = {"value": args.batch * 1e3 / cms, "unit": "tokens/s", "cores": threads, "kind": kind,
+                   "sample": sample, "ms_per_token": cms}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f16" if args.dtype == "fp16" else "int8", "data": "synthetic",
+        "config": workload_config(args, preset, world),
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": 4 * args.batch,
+                "d2h_bytes_per_step": 4 * args.batch, "ms_per_step": e2e_s * 1e3 / args.steps},
+        "gpu_launches": int(info.kernels_per_step) * args.steps,
+        "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+        "prefill_ms": round(prefill_s * 1e3, 2), "generated_sample": gen_sample,
+    }
+    model.close()
+    if comm is not None:
+        capi.lib.dsinf_nccl_comm_destroy(comm)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="gptj-6b")
+    ap.add_argument("--dtype", choices=["fp16", "int8"], default="fp16")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--prompt", type=int, default=128)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
+    ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_2207_00032_b200.engine import PRESETS
+
+    preset = PRESETS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world == 1:
+        world = 1
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    if args.impl == "reference":
+        run_reference(args, preset, rank, world)
+    else:
+        run_ours(args, preset, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+// C ABI for the device operators: SBI-GeMM, weight packing / INT8 quantisation, decode
+// attention, and the exec_reference drop-in (gemm.hpp:147-202) executed on the GPU.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+#include "ops.cuh"
+#include "sbi_gemm.cuh"
+#include "synth.h"
+
+using namespace dsinf;
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
+  require(a.w_packed && a.x && a.out, "null pointer argument");
+  require(a.N >= 1 && a.K >= 1 && a.B >= 1, "gemm shape dims must be positive");
+  require(a.N <= (1LL << 30) && a.K <= (1LL << 30), "gemm dims too large");
+  require(a.w_dtype == DSINF_DT_F16 || a.w_dtype == DSINF_DT_I8, "w_dtype must be F16 or I8");
+  require(a.out_dtype == DSINF_DT_F32 || a.out_dtype == DSINF_DT_F16, "out_dtype must be F32 or F16");
+  require(a.epilogue == DSINF_EPI_NONE || a.epilogue == DSINF_EPI_GELU, "unknown epilogue");
+  require(!(a.epilogue == DSINF_EPI_GELU && a.out_dtype == DSINF_DT_F32), "GeLU epilogue writes F16");
+  const bool i8w = a.w_dtype == DSINF_DT_I8;
+  if (i8w) {
+    require(a.w_scales != nullptr, "I8 weights need w_scales");
+    require(a.x_dtype == DSINF_DT_F16 || a.x_dtype == DSINF_DT_I8, "x_dtype must be F16 or I8");
+    if (a.x_dtype == DSINF_DT_I8) require(a.x_scales != nullptr, "I8 x needs x_scales");
+  } else {
+    require(a.x_dtype == DSINF_DT_F16, "F16 weights take F16 x");
+  }
+  const int N = static_cast<int>(a.N), K = static_cast<int>(a.K);
+  for (int64_t b0 = 0; b0 < a.B; b0 += gemm::kMaxB) {
+    const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
+    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit);
+    gemm::Params p{};
+    p.w = static_cast<const uint32_t*>(a.w_packed);
+    p.w_scale = a.w_scales;
+    p.N = N;
+    p.K = K;
+    p.rows = (K + (i8w ? 3 : 1)) / (i8w ? 4 : 2);
+    p.B = nb;
+    const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
+    p.x = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;
+    p.x_ld = K;
+    if (i8w)
+      p.pro = a.x_dtype == DSINF_DT_I8 ? gemm::PRO_I8 : gemm::PRO_QUANT;
+    else
+      p.pro = gemm::PRO_F16;
+    p.x_scale = a.x_scales ? a.x_scales + b0 : nullptr;
+    p.bias = static_cast<const __half*>(a.bias);
+    const int oes = a.out_dtype == DSINF_DT_F32 ? 4 : 2;
+    p.out = static_cast<uint8_t*>(a.out) + b0 * a.N * oes;
+    p.out_ld = N;
+    p.epi = a.out_dtype == DSINF_DT_F32 ? gemm::EPI_F32
+                                        : (a.epilogue == DSINF_EPI_GELU ? gemm::EPI_GELU_F16 : gemm::EPI_F16);
+    gemm::launch(p, plan, i8w, s, false);
+  }
+}
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  explicit DeviceBuffer(size_t bytes) { DSINF_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+  ~DeviceBuffer() { cudaFree(p); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
+
+}  // namespace
+
+extern "C" {
+
+int dsinf_gemm(const dsinf_gemm_args* args, void* stream) {
+  return guarded([&] {
+    require(args != nullptr, "null args");
+    gemm::configure();
+    run_gemm(*args, as_stream(stream));
+  });
+}
+
+int dsinf_gemm_launch_plan(int64_t N, int64_t K, int64_t B, int32_t w_dtype, dsinf_launch_plan* out) {
+  return guarded([&] {
+    require(out != nullptr, "null out");
+    require(N >= 1 && K >= 1 && B >= 1, "gemm shape dims must be positive");
+    const gemm::Plan p = gemm::make_plan(static_cast<int>(N), static_cast<int>(K),
+                                         static_cast<int>(std::min<int64_t>(B, gemm::kMaxB)), w_dtype == DSINF_DT_I8, 0);
+    out->col_tile = gemm::kColTile;
+    out->ksplit = p.ksplit;
+    out->rows_per_split = p.rows_per_split;
+    out->ctas = p.col_tiles * p.ksplit;
+    out->stages = p.stages;
+  });
+}
+
+int dsinf_pack_weights_device(const void* w_rowmajor, int32_t src_dtype, int64_t N, int64_t K, int32_t pack_M,
+                              void* packed_f16, void* stream) {
+  return guarded([&] {
+    require(w_rowmajor && packed_f16, "null pointer argument");
+    require(N >= 1 && K >= 1, "gemm shape dims must be positive");
+    require(src_dtype == DSINF_DT_F16 || src_dtype == DSINF_DT_F32, "src_dtype must be F16 or F32");
+    if (pack_M != 1 && pack_M != 2 && pack_M != 4) throw ConfigError("pack_M must be one of {1, 2, 4}");
+    ops::pack_f16(w_rowmajor, src_dtype == DSINF_DT_F32, N, K, pack_M, static_cast<__half*>(packed_f16),
+                  as_stream(stream));
+  });
+}
+
+int dsinf_quantize_weights_int8(const void* w_rowmajor_f16, int64_t N, int64_t K, int8_t* packed_i8, float* row_scales,
+                                void* stream) {
+  return guarded([&] {
+    require(w_rowmajor_f16 && packed_i8 && row_scales, "null pointer argument");
+    require(N >= 1 && K >= 1, "gemm shape dims must be positive");
+    ops::quantize_weights_i8(static_cast<const __half*>(w_rowmajor_f16), N, K, packed_i8, row_scales,
+                             as_stream(stream));
+  });
+}
+
+int dsinf_quantize_activations_int8(const void* x_f16, int64_t B, int64_t K, int8_t* xq, float* scales, void* stream) {
+  return guarded([&] {
+    require(x_f16 && xq && scales, "null pointer argument");
+    require(B >= 1 && K >= 1, "shape dims must be positive");
+    ops::quantize_act_i8(static_cast<const __half*>(x_f16), B, K, xq, scales, as_stream(stream));
+  });
+}
+
+int dsinf_attention_decode(const void* q, const void* kcache, const void* vcache, const int32_t* pos_dev, int64_t B,
+                           int64_t H, int64_t d, int64_t max_seq, void* out, void* stream) {
+  return guarded([&] {
+    require(q && kcache && vcache && pos_dev && out, "null pointer argument");
+    require(B >= 1 && H >= 1 && d >= 2 && max_seq >= 1, "bad attention shape");
+    ops::configure();
+    ops::AttnParams a{};
+    a.q = static_cast<const __half*>(q);
+    a.kc = static_cast<const __half*>(kcache);
+    a.vc = static_cast<const __half*>(vcache);
+    a.pos = pos_dev;
+    a.out = static_cast<__half*>(out);
+    a.B = static_cast<int>(B);
+    a.H = static_cast<int>(H);
+    a.d = static_cast<int>(d);
+    a.max_seq = static_cast<int>(max_seq);
+    a.scale = 1.0f / std::sqrt(static_cast<float>(d));
+    ops::attention(a, ops::attention_chunks(a.B, a.H), as_stream(stream), false);
+  });
+}
+
+int dsinf_exec_device(const double* packed, int64_t packed_len, const dsinf_gemm_shape* shape,
+                      const dsinf_gemm_schedule* schedule, const double* x, int64_t x_len, int64_t batch,
+                      int32_t compute_dtype, double* out, int64_t out_len) {
+  return guarded([&] {
+    require(packed && shape && schedule && x && out, "null pointer argument");
+    const int64_t N = shape->out_dim, K = shape->in_dim;
+    if (N < 1 || K < 1) throw ConfigError("gemm shape dims must be positive");
+    if (batch < 1 || x_len != batch * K) throw ConfigError("input shape mismatch");  // gemm.hpp:153-154
+    const int M = schedule->pack_M;
+    if (M != 1 && M != 2 && M != 4) throw ConfigError("pack_M must be one of {1, 2, 4}");
+    const int64_t kp = (K + M - 1) / M * M;
+    if (packed_len != N * kp) throw ConfigError("packed buffer size mismatch");
+    if (out_len != batch * N) throw ConfigError("output buffer size mismatch");
+    require(compute_dtype == DSINF_DT_F16 || compute_dtype == DSINF_DT_I8, "compute_dtype must be F16 or I8");
+    // unpack (host) -> fp16 row-major on device -> device pack / quantise -> SBI-GeMM
+    std::vector<uint16_t> w16(static_cast<size_t>(N * K));
+    for (int64_t n = 0; n < N; ++n)
+      for (int64_t k = 0; k < K; ++k)
+        w16[n * K + k] = f32_to_f16_bits(static_cast<float>(packed[(k / M) * (N * M) + n * M + (k % M)]));
+    std::vector<uint16_t> x16(static_cast<size_t>(batch * K));
+    for (int64_t i = 0; i < batch * K; ++i) x16[i] = f32_to_f16_bits(static_cast<float>(x[i]));
+    cudaStream_t s = nullptr;
+    DeviceBuffer dw(w16.size() * 2), dx(x16.size() * 2), dout(static_cast<size_t>(batch * N) * 4);
+    DSINF_CUDA_CHECK(cudaMemcpy(dw.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
+    DSINF_CUDA_CHECK(cudaMemcpy(dx.p, x16.data(), x16.size() * 2, cudaMemcpyHostToDevice));
+    gemm::configure();
+    dsinf_gemm_args a{};
+    a.N = N;
+    a.K = K;
+    a.B = batch;
+    a.x = dx.p;
+    a.x_dtype = DSINF_DT_F16;
+    a.out = dout.p;
+    a.out_dtype = DSINF_DT_F32;
+    a.epilogue = DSINF_EPI_NONE;
+    if (compute_dtype == DSINF_DT_F16) {
+      DeviceBuffer dp(static_cast<size_t>((K + 1) / 2 * 2 * N) * 2);
+      ops::pack_f16(dw.p, false, N, K, 2, static_cast<__half*>(dp.p), s);
+      a.w_packed = dp.p;
+      a.w_dtype = DSINF_DT_F16;
+      run_gemm(a, s);
+      DSINF_CUDA_CHECK(cudaDeviceSynchronize());
+    } else {
+      DeviceBuffer dp(static_cast<size_t>((K + 3) / 4 * 4 * N)), ds(static_cast<size_t>(N) * 4);
+      ops::quantize_weights_i8(static_cast<const __half*>(dw.p), N, K, static_cast<int8_t*>(dp.p),
+                               static_cast<float*>(ds.p), s);
+      a.w_packed = dp.p;
+      a.w_dtype = DSINF_DT_I8;
+      a.w_scales = static_cast<const float*>(ds.p);
+      run_gemm(a, s);
+      DSINF_CUDA_CHECK(cudaDeviceSynchronize());
+    }
+    std::vector<float> o(static_cast<size_t>(batch * N));
+    DSINF_CUDA_CHECK(cudaMemcpy(o.data(), dout.p, o.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < o.size(); ++i) out[i] = o[i];
+  });
+}
+
+}  // extern "C"

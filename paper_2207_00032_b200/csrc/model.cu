@@ -1,0 +1,725 @@
+// Decoder-model runtime: synthetic weights on device, the per-step kernel schedule (Deep-Fusion
+// regions of PAPER.md:988-993 around SBI-GeMM), tensor-parallel sharding with NCCL (or all
+// shards on one device), and whole-step CUDA-graph capture.
+//
+// Step schedule per shard (t = TP degree; "AR" = all-reduce of a fp32 [B][h] partial):
+//   embed                                  res0 = wte[token]
+//   per layer:
+//     K1 LN1+QKV+bias+RoPE+KV-append       prologue: res1 = res0 (+ d_mlp + b_down[l-1]) ; LN1
+//     K2 attention over the KV cache
+//     K3 attn-out GEMM                     -> d_attn (partial when t > 1)         AR(d_attn)
+//     K4 LN2+MLP-up+bias+GeLU              prologue: res0 = res1 + d_attn + b_o ; LN2
+//     K5 MLP-down GEMM                     -> d_mlp                               AR(d_mlp)
+//   LM head (final LN prologue: res0 + d_mlp + b_down[L-1]) -> logits ; argmax    AG(argmax)
+//   select: greedy token (ties -> lowest id), pos += 1
+// The residual bias+add (paper region 4) lives in the next LayerNorm's prologue, which is
+// also where the TP all-reduced partial is folded in, so t = 1 and t > 1 share one path.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "nccl_dl.h"
+#include "ops.cuh"
+#include "sbi_gemm.cuh"
+#include "synth.h"
+
+namespace dsinf {
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct LayerW {
+  uint32_t* wqkv = nullptr;
+  float* sqkv = nullptr;
+  __half* bqkv = nullptr;
+  __half *ln1g = nullptr, *ln1b = nullptr;
+  uint32_t* wo = nullptr;
+  float* so = nullptr;
+  __half* bo = nullptr;
+  __half *ln2g = nullptr, *ln2b = nullptr;
+  uint32_t* wup = nullptr;
+  float* sup = nullptr;
+  __half* bup = nullptr;
+  uint32_t* wdown = nullptr;
+  float* sdown = nullptr;
+  __half* bdown = nullptr;
+};
+
+struct Shard {
+  int rank = 0;
+  std::vector<LayerW> layers;
+  uint32_t* wlm = nullptr;  // fp16 packed [h/2][Vl][2]
+  __half *lnfg = nullptr, *lnfb = nullptr;
+  __half* wte = nullptr;    // row-major [V][h] (replicated)
+  float* res[2] = {nullptr, nullptr};
+  float* d_attn = nullptr;
+  float* d_mlp = nullptr;
+  __half* q = nullptr;
+  __half* a = nullptr;
+  __half* u = nullptr;
+  float* logits = nullptr;
+  __half* kc = nullptr;
+  __half* vc = nullptr;
+  gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
+};
+
+}  // namespace
+
+}  // namespace dsinf
+
+struct dsinf_model {
+  dsinf_model_config cfg{};
+  dsinf_runtime_config rt{};
+  int64_t h = 0, L = 0, H = 0, d = 0, Hl = 0, V = 0, Vpad = 0, Vl = 0, F = 0, Fl = 0;
+  int B = 0, t = 1, max_ctx = 0;
+  bool int8 = false;
+  std::vector<dsinf::DevBuf> allocs;
+  std::vector<dsinf::Shard> shards;
+  float2* rope = nullptr;
+  int32_t* prompt = nullptr;
+  int prompt_cap = 0, prompt_len = 0;
+  int32_t* next_tok = nullptr;
+  int32_t* hist = nullptr;
+  int* pos = nullptr;
+  float* am_val = nullptr;  // [t][B]
+  int32_t* am_idx = nullptr;
+  dsinf::nccl::Comm comm = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t host_pos = 0;
+  int64_t weight_bytes = 0;
+  int64_t kernels_per_step = 0;
+  int attn_chunks = 1;
+
+  void* alloc(size_t bytes) {
+    void* p = nullptr;
+    DSINF_CUDA_CHECK(cudaMalloc(&p, bytes));
+    allocs.push_back({p, bytes});
+    return p;
+  }
+  template <class T>
+  T* alloc_n(int64_t n) {
+    return static_cast<T*>(alloc(static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T)));
+  }
+  ~dsinf_model() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (auto& a : allocs) cudaFree(a.p);
+  }
+};
+
+namespace dsinf {
+
+namespace {
+
+using Model = dsinf_model;
+
+ops::ShardMap make_map(const Model& m, int64_t N_local, int64_t K_local, int64_t N_global, int64_t K_global,
+                       int64_t sec_local, int64_t sec_global, int64_t row_off, int64_t col_off, int layer,
+                       int tensor, float amp, int64_t valid_rows = -1) {
+  ops::ShardMap s{};
+  s.N_local = N_local;
+  s.K_local = K_local;
+  s.N_global = N_global;
+  s.K_global = K_global;
+  s.sec_local = sec_local;
+  s.sec_global = sec_global;
+  s.row_off = row_off;
+  s.col_off = col_off;
+  s.valid_rows = valid_rows < 0 ? N_global : valid_rows;
+  s.base = synth_base(m.rt.seed, layer, tensor);
+  s.amp = amp;
+  return s;
+}
+
+// Allocates and generates one GEMM weight in the packed layout (fp16 M=2 or int8 M=4).
+uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaStream_t s) {
+  const int M = m.int8 ? 4 : 2;
+  const int64_t words = (map.K_local + M - 1) / M * map.N_local;
+  uint32_t* w = m.alloc_n<uint32_t>(words);
+  m.weight_bytes += words * 4;
+  if (m.int8) {
+    *scales = m.alloc_n<float>(map.N_local);
+    m.weight_bytes += map.N_local * 4;
+    ops::init_packed_i8(map, w, *scales, s);
+  } else {
+    *scales = nullptr;
+    ops::init_packed_f16(map, w, s);
+  }
+  return w;
+}
+
+__half* make_vec(Model& m, const ops::ShardMap& map, float offset, cudaStream_t s) {
+  __half* v = m.alloc_n<__half>(map.N_local);
+  m.weight_bytes += map.N_local * 2;
+  ops::init_vector_f16(map, offset, v, s);
+  return v;
+}
+
+void build_shard(Model& m, Shard& sh, cudaStream_t s) {
+  const int r = sh.rank;
+  const int64_t h = m.h, Hl = m.Hl, d = m.d, Fl = m.Fl;
+  const float aw = SynthScale::kWeight, ab = SynthScale::kBias;
+  sh.layers.resize(m.L);
+  for (int l = 0; l < m.L; ++l) {
+    LayerW& w = sh.layers[l];
+    // QKV: column parallel by head; local rows [q_r | k_r | v_r]
+    w.wqkv = make_weight(m, make_map(m, 3 * Hl * d, h, 3 * h, h, Hl * d, h, r * Hl * d, 0, l, DSINF_T_QKV, aw), &w.sqkv, s);
+    w.bqkv = make_vec(m, make_map(m, 3 * Hl * d, 1, 3 * h, 1, Hl * d, h, r * Hl * d, 0, l, DSINF_T_QKV_BIAS, ab), 0.f, s);
+    // attn-out: row parallel (K = this rank's heads)
+    w.wo = make_weight(m, make_map(m, h, Hl * d, h, h, h, h, 0, r * Hl * d, l, DSINF_T_O, aw), &w.so, s);
+    w.bo = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_O_BIAS, ab), 0.f, s);
+    // MLP: up column parallel, down row parallel
+    w.wup = make_weight(m, make_map(m, Fl, h, m.F, h, Fl, m.F, r * Fl, 0, l, DSINF_T_UP, aw), &w.sup, s);
+    w.bup = make_vec(m, make_map(m, Fl, 1, m.F, 1, Fl, m.F, r * Fl, 0, l, DSINF_T_UP_BIAS, ab), 0.f, s);
+    w.wdown = make_weight(m, make_map(m, h, Fl, h, m.F, h, h, 0, r * Fl, l, DSINF_T_DOWN, aw), &w.sdown, s);
+    w.bdown = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_DOWN_BIAS, ab), 0.f, s);
+    w.ln1g = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN1_G, SynthScale::kLnGamma), 1.f, s);
+    w.ln1b = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN1_B, SynthScale::kLnBeta), 0.f, s);
+    w.ln2g = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN2_G, SynthScale::kLnGamma), 1.f, s);
+    w.ln2b = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN2_B, SynthScale::kLnBeta), 0.f, s);
+  }
+  // LM head (tied with the embedding, fp16 in both modes): vocab parallel, padded rows are 0
+  {
+    const ops::ShardMap lm = make_map(m, m.Vl, h, m.Vpad, h, m.Vl, m.Vpad, r * m.Vl, 0, -1, DSINF_T_WTE, aw, m.V);
+    const int64_t words = (h + 1) / 2 * m.Vl;
+    sh.wlm = m.alloc_n<uint32_t>(words);
+    m.weight_bytes += words * 4;
+    ops::init_packed_f16(lm, sh.wlm, s);
+  }
+  sh.lnfg = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, -1, DSINF_T_LNF_G, SynthScale::kLnGamma), 1.f, s);
+  sh.lnfb = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, -1, DSINF_T_LNF_B, SynthScale::kLnBeta), 0.f, s);
+  if (r == 0 || m.rt.tp_mode == DSINF_TP_NCCL) {
+    sh.wte = m.alloc_n<__half>(m.V * h);
+    ops::init_rowmajor_f16(synth_base(m.rt.seed, -1, DSINF_T_WTE), aw, m.V, h, sh.wte, s);
+  } else {
+    sh.wte = m.shards[0].wte;
+  }
+  const int B = m.B;
+  sh.res[0] = m.alloc_n<float>(B * h);
+  sh.res[1] = m.alloc_n<float>(B * h);
+  sh.d_attn = m.alloc_n<float>(B * h);
+  sh.d_mlp = m.alloc_n<float>(B * h);
+  sh.q = m.alloc_n<__half>(B * Hl * d);
+  sh.a = m.alloc_n<__half>(B * Hl * d);
+  sh.u = m.alloc_n<__half>(B * Fl);
+  sh.logits = m.alloc_n<float>(B * m.Vl);
+  const int64_t kv = m.L * B * Hl * static_cast<int64_t>(m.max_ctx) * d;
+  sh.kc = m.alloc_n<__half>(kv);
+  sh.vc = m.alloc_n<__half>(kv);
+  DSINF_CUDA_CHECK(cudaMemsetAsync(sh.kc, 0, kv * 2, s));
+  DSINF_CUDA_CHECK(cudaMemsetAsync(sh.vc, 0, kv * 2, s));
+  DSINF_CUDA_CHECK(cudaMemsetAsync(sh.d_mlp, 0, B * h * 4, s));
+  const bool i8 = m.int8;
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0);
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0);
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0);
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0);
+  sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0);
+}
+
+gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w) {
+  gemm::Params p{};
+  p.rows = int8_w ? (K + 3) / 4 : (K + 1) / 2;
+  p.w = w;
+  p.w_scale = ws;
+  p.N = N;
+  p.K = K;
+  p.B = m.B;
+  p.ln_eps = m.rt.ln_eps;
+  p.out_ld = N;
+  return p;
+}
+
+struct Enqueuer {
+  Model& m;
+  cudaStream_t s;
+  bool pdl;
+  int64_t launches = 0;
+
+  void gemm_launch(const gemm::Params& p, const gemm::Plan& plan, bool int8_w) {
+    gemm::launch(p, plan, int8_w, s, pdl);
+    ++launches;
+  }
+
+  void k1_qkv(Shard& sh, int l) {
+    const LayerW& w = sh.layers[l];
+    const int N = static_cast<int>(3 * m.Hl * m.d);
+    gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8);
+    p.pro = gemm::PRO_LN;
+    p.res_in = sh.res[0];
+    p.res_delta = l > 0 ? sh.d_mlp : nullptr;
+    p.delta_bias = l > 0 ? sh.layers[l - 1].bdown : nullptr;
+    p.res_out = sh.res[1];
+    p.ln_g = w.ln1g;
+    p.ln_b = w.ln1b;
+    p.epi = gemm::EPI_QKV;
+    p.bias = w.bqkv;
+    p.q_out = sh.q;
+    const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+    p.k_cache = sh.kc + l * layer_kv;
+    p.v_cache = sh.vc + l * layer_kv;
+    p.rope = m.rope;
+    p.pos = m.pos;
+    p.heads = static_cast<int>(m.Hl);
+    p.head_dim = static_cast<int>(m.d);
+    p.max_seq = m.max_ctx;
+    gemm_launch(p, sh.plan_qkv, m.int8);
+  }
+
+  void k2_attn(Shard& sh, int l) {
+    ops::AttnParams a{};
+    const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+    a.q = sh.q;
+    a.kc = sh.kc + l * layer_kv;
+    a.vc = sh.vc + l * layer_kv;
+    a.pos = m.pos;
+    a.out = sh.a;
+    a.B = m.B;
+    a.H = static_cast<int>(m.Hl);
+    a.d = static_cast<int>(m.d);
+    a.max_seq = m.max_ctx;
+    a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+    ops::attention(a, m.attn_chunks, s, pdl);
+    ++launches;
+  }
+
+  void k3_attn_out(Shard& sh, int l) {
+    const LayerW& w = sh.layers[l];
+    gemm::Params p = base_params(m, w.wo, w.so, static_cast<int>(m.h), static_cast<int>(m.Hl * m.d), m.int8);
+    p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.x = sh.a;
+    p.x_ld = static_cast<int>(m.Hl * m.d);
+    p.epi = gemm::EPI_F32;
+    p.out = sh.d_attn;
+    gemm_launch(p, sh.plan_o, m.int8);
+  }
+
+  void k4_up(Shard& sh, int l) {
+    const LayerW& w = sh.layers[l];
+    gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
+    p.pro = gemm::PRO_LN;
+    p.res_in = sh.res[1];
+    p.res_delta = sh.d_attn;
+    p.delta_bias = w.bo;
+    p.res_out = sh.res[0];
+    p.ln_g = w.ln2g;
+    p.ln_b = w.ln2b;
+    p.epi = gemm::EPI_GELU_F16;
+    p.bias = w.bup;
+    p.out = sh.u;
+    gemm_launch(p, sh.plan_up, m.int8);
+  }
+
+  void k5_down(Shard& sh, int l) {
+    const LayerW& w = sh.layers[l];
+    gemm::Params p = base_params(m, w.wdown, w.sdown, static_cast<int>(m.h), static_cast<int>(m.Fl), m.int8);
+    p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.x = sh.u;
+    p.x_ld = static_cast<int>(m.Fl);
+    p.epi = gemm::EPI_F32;
+    p.out = sh.d_mlp;
+    gemm_launch(p, sh.plan_down, m.int8);
+  }
+
+  void lm_head(Shard& sh) {
+    gemm::Params p = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), static_cast<int>(m.h), false);
+    p.pro = gemm::PRO_LN;
+    p.res_in = sh.res[0];
+    p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
+    p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
+    p.res_out = nullptr;
+    p.ln_g = sh.lnfg;
+    p.ln_b = sh.lnfb;
+    p.epi = gemm::EPI_F32;
+    p.out = sh.logits;
+    gemm_launch(p, sh.plan_lm, false);
+    ops::ArgmaxParams ap{};
+    ap.logits = sh.logits;
+    ap.ld = static_cast<int>(m.Vl);
+    const int64_t first = sh.rank * m.Vl;
+    ap.valid = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(m.Vl, m.V - first)));
+    ap.B = m.B;
+    ap.idx_offset = first;
+    ap.out_val = m.am_val + sh.rank * m.B;
+    ap.out_idx = m.am_idx + sh.rank * m.B;
+    ops::argmax(ap, s, pdl);
+    ++launches;
+  }
+
+  // Sum of the t partials of `which` (0 = d_attn, 1 = d_mlp).
+  void allreduce(int which) {
+    if (m.t == 1) return;
+    const int64_t count = static_cast<int64_t>(m.B) * m.h;
+    if (m.rt.tp_mode == DSINF_TP_NCCL) {
+      Shard& sh = m.shards[0];
+      nccl::allreduce_sum_f32(which == 0 ? sh.d_attn : sh.d_mlp, count, m.comm, s);
+    } else {
+      ops::LocalReduceParams p{};
+      p.shards = m.t;
+      p.count = count;
+      for (int i = 0; i < m.t; ++i) p.buf[i] = which == 0 ? m.shards[i].d_attn : m.shards[i].d_mlp;
+      ops::local_allreduce(p, s, pdl);
+      ++launches;
+    }
+  }
+
+  void step() {
+    for (Shard& sh : m.shards) {
+      ops::EmbedParams e{};
+      e.wte = sh.wte;
+      e.prompt = m.prompt;
+      e.prompt_len = m.prompt_len;
+      e.prompt_ld = m.prompt_cap;
+      e.next_tok = m.next_tok;
+      e.pos = m.pos;
+      e.hist = m.hist;
+      e.max_ctx = m.max_ctx;
+      e.res = sh.res[0];
+      e.B = m.B;
+      e.h = static_cast<int>(m.h);
+      e.V = static_cast<int>(m.V);
+      ops::embed(e, s, pdl);
+      ++launches;
+    }
+    for (int l = 0; l < m.L; ++l) {
+      for (Shard& sh : m.shards) {
+        k1_qkv(sh, l);
+        k2_attn(sh, l);
+        k3_attn_out(sh, l);
+      }
+      allreduce(0);
+      for (Shard& sh : m.shards) {
+        k4_up(sh, l);
+        k5_down(sh, l);
+      }
+      allreduce(1);
+    }
+    for (Shard& sh : m.shards) lm_head(sh);
+    if (m.t > 1 && m.rt.tp_mode == DSINF_TP_NCCL) {
+      // gather every rank's (value, index) pair; slots are laid out [rank][B]
+      nccl::allgather_bytes(m.am_val + m.shards[0].rank * m.B, m.am_val, m.B * sizeof(float), m.comm, s);
+      nccl::allgather_bytes(m.am_idx + m.shards[0].rank * m.B, m.am_idx, m.B * sizeof(int32_t), m.comm, s);
+    }
+    ops::SelectParams sp{};
+    sp.vals = m.am_val;
+    sp.idxs = m.am_idx;
+    sp.shards = m.t;
+    sp.B = m.B;
+    sp.next_tok = m.next_tok;
+    sp.pos = m.pos;
+    sp.hist = m.hist;
+    sp.max_ctx = m.max_ctx;
+    ops::select_token(sp, s, pdl);
+    ++launches;
+  }
+};
+
+void validate_configs(const dsinf_model_config& c, const dsinf_runtime_config& r) {
+  require(c.hidden_dim > 0 && c.num_layers >= 0 && c.num_heads > 0 && c.vocab_size > 0, "bad model dims");
+  require(c.hidden_dim % c.num_heads == 0, "hidden_dim must be divisible by num_heads");
+  require(c.dtype_bytes == 1 || c.dtype_bytes == 2, "dtype_bytes must be 2 (fp16) or 1 (int8)");
+  require(r.batch >= 1 && r.batch <= gemm::kMaxB, "batch must be in [1, 16]");
+  require(r.tp_size >= 1 && r.tp_size <= 8, "tp_size must be in [1, 8]");
+  require(c.num_heads % r.tp_size == 0, "num_heads must be divisible by tp_size");
+  require((4 * c.hidden_dim) % r.tp_size == 0, "4*hidden must be divisible by tp_size");
+  require(c.hidden_dim % 8 == 0, "hidden_dim must be a multiple of 8");
+  require((c.hidden_dim / c.num_heads) % 2 == 0, "head dim must be even (rotary pairs)");
+  require(r.max_ctx >= 1 && r.max_ctx <= c.max_seq, "max_ctx must be in [1, max_seq]");
+  if (r.tp_size > 1) require(r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_LOCAL, "tp_size > 1 needs a TP mode");
+  if (r.tp_mode == DSINF_TP_NCCL) require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
+}
+
+void build_rope(Model& m, cudaStream_t s) {
+  const int64_t half = m.d / 2;
+  std::vector<float2> tab(static_cast<size_t>(m.max_ctx) * half);
+  for (int64_t p = 0; p < m.max_ctx; ++p)
+    for (int64_t i = 0; i < half; ++i) {
+      const double inv = std::pow(static_cast<double>(m.rt.rope_base), -2.0 * static_cast<double>(i) / static_cast<double>(m.d));
+      const double ang = static_cast<double>(p) * inv;
+      tab[p * half + i] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+  m.rope = m.alloc_n<float2>(tab.size());
+  DSINF_CUDA_CHECK(cudaMemcpyAsync(m.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, s));
+}
+
+void enqueue_eager(Model& m, cudaStream_t s) {
+  Enqueuer e{m, s, m.rt.use_pdl != 0};
+  e.step();
+  m.kernels_per_step = e.launches;
+}
+
+void ensure_graph(Model& m) {
+  if (m.exec) return;
+  DSINF_CUDA_CHECK(cudaStreamBeginCapture(m.cap_stream, cudaStreamCaptureModeThreadLocal));
+  Enqueuer e{m, m.cap_stream, m.rt.use_pdl != 0};
+  try {
+    e.step();
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(m.cap_stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  DSINF_CUDA_CHECK(cudaStreamEndCapture(m.cap_stream, &m.graph));
+  DSINF_CUDA_CHECK(cudaGraphInstantiate(&m.exec, m.graph, 0));
+  m.kernels_per_step = e.launches;
+}
+
+}  // namespace
+}  // namespace dsinf
+
+using namespace dsinf;
+
+extern "C" {
+
+int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config* rt, void* nccl_comm,
+                       dsinf_model** out) {
+  return guarded([&] {
+    require(cfg && rt && out, "null argument");
+    validate_configs(*cfg, *rt);
+    auto m = std::make_unique<dsinf_model>();
+    m->cfg = *cfg;
+    m->rt = *rt;
+    if (m->rt.ln_eps <= 0.f) m->rt.ln_eps = 1e-5f;
+    if (m->rt.rope_base <= 0.f) m->rt.rope_base = 10000.f;
+    DSINF_CUDA_CHECK(cudaSetDevice(rt->device));
+    gemm::configure();
+    ops::configure();
+    m->h = cfg->hidden_dim;
+    m->L = cfg->num_layers;
+    m->H = cfg->num_heads;
+    m->d = m->h / m->H;
+    m->t = rt->tp_size;
+    m->Hl = m->H / m->t;
+    m->V = cfg->vocab_size;
+    const int64_t vq = 128LL * m->t;
+    m->Vpad = (m->V + vq - 1) / vq * vq;
+    m->Vl = m->Vpad / m->t;
+    m->F = 4 * m->h;
+    m->Fl = m->F / m->t;
+    m->B = rt->batch;
+    m->max_ctx = static_cast<int>(rt->max_ctx);
+    m->int8 = cfg->dtype_bytes == 1;
+    m->attn_chunks = ops::attention_chunks(m->B, static_cast<int>(m->Hl));
+    if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
+      require(nccl_comm != nullptr, "NCCL mode needs a communicator");
+      m->comm = static_cast<nccl::Comm>(nccl_comm);
+    }
+    DSINF_CUDA_CHECK(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t s = m->cap_stream;
+    const int nshards = (rt->tp_mode == DSINF_TP_LOCAL) ? m->t : 1;
+    m->shards.resize(nshards);
+    for (int i = 0; i < nshards; ++i) m->shards[i].rank = (rt->tp_mode == DSINF_TP_NCCL) ? rt->tp_rank : i;
+    build_rope(*m, s);
+    m->prompt_cap = m->max_ctx;
+    m->prompt = m->alloc_n<int32_t>(static_cast<int64_t>(m->B) * m->prompt_cap);
+    m->next_tok = m->alloc_n<int32_t>(m->B);
+    m->hist = m->alloc_n<int32_t>(static_cast<int64_t>(m->B) * m->max_ctx);
+    m->pos = m->alloc_n<int>(1);
+    m->am_val = m->alloc_n<float>(static_cast<int64_t>(m->t) * m->B);
+    m->am_idx = m->alloc_n<int32_t>(static_cast<int64_t>(m->t) * m->B);
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m->prompt, 0, sizeof(int32_t) * m->B * m->prompt_cap, s));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m->next_tok, 0, sizeof(int32_t) * m->B, s));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m->hist, 0, sizeof(int32_t) * m->B * m->max_ctx, s));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m->pos, 0, sizeof(int), s));
+    for (auto& sh : m->shards) build_shard(*m, sh, s);
+    DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+    *out = m.release();
+  });
+}
+
+int dsinf_model_destroy(dsinf_model* m) {
+  return guarded([&] { delete m; });
+}
+
+static void set_prompt_common(dsinf_model* m, const int32_t* src, int64_t prompt_len, bool host, cudaStream_t s) {
+  require(m != nullptr, "null model");
+  require(prompt_len >= 0 && prompt_len <= m->prompt_cap, "prompt_len exceeds the KV-cache capacity");
+  const size_t bytes = sizeof(int32_t) * m->B * prompt_len;
+  if (prompt_len > 0) {
+    require(src != nullptr, "null prompt");
+    DSINF_CUDA_CHECK(cudaMemcpy2DAsync(m->prompt, sizeof(int32_t) * m->prompt_cap, src, sizeof(int32_t) * prompt_len,
+                                       sizeof(int32_t) * prompt_len, m->B,
+                                       host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  }
+  (void)bytes;
+  m->prompt_len = static_cast<int>(prompt_len);
+  DSINF_CUDA_CHECK(cudaMemsetAsync(m->pos, 0, sizeof(int), s));
+  DSINF_CUDA_CHECK(cudaMemsetAsync(m->next_tok, 0, sizeof(int32_t) * m->B, s));
+  m->host_pos = 0;
+  // prompt_len is a kernel argument: re-capture the step graph
+  if (m->exec) {
+    cudaGraphExecDestroy(m->exec);
+    m->exec = nullptr;
+  }
+  if (m->graph) {
+    cudaGraphDestroy(m->graph);
+    m->graph = nullptr;
+  }
+}
+
+int dsinf_model_set_prompt(dsinf_model* m, const int32_t* prompt_host, int64_t prompt_len, void* stream) {
+  return guarded([&] { set_prompt_common(m, prompt_host, prompt_len, true, static_cast<cudaStream_t>(stream)); });
+}
+
+int dsinf_model_set_prompt_device(dsinf_model* m, const int32_t* prompt_dev, int64_t prompt_len, void* stream) {
+  return guarded([&] { set_prompt_common(m, prompt_dev, prompt_len, false, static_cast<cudaStream_t>(stream)); });
+}
+
+int dsinf_decode_step(dsinf_model* m, void* stream) { return dsinf_decode_steps(m, 1, stream); }
+
+int dsinf_decode_steps(dsinf_model* m, int64_t steps, void* stream) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    require(steps >= 0, "negative step count");
+    if (m->host_pos + steps > m->max_ctx)
+      throw InfeasibleError("decode would run past the KV-cache capacity (max_ctx)");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m->rt.use_cuda_graph) {
+      ensure_graph(*m);
+      for (int64_t i = 0; i < steps; ++i) DSINF_CUDA_CHECK(cudaGraphLaunch(m->exec, s));
+    } else {
+      for (int64_t i = 0; i < steps; ++i) enqueue_eager(*m, s);
+    }
+    m->host_pos += steps;
+  });
+}
+
+int dsinf_decode_step_host(dsinf_model* m, const int32_t* tokens_in, int32_t* tokens_out, void* stream) {
+  return guarded([&] {
+    require(m && tokens_in && tokens_out, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DSINF_CUDA_CHECK(cudaMemcpyAsync(m->next_tok, tokens_in, sizeof(int32_t) * m->B, cudaMemcpyHostToDevice, s));
+    const int rc = dsinf_decode_steps(m, 1, stream);
+    if (rc == DSINF_ERR_INFEASIBLE) throw InfeasibleError(dsinf_last_error());
+    if (rc == DSINF_ERR_CONFIG) throw ConfigError(dsinf_last_error());
+    if (rc != DSINF_OK) throw CudaError(dsinf_last_error());
+    DSINF_CUDA_CHECK(cudaMemcpyAsync(tokens_out, m->next_tok, sizeof(int32_t) * m->B, cudaMemcpyDeviceToHost, s));
+    DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int dsinf_model_outputs(dsinf_model* m, float** logits, int64_t* logits_ld, int32_t** next_tokens, int32_t** history,
+                        int32_t** pos) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    if (logits) *logits = m->shards[0].logits;
+    if (logits_ld) *logits_ld = m->Vl;
+    if (next_tokens) *next_tokens = m->next_tok;
+    if (history) *history = m->hist;
+    if (pos) *pos = m->pos;
+  });
+}
+
+int dsinf_model_read_logits(dsinf_model* m, float* host, int64_t len, void* stream) {
+  return guarded([&] {
+    require(m && host, "null argument");
+    const int64_t per = static_cast<int64_t>(m->B) * m->Vl;
+    require(len == per * static_cast<int64_t>(m->shards.size()), "logits buffer must be shards*B*vocab_local");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (size_t i = 0; i < m->shards.size(); ++i)
+      DSINF_CUDA_CHECK(cudaMemcpyAsync(host + i * per, m->shards[i].logits, per * 4, cudaMemcpyDeviceToHost, s));
+    DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int dsinf_model_read_tokens(dsinf_model* m, int32_t* next_host, int32_t* history_host, int64_t history_len,
+                            void* stream) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (next_host) DSINF_CUDA_CHECK(cudaMemcpyAsync(next_host, m->next_tok, 4 * m->B, cudaMemcpyDeviceToHost, s));
+    if (history_host) {
+      require(history_len == static_cast<int64_t>(m->B) * m->max_ctx, "history buffer must be B*max_ctx");
+      DSINF_CUDA_CHECK(cudaMemcpyAsync(history_host, m->hist, 4 * history_len, cudaMemcpyDeviceToHost, s));
+    }
+    DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int64_t dsinf_model_bytes_per_step(const dsinf_model* m, int64_t pos) {
+  if (!m) return -1;
+  const int64_t ctx = pos + 1;
+  const int64_t kv_read = 2LL * m->B * ctx * m->Hl * m->d * 2;
+  const int64_t kv_write = 2LL * m->B * m->Hl * m->d * 2;
+  const int64_t per_shard = m->weight_bytes / static_cast<int64_t>(m->shards.size()) + m->L * (kv_read + kv_write) +
+                            static_cast<int64_t>(m->B) * m->h * 2;
+  return per_shard * static_cast<int64_t>(m->shards.size());
+}
+
+int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out) {
+  return guarded([&] {
+    require(m && out, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->weight_bytes = m->weight_bytes;
+    out->bytes_per_token = dsinf_model_bytes_per_step(m, m->host_pos);
+    out->kernels_per_step = m->kernels_per_step;
+    out->vocab_local = m->Vl;
+    out->heads_local = m->Hl;
+    out->kv_bytes = 2LL * m->L * m->B * m->Hl * m->max_ctx * m->d * 2 * static_cast<int64_t>(m->shards.size());
+    out->shards = static_cast<int32_t>(m->shards.size());
+    out->graph_ready = m->exec != nullptr;
+  });
+}
+
+int dsinf_synthetic_tensor(uint64_t seed, int32_t layer, int32_t tensor, int64_t rows, int64_t cols,
+                           float* out) {
+  return guarded([&] {
+    require(out != nullptr && rows >= 0 && cols >= 0, "bad arguments");
+    float amp = SynthScale::kWeight, offset = 0.f;
+    switch (tensor) {
+      case DSINF_T_QKV_BIAS:
+      case DSINF_T_O_BIAS:
+      case DSINF_T_UP_BIAS:
+      case DSINF_T_DOWN_BIAS: amp = SynthScale::kBias; break;
+      case DSINF_T_LN1_G:
+      case DSINF_T_LN2_G:
+      case DSINF_T_LNF_G: amp = SynthScale::kLnGamma; offset = 1.f; break;
+      case DSINF_T_LN1_B:
+      case DSINF_T_LN2_B:
+      case DSINF_T_LNF_B: amp = SynthScale::kLnBeta; break;
+      default: break;
+    }
+    const uint64_t base = synth_base(seed, layer, tensor);
+    for (int64_t i = 0; i < rows * cols; ++i) {
+      const float v = offset + synth_unit(base, static_cast<uint64_t>(i)) * amp;
+      out[i] = f16_bits_to_f32(f32_to_f16_bits(v));
+    }
+  });
+}
+
+int dsinf_nccl_get_unique_id(uint8_t id_out[128]) {
+  return guarded([&] {
+    require(id_out != nullptr, "null id");
+    nccl::UniqueId id;
+    nccl::get_unique_id(&id);
+    std::memcpy(id_out, id.internal, 128);
+  });
+}
+
+int dsinf_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, void** comm_out) {
+  return guarded([&] {
+    require(id && comm_out, "null argument");
+    DSINF_CUDA_CHECK(cudaSetDevice(device));
+    nccl::UniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    *comm_out = nccl::init_rank(nranks, uid, rank);
+  });
+}
+
+int dsinf_nccl_comm_destroy(void* comm) {
+  return guarded([&] { nccl::destroy(static_cast<nccl::Comm>(comm)); });
+}
+
+}  // extern "C"

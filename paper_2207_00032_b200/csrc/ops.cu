@@ -1,0 +1,451 @@
+// Non-GEMM device operators: synthetic weight init / packing / quantisation, decode
+// attention over the KV cache, embedding, greedy argmax and the single-device shard reduce.
+#include <cfloat>
+#include <cmath>
+
+#include "common.h"
+#include "ops.cuh"
+#include "ptx.cuh"
+#include "synth.h"
+
+namespace dsinf {
+namespace ops {
+
+namespace {
+
+inline int blocks_for(int64_t n, int threads, int cap = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<int>(b);
+}
+
+__device__ __forceinline__ int64_t global_row(const ShardMap& m, int64_t n) {
+  return (n / m.sec_local) * m.sec_global + m.row_off + (n % m.sec_local);
+}
+
+__device__ __forceinline__ float synth_value(const ShardMap& m, int64_t grow, int64_t gcol) {
+  if (grow >= m.valid_rows || gcol >= m.K_global) return 0.0f;
+  const float w = __fmul_rn(synth_unit(m.base, static_cast<uint64_t>(grow * m.K_global + gcol)), m.amp);
+  return __half2float(__float2half_rn(w));
+}
+
+__global__ void init_packed_f16_kernel(ShardMap m, uint32_t* packed) {
+  const int64_t rows = (m.K_local + 1) / 2;
+  const int64_t total = rows * m.N_local;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / m.N_local, n = i - r * m.N_local;
+    const int64_t grow = global_row(m, n);
+    const int64_t k = 2 * r;
+    const float v0 = synth_value(m, grow, m.col_off + k);
+    const float v1 = (k + 1 < m.K_local) ? synth_value(m, grow, m.col_off + k + 1) : 0.0f;
+    const __half2 h = __floats2half2_rn(v0, v1);
+    packed[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+
+// int8 row scale over the FULL global row (TP-invariant quantisation).
+__global__ void init_row_scale_kernel(ShardMap m, float* scales) {
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t n = blockIdx.x * warps + (threadIdx.x >> 5); n < m.N_local; n += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t grow = global_row(m, n);
+    float mx = 0.f;
+    for (int64_t k = lane; k < m.K_global; k += 32) mx = fmaxf(mx, fabsf(synth_value(m, grow, k)));
+    mx = ptx::warp_max(mx);
+    if (lane == 0) scales[n] = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+  }
+}
+
+__device__ __forceinline__ uint32_t q8(float x, float scale) {
+  int q = __float2int_rn(__fdiv_rn(x, scale));
+  q = max(-127, min(127, q));
+  return static_cast<uint32_t>(q) & 0xffu;
+}
+
+__global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t* packed) {
+  const int64_t rows = (m.K_local + 3) / 4;
+  const int64_t total = rows * m.N_local;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / m.N_local, n = i - r * m.N_local;
+    const int64_t grow = global_row(m, n);
+    const float s = scales[n];
+    uint32_t word = 0;
+    for (int e = 0; e < 4; ++e) {
+      const int64_t k = 4 * r + e;
+      if (k < m.K_local) word |= q8(synth_value(m, grow, m.col_off + k), s) << (8 * e);
+    }
+    packed[i] = word;
+  }
+}
+
+__global__ void init_vector_kernel(ShardMap m, float offset, __half* out) {
+  for (int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; n < m.N_local;
+       n += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t grow = global_row(m, n);
+    float v = 0.f;
+    if (grow < m.valid_rows) v = __fadd_rn(offset, __fmul_rn(synth_unit(m.base, static_cast<uint64_t>(grow)), m.amp));
+    out[n] = __float2half_rn(v);
+  }
+}
+
+__global__ void init_rowmajor_kernel(uint64_t base, float amp, int64_t total, __half* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2half_rn(__fmul_rn(synth_unit(base, static_cast<uint64_t>(i)), amp));
+}
+
+__global__ void pack_f16_kernel(const void* w, bool src_f32, int64_t N, int64_t K, int M, __half* out) {
+  const int64_t rows = (K + M - 1) / M;
+  const int64_t total = rows * N * M;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (N * M);
+    const int64_t rem = i - r * N * M;
+    const int64_t n = rem / M;
+    const int64_t k = r * M + (rem - n * M);
+    __half v = __float2half(0.f);
+    if (k < K) {
+      if (src_f32)
+        v = __float2half_rn(static_cast<const float*>(w)[n * K + k]);
+      else
+        v = static_cast<const __half*>(w)[n * K + k];
+    }
+    out[i] = v;
+  }
+}
+
+__global__ void row_maxabs_scale_kernel(const __half* w, int64_t N, int64_t K, float* scales) {
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t n = blockIdx.x * warps + (threadIdx.x >> 5); n < N; n += static_cast<int64_t>(gridDim.x) * warps) {
+    float mx = 0.f;
+    for (int64_t k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(__half2float(w[n * K + k])));
+    mx = ptx::warp_max(mx);
+    if (lane == 0) scales[n] = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+  }
+}
+
+__global__ void quant_pack_i8_kernel(const __half* w, int64_t N, int64_t K, const float* scales, uint32_t* packed) {
+  const int64_t rows = (K + 3) / 4;
+  const int64_t total = rows * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / N, n = i - r * N;
+    uint32_t word = 0;
+    for (int e = 0; e < 4; ++e) {
+      const int64_t k = 4 * r + e;
+      if (k < K) word |= q8(__half2float(w[n * K + k]), scales[n]) << (8 * e);
+    }
+    packed[i] = word;
+  }
+}
+
+__global__ void quant_act_kernel(const __half* x, int64_t K, int8_t* q, float* scales) {
+  const int64_t b = blockIdx.x;
+  __shared__ float red[32];
+  float mx = 0.f;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(__half2float(x[b * K + k])));
+  mx = ptx::warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    v = ptx::warp_max(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float s = red[0] > 0.f ? __fdiv_rn(red[0], 127.0f) : 1.0f;
+  if (threadIdx.x == 0) scales[b] = s;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+    q[b * K + k] = static_cast<int8_t>(static_cast<int>(q8(__half2float(x[b * K + k]), s) << 24) >> 24);
+}
+
+// ---------------------------------------------------------------- attention
+constexpr int kAttnThreads = 128;
+
+__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ __align__(16) float asmem[];
+  const int d = p.d;
+  float* qf = asmem;              // [d]
+  float* of = qf + d;             // [d]
+  float* stat = of + d;           // [4]: m, l
+  float* sc = stat + 4;           // [chunk]
+  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int ctx = *p.pos + 1;
+  const int chunk = (ctx + C - 1) / C;
+  const int j0 = c * chunk;
+  const int j1 = min(ctx, j0 + chunk);
+  const int hd = p.H * d;
+  for (int i = threadIdx.x; i < d; i += kAttnThreads) qf[i] = __half2float(p.q[static_cast<size_t>(b) * hd + head * d + i]);
+  __syncthreads();
+  const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
+  const __half* kb = p.kc + kv_base;
+  const __half* vb = p.vc + kv_base;
+  // scores: one warp per position, lanes over half2 pairs of the head dim
+  for (int j = j0 + warp; j < j1; j += kAttnThreads / 32) {
+    const __half2* kr = reinterpret_cast<const __half2*>(kb + static_cast<size_t>(j) * d);
+    float acc = 0.f;
+    for (int pidx = lane; pidx < d / 2; pidx += 32) {
+      const float2 kv = __half22float2(kr[pidx]);
+      acc = fmaf(qf[2 * pidx], kv.x, acc);
+      acc = fmaf(qf[2 * pidx + 1], kv.y, acc);
+    }
+    acc = ptx::warp_sum(acc);
+    if (lane == 0) sc[j - j0] = acc * p.scale;
+  }
+  __syncthreads();
+  const int n = max(0, j1 - j0);
+  if (warp == 0) {
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, sc[j]);
+    mx = ptx::warp_max(mx);
+    float l = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float e = expf(sc[j] - mx);
+      sc[j] = e;
+      l += e;
+    }
+    l = ptx::warp_sum(l);
+    if (lane == 0) {
+      stat[0] = mx;
+      stat[1] = l;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += kAttnThreads) {
+    float acc = 0.f;
+    for (int j = 0; j < n; ++j) acc = fmaf(sc[j], __half2float(vb[static_cast<size_t>(j0 + j) * d + i]), acc);
+    of[i] = acc;
+  }
+  // combine the chunks of this (b, head) through distributed shared memory
+  if (C > 1)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
+  const uint32_t rank = c;
+  float M = -INFINITY;
+  for (int r = 0; r < C; ++r) M = fmaxf(M, ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[0], r)));
+  float L = 0.f;
+  float wts[16];
+  for (int r = 0; r < C; ++r) {
+    const float mr = ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[0], r));
+    const float lr = ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[1], r));
+    const float w = (mr == -INFINITY) ? 0.f : expf(mr - M);
+    wts[r] = w;
+    L += w * lr;
+  }
+  const float invL = 1.0f / L;
+  for (int i = rank + C * threadIdx.x; i < d; i += C * kAttnThreads) {
+    float o = 0.f;
+    for (int r = 0; r < C; ++r) o = fmaf(wts[r], ptx::ld_dsmem_f(ptx::map_shared_rank(&of[i], r)), o);
+    p.out[static_cast<size_t>(b) * hd + head * d + i] = __float2half_rn(o * invL);
+  }
+  if (C > 1) ptx::cluster_sync();
+}
+
+// ---------------------------------------------------------------- step boundary
+__global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int b = blockIdx.x;
+  const int pos = *p.pos;
+  int tok = pos < p.prompt_len ? p.prompt[static_cast<size_t>(b) * p.prompt_ld + pos] : p.next_tok[b];
+  if (tok < 0 || tok >= p.V) tok = 0;
+  if (threadIdx.x == 0 && pos < p.max_ctx) p.hist[static_cast<size_t>(b) * p.max_ctx + pos] = tok;
+  const __half* row = p.wte + static_cast<size_t>(tok) * p.h;
+  float* out = p.res + static_cast<size_t>(b) * p.h;
+  for (int k = threadIdx.x; k < p.h; k += blockDim.x) out[k] = __half2float(row[k]);
+}
+
+__global__ void argmax_kernel(const __grid_constant__ ArgmaxParams p) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int b = blockIdx.x;
+  const float* row = p.logits + static_cast<size_t>(b) * p.ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < p.valid; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) {  // strided ascending scan: first max per thread is the lowest index
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bv = sv[0];
+    int bx = si[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+      if (sv[w] > bv || (sv[w] == bv && si[w] < bx)) {
+        bv = sv[w];
+        bx = si[w];
+      }
+    p.out_val[b] = bv;
+    p.out_idx[b] = static_cast<int32_t>(bx + p.idx_offset);
+  }
+}
+
+__global__ void select_kernel(const __grid_constant__ SelectParams p) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int pos = *p.pos;
+  for (int b = threadIdx.x; b < p.B; b += blockDim.x) {
+    float bv = p.vals[b];
+    int32_t bx = p.idxs[b];
+    for (int s = 1; s < p.shards; ++s) {  // ties -> lowest vocabulary index
+      const float v = p.vals[s * p.B + b];
+      const int32_t x = p.idxs[s * p.B + b];
+      if (v > bv || (v == bv && x < bx)) {
+        bv = v;
+        bx = x;
+      }
+    }
+    p.next_tok[b] = bx;
+    if (pos + 1 < p.max_ctx) p.hist[static_cast<size_t>(b) * p.max_ctx + pos + 1] = bx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *p.pos = pos + 1;
+}
+
+__global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams p) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < p.count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = p.buf[0][i];
+    for (int s = 1; s < p.shards; ++s) acc += p.buf[s][i];
+    for (int s = 0; s < p.shards; ++s) p.buf[s][i] = acc;
+  }
+}
+
+template <class K, class P>
+void launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const P& params,
+                int cluster_z = 1) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (cluster_z > 1) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = 1;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = cluster_z;
+    ++na;
+  }
+  if (pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, params));
+}
+
+}  // namespace
+
+void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s) {
+  const int64_t total = (m.K_local + 1) / 2 * m.N_local;
+  init_packed_f16_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, packed);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s) {
+  init_row_scale_kernel<<<blocks_for(m.N_local, 8, 148 * 8), 256, 0, s>>>(m, scales);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+  const int64_t total = (m.K_local + 3) / 4 * m.N_local;
+  init_packed_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, scales, packed);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_vector_f16(const ShardMap& m, float offset, __half* out, cudaStream_t s) {
+  init_vector_kernel<<<blocks_for(m.N_local, 256), 256, 0, s>>>(m, offset, out);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_rowmajor_f16(uint64_t base, float amp, int64_t rows, int64_t cols, __half* out, cudaStream_t s) {
+  init_rowmajor_kernel<<<blocks_for(rows * cols, 256), 256, 0, s>>>(base, amp, rows * cols, out);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void pack_f16(const void* w, bool src_f32, int64_t N, int64_t K, int pack_M, __half* out, cudaStream_t s) {
+  const int64_t total = (K + pack_M - 1) / pack_M * N * pack_M;
+  pack_f16_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, src_f32, N, K, pack_M, out);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, float* scales, cudaStream_t s) {
+  row_maxabs_scale_kernel<<<blocks_for(N, 8, 148 * 8), 256, 0, s>>>(w, N, K, scales);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+  const int64_t total = (K + 3) / 4 * N;
+  quant_pack_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, N, K, scales, reinterpret_cast<uint32_t*>(packed));
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void quantize_act_i8(const __half* x, int64_t B, int64_t K, int8_t* q, float* scales, cudaStream_t s) {
+  quant_act_kernel<<<static_cast<unsigned>(B), 256, 0, s>>>(x, K, q, scales);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+int attention_chunks(int B, int H) {
+  const int pairs = B * H;
+  int c = 1;
+  while (c < 8 && pairs * c < 2 * 148) c <<= 1;
+  return c;
+}
+
+void configure() {
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl) {
+  if (p.d % 2 != 0 || p.d > 1024) throw ConfigError("attention: head dim must be even and <= 1024");
+  if (chunks < 1 || chunks > 16) throw ConfigError("attention: bad chunk count");
+  const int max_chunk = (p.max_seq + chunks - 1) / chunks;
+  const size_t smem = (2 * static_cast<size_t>(p.d) + 4 + max_chunk) * sizeof(float);
+  if (smem > 200 * 1024) throw ConfigError("attention: context too long for one chunk");
+  launch_pdl(attention_kernel, dim3(p.H, p.B, chunks), dim3(kAttnThreads), smem, s, pdl, p, chunks);
+}
+
+void embed(const EmbedParams& p, cudaStream_t s, bool pdl) {
+  launch_pdl(embed_kernel, dim3(p.B), dim3(256), 0, s, pdl, p);
+}
+
+void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl) {
+  launch_pdl(argmax_kernel, dim3(p.B), dim3(1024), 0, s, pdl, p);
+}
+
+void select_token(const SelectParams& p, cudaStream_t s, bool pdl) {
+  launch_pdl(select_kernel, dim3(1), dim3(32), 0, s, pdl, p);
+}
+
+void local_allreduce(const LocalReduceParams& p, cudaStream_t s, bool pdl) {
+  launch_pdl(local_allreduce_kernel, dim3(blocks_for(p.count, 256, 148)), dim3(256), 0, s, pdl, p);
+}
+
+}  // namespace ops
+}  // namespace dsinf

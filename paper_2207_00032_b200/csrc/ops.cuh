@@ -1,0 +1,97 @@
+// Non-GEMM device operators of the decode step and the weight-initialisation kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace dsinf {
+namespace ops {
+
+// Logical (un-sharded) position of a local weight element under Megatron TP sharding.
+//   global row = (n / sec_local) * sec_global + row_off + n % sec_local
+//   global col = col_off + k;  flat = row * K_global + col
+struct ShardMap {
+  int64_t N_local, K_local;
+  int64_t N_global, K_global;
+  int64_t sec_local, sec_global, row_off, col_off;
+  int64_t valid_rows;  // global rows >= valid_rows are zero padding (vocab)
+  uint64_t base;       // synth_base(seed, layer, tensor)
+  float amp;
+};
+
+// Synthetic weight tensor written in the reference packed layout, fp16, pack_M = 2.
+void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s);
+// Same tensor quantised per global output row to int8 (pack_M = 4) + fp32 row scales.
+void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s);
+// 1-D tensor (bias / LN) of length n_local: value = offset + unit(flat = row(n)) * amp.
+void init_vector_f16(const ShardMap& m, float offset, __half* out, cudaStream_t s);
+// Row-major fp16 [rows][cols] (replicated embedding table).
+void init_rowmajor_f16(uint64_t base, float amp, int64_t rows, int64_t cols, __half* out, cudaStream_t s);
+
+// pack_weights on device (gemm.hpp:113-130): row-major [N][K] -> [ceil(K/M)][N][M] fp16.
+void pack_f16(const void* w, bool src_f32, int64_t N, int64_t K, int pack_M, __half* out, cudaStream_t s);
+// Per-row int8 quantisation of a row-major fp16 matrix into the packed M=4 layout.
+void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, float* scales, cudaStream_t s);
+// Per-token int8 quantisation of activations [B][K] (same formula as the GEMM prologue).
+void quantize_act_i8(const __half* x, int64_t B, int64_t K, int8_t* q, float* scales, cudaStream_t s);
+
+// Decode attention (paper region 2): split over ctx chunks inside a cluster of `chunks` CTAs.
+struct AttnParams {
+  const __half* q;        // [B][H*d]
+  const __half* kc;       // [B][H][max_seq][d]
+  const __half* vc;
+  const int* pos;         // attend to positions 0..*pos
+  __half* out;            // [B][H*d]
+  int B, H, d, max_seq;
+  float scale;
+};
+int attention_chunks(int B, int H);
+// Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
+void configure();
+void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl);
+
+// Step-boundary kernels.
+struct EmbedParams {
+  const __half* wte;      // [V][h]
+  const int32_t* prompt;  // [B][prompt_ld]
+  int prompt_len, prompt_ld;
+  const int32_t* next_tok;  // [B]
+  const int* pos;
+  int32_t* hist;          // [B][max_ctx]
+  int max_ctx;
+  float* res;             // [B][h]
+  int B, h, V;
+};
+void embed(const EmbedParams& p, cudaStream_t s, bool pdl);
+
+struct ArgmaxParams {
+  const float* logits;  // [B][ld]
+  int ld, valid, B;
+  int64_t idx_offset;   // global vocab index of local column 0
+  float* out_val;       // [B]
+  int32_t* out_idx;     // [B]
+};
+void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl);
+
+struct SelectParams {
+  const float* vals;     // [shards][B] (row stride B)
+  const int32_t* idxs;   // [shards][B]
+  int shards, B;
+  int32_t* next_tok;
+  int* pos;
+  int32_t* hist;
+  int max_ctx;
+};
+void select_token(const SelectParams& p, cudaStream_t s, bool pdl);
+
+// Sum of `n` shard buffers (in shard order), written back to every shard buffer.
+struct LocalReduceParams {
+  float* buf[8];
+  int shards;
+  int64_t count;
+};
+void local_allreduce(const LocalReduceParams& p, cudaStream_t s, bool pdl);
+
+}  // namespace ops
+}  // namespace dsinf

@@ -1,0 +1,87 @@
+// SBI-GeMM for sm_100a: the skinny decode GEMM (infersim gemm.hpp:147-202)
+// with Deep-Fusion prologues (LayerNorm / residual add / activation quantisation) and
+// epilogues (bias, GeLU, RoPE + KV-cache append, INT8 dequant).
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace dsinf {
+namespace gemm {
+
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kColTile = 128;                    // output columns per CTA
+constexpr int kRowsPerStage = 32;                // packed rows per pipeline stage
+constexpr int kRowWords = kColTile + 8;          // 136 words: conflict-free fragment reads
+constexpr int kStageWords = kRowsPerStage * kRowWords;
+constexpr int kMaxStages = 8;
+constexpr int kMaxB = 16;                        // batch rows per launch
+constexpr int kPartLd = kColTile + 4;            // split-K partial row stride (floats)
+constexpr int kHeaderBytes = 1024;               // barriers + per-row scalars
+
+enum Prologue : int {
+  PRO_F16 = 0,    // x fp16 [B][x_ld] from global
+  PRO_I8 = 1,     // x int8 [B][x_ld] + scales from global (already quantised)
+  PRO_LN = 2,     // LayerNorm of (res_in [+ res_delta + delta_bias]) -> fp16 (or int8)
+  PRO_QUANT = 3,  // x fp16 from global, per-token int8 quantisation on the fly
+};
+
+enum Epilogue : int {
+  EPI_F32 = 0,       // out fp32 = y (+ bias)
+  EPI_F16 = 1,       // out fp16 = y (+ bias)
+  EPI_GELU_F16 = 2,  // out fp16 = gelu(y + bias)
+  EPI_QKV = 3,       // q/k/v = y + bias, RoPE on q,k, q -> q_out, k/v -> KV cache at pos
+};
+
+struct Params {
+  // packed weights: word (row r, column n) at w[r * N + n]; a word holds pack_M k-values
+  const uint32_t* w;
+  const float* w_scale;  // int8: per-output-row scale [N]
+  int N, rows, K, B;
+  int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
+  int stages;
+  int x_row_words;       // smem stride of one x row (== 4 mod 32)
+  int aligned;           // N % 4 == 0 (bulk copies) else synchronous staging
+  // prologue
+  int pro;
+  const void* x;
+  int x_ld;
+  const float* x_scale;
+  const float* res_in;
+  const float* res_delta;
+  const __half* delta_bias;
+  float* res_out;
+  const __half* ln_g;
+  const __half* ln_b;
+  float ln_eps;
+  // epilogue
+  int epi;
+  const __half* bias;
+  void* out;
+  int out_ld;
+  __half* q_out;      // [B][heads*head_dim]
+  __half* k_cache;    // [B][heads][max_seq][head_dim] (this layer)
+  __half* v_cache;
+  const float2* rope;  // [max_seq][head_dim/2] (cos, sin)
+  const int* pos;
+  int heads, head_dim, max_seq;
+};
+
+struct Plan {
+  int col_tiles;
+  int ksplit;
+  int rows_per_split;
+  int stages;
+  int nb8;
+  size_t smem_bytes;
+};
+
+// Sets kernel attributes for every instantiation; call before graph capture.
+void configure();
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split);
+void launch(const Params& p, const Plan& plan, bool int8_weights, cudaStream_t stream, bool pdl);
+
+}  // namespace gemm
+}  // namespace dsinf

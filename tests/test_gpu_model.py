@@ -1,0 +1,113 @@
+"""End-to-end decode parity: the B200 model (through the C ABI) against the CPU oracle on identical
+synthetic weights and prompts.
+
+Stated tolerances (fp16 weights, fp32 accumulation, fp16 activations at the storage points):
+  max |logit_gpu - logit_oracle| <= 0.03 * std(logits) + 0.01   (fp16 path)
+  max |logit_gpu - logit_oracle| <= 0.06 * std(logits) + 0.02   (int8 W8A8 path)
+Greedy token ids must be identical whenever the oracle's top-1/top-2 margin exceeds the logit
+tolerance (the margins are printed); the oracle is always fed the same tokens as the GPU.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2207_00032_b200 import _capi as capi  # noqa: E402
+from paper_2207_00032_b200.engine import DecoderModel  # noqa: E402
+
+SEED = 20220701
+
+
+def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, prompt_len=6, gen=4,
+               use_graph=True, use_pdl=True, max_ctx=32):
+    tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
+    rng = np.random.default_rng(hidden + layers + batch)
+    prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
+    mode = capi.TP_LOCAL if tp > 1 else capi.TP_NONE
+    gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx,
+                       tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED)
+    ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=batch, max_ctx=max_ctx,
+                        seed=SEED)
+    gpu.set_prompt(prompt)
+    worst = 0.0
+    margins = []
+    for pos in range(prompt_len + gen - 1):
+        gpu.step(1)
+        torch.cuda.synchronize()
+        lg = gpu.full_logits()
+        nxt, hist = gpu.read_tokens()
+        tokens = hist[:, pos]
+        ol, onext = ora.step(tokens, pos)
+        tol = tol_rel * float(ol.std()) + tol_abs
+        err = float(np.abs(lg - ol).max())
+        worst = max(worst, err / tol)
+        assert err <= tol, f"pos {pos}: max|dlogit| {err:.4g} > tol {tol:.4g}"
+        srt = np.sort(ol, axis=1)
+        margin = srt[:, -1] - srt[:, -2]
+        margins.extend(margin.tolist())
+        for b in range(batch):
+            if margin[b] > tol:
+                assert nxt[b] == onext[b], f"pos {pos} b {b}: token {nxt[b]} != oracle {onext[b]}"
+    gpu.close()
+    ora.close()
+    print(f"worst err/tol {worst:.3f}; min top1-top2 margin {min(margins):.4f}")
+    return worst
+
+
+def test_small_fp16_b1():
+    run_parity(256, 2, 4, 1000)
+
+
+def test_small_fp16_batch3_eager():
+    run_parity(256, 2, 4, 1000, batch=3, use_graph=False, use_pdl=False)
+
+
+def test_small_fp16_batch16():
+    run_parity(512, 2, 8, 2000, batch=16)
+
+
+def test_small_int8_b1():
+    run_parity(256, 2, 4, 1000, dtype_bytes=1)
+
+
+def test_small_int8_batch8():
+    run_parity(512, 2, 8, 2000, batch=8, dtype_bytes=1)
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_local_fp16(tp):
+    run_parity(512, 2, 8, 1000, tp=tp, batch=2)
+
+
+def test_tp_local_int8():
+    run_parity(512, 2, 8, 1000, tp=2, dtype_bytes=1)
+
+
+def test_gptj_width_one_layer():
+    run_parity(4096, 1, 32, 50257, prompt_len=3, gen=2, max_ctx=8)
+
+
+def test_graph_replay_is_deterministic():
+    m = DecoderModel(256, 2, 4, 1000, batch=2, max_ctx=32, seed=SEED)
+    prompt = np.arange(10, dtype=np.int32).reshape(2, 5)
+    outs = []
+    for _ in range(2):
+        m.set_prompt(prompt)
+        m.step(12)
+        _, hist = m.read_tokens()
+        outs.append((hist.copy(), m.full_logits().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    m.close()
+
+
+def test_context_capacity_is_enforced():
+    m = DecoderModel(256, 1, 4, 1000, max_ctx=8, seed=SEED)
+    m.set_prompt(np.zeros((1, 4), dtype=np.int32))
+    m.step(8)
+    with pytest.raises(capi.InfeasibleError):
+        m.step(1)
+    m.close()
