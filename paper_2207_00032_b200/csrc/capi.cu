@@ -37,11 +37,11 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
     const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit);
     gemm::Params p{};
-    p.w = static_cast<const uint32_t*>(a.w_packed);
     p.w_scale = a.w_scales;
     p.N = N;
     p.K = K;
     p.rows = (K + (i8w ? 3 : 1)) / (i8w ? 4 : 2);
+    gemm::make_weight_map(&p.tmap, a.w_packed, N, p.rows);
     p.B = nb;
     const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
     p.x = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;

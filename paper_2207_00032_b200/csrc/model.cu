@@ -231,7 +231,7 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
 gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w) {
   gemm::Params p{};
   p.rows = int8_w ? (K + 3) / 4 : (K + 1) / 2;
-  p.w = w;
+  gemm::make_weight_map(&p.tmap, w, N, p.rows);
   p.w_scale = ws;
   p.N = N;
   p.K = K;

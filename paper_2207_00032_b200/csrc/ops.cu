@@ -4,6 +4,7 @@
 #include <cmath>
 
 #include "common.h"
+#include "launch.cuh"
 #include "ops.cuh"
 #include "ptx.cuh"
 #include "synth.h"
@@ -163,92 +164,6 @@ __global__ void quant_act_kernel(const __half* x, int64_t K, int8_t* q, float* s
     q[b * K + k] = static_cast<int8_t>(static_cast<int>(q8(__half2float(x[b * K + k]), s) << 24) >> 24);
 }
 
-// ---------------------------------------------------------------- attention
-constexpr int kAttnThreads = 128;
-
-__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_constant__ AttnParams p) {
-  extern __shared__ __align__(16) float asmem[];
-  const int d = p.d;
-  float* qf = asmem;              // [d]
-  float* of = qf + d;             // [d]
-  float* stat = of + d;           // [4]: m, l
-  float* sc = stat + 4;           // [chunk]
-  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
-  const int ctx = *p.pos + 1;
-  const int chunk = (ctx + C - 1) / C;
-  const int j0 = c * chunk;
-  const int j1 = min(ctx, j0 + chunk);
-  const int hd = p.H * d;
-  for (int i = threadIdx.x; i < d; i += kAttnThreads) qf[i] = __half2float(p.q[static_cast<size_t>(b) * hd + head * d + i]);
-  __syncthreads();
-  const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
-  const __half* kb = p.kc + kv_base;
-  const __half* vb = p.vc + kv_base;
-  // scores: one warp per position, lanes over half2 pairs of the head dim
-  for (int j = j0 + warp; j < j1; j += kAttnThreads / 32) {
-    const __half2* kr = reinterpret_cast<const __half2*>(kb + static_cast<size_t>(j) * d);
-    float acc = 0.f;
-    for (int pidx = lane; pidx < d / 2; pidx += 32) {
-      const float2 kv = __half22float2(kr[pidx]);
-      acc = fmaf(qf[2 * pidx], kv.x, acc);
-      acc = fmaf(qf[2 * pidx + 1], kv.y, acc);
-    }
-    acc = ptx::warp_sum(acc);
-    if (lane == 0) sc[j - j0] = acc * p.scale;
-  }
-  __syncthreads();
-  const int n = max(0, j1 - j0);
-  if (warp == 0) {
-    float mx = -INFINITY;
-    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, sc[j]);
-    mx = ptx::warp_max(mx);
-    float l = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float e = expf(sc[j] - mx);
-      sc[j] = e;
-      l += e;
-    }
-    l = ptx::warp_sum(l);
-    if (lane == 0) {
-      stat[0] = mx;
-      stat[1] = l;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < d; i += kAttnThreads) {
-    float acc = 0.f;
-    for (int j = 0; j < n; ++j) acc = fmaf(sc[j], __half2float(vb[static_cast<size_t>(j0 + j) * d + i]), acc);
-    of[i] = acc;
-  }
-  // combine the chunks of this (b, head) through distributed shared memory
-  if (C > 1)
-    ptx::cluster_sync();
-  else
-    __syncthreads();
-  const uint32_t rank = c;
-  float M = -INFINITY;
-  for (int r = 0; r < C; ++r) M = fmaxf(M, ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[0], r)));
-  float L = 0.f;
-  float wts[16];
-  for (int r = 0; r < C; ++r) {
-    const float mr = ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[0], r));
-    const float lr = ptx::ld_dsmem_f(ptx::map_shared_rank(&stat[1], r));
-    const float w = (mr == -INFINITY) ? 0.f : expf(mr - M);
-    wts[r] = w;
-    L += w * lr;
-  }
-  const float invL = 1.0f / L;
-  for (int i = rank + C * threadIdx.x; i < d; i += C * kAttnThreads) {
-    float o = 0.f;
-    for (int r = 0; r < C; ++r) o = fmaf(wts[r], ptx::ld_dsmem_f(ptx::map_shared_rank(&of[i], r)), o);
-    p.out[static_cast<size_t>(b) * hd + head * d + i] = __float2half_rn(o * invL);
-  }
-  if (C > 1) ptx::cluster_sync();
-}
-
 // ---------------------------------------------------------------- step boundary
 __global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
   ptx::pdl_trigger();
@@ -338,33 +253,6 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
   }
 }
 
-template <class K, class P>
-void launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const P& params,
-                int cluster_z = 1) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[2];
-  int na = 0;
-  if (cluster_z > 1) {
-    attrs[na].id = cudaLaunchAttributeClusterDimension;
-    attrs[na].val.clusterDim.x = 1;
-    attrs[na].val.clusterDim.y = 1;
-    attrs[na].val.clusterDim.z = cluster_z;
-    ++na;
-  }
-  if (pdl) {
-    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  cfg.attrs = attrs;
-  cfg.numAttrs = na;
-  DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, params));
-}
-
 }  // namespace
 
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s) {
@@ -408,27 +296,6 @@ void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, 
 void quantize_act_i8(const __half* x, int64_t B, int64_t K, int8_t* q, float* scales, cudaStream_t s) {
   quant_act_kernel<<<static_cast<unsigned>(B), 256, 0, s>>>(x, K, q, scales);
   DSINF_CUDA_CHECK(cudaGetLastError());
-}
-
-int attention_chunks(int B, int H) {
-  const int pairs = B * H;
-  int c = 1;
-  while (c < 8 && pairs * c < 2 * 148) c <<= 1;
-  return c;
-}
-
-void configure() {
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-}
-
-void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl) {
-  if (p.d % 2 != 0 || p.d > 1024) throw ConfigError("attention: head dim must be even and <= 1024");
-  if (chunks < 1 || chunks > 16) throw ConfigError("attention: bad chunk count");
-  const int max_chunk = (p.max_seq + chunks - 1) / chunks;
-  const size_t smem = (2 * static_cast<size_t>(p.d) + 4 + max_chunk) * sizeof(float);
-  if (smem > 200 * 1024) throw ConfigError("attention: context too long for one chunk");
-  launch_pdl(attention_kernel, dim3(p.H, p.B, chunks), dim3(kAttnThreads), smem, s, pdl, p, chunks);
 }
 
 void embed(const EmbedParams& p, cudaStream_t s, bool pdl) {

@@ -4,21 +4,29 @@
 // form a thread-block cluster and reduce through distributed shared memory (the paper's
 // "second kernel" cross-tile reduction, gemm.hpp:194-198, done in-cluster instead).
 //
-//   warp 0      producer: streams packed weight rows HBM -> smem with 1-D bulk async copies
-//               (TMA engine) into a multi-stage mbarrier ring.  Weights do not depend on the
-//               previous kernel, so the ring is filled *before* griddepcontrol.wait (PDL).
+//   warp 0      producer: one elected thread streams the packed weights HBM -> smem with 2-D
+//               tensor TMA (4 boxes of 32 rows x 32 words per 16 KB stage) into an mbarrier
+//               ring.  Weights do not depend on the previous kernel, so the ring is filled
+//               *before* griddepcontrol.wait (programmatic dependent launch).
 //   warps 1..4  consumers: Deep-Fusion prologue (LayerNorm / residual add / quantisation)
 //               into a smem x slice, then warp MMAs over the ring.
 //
 // The reference packed layout [ceil(K/M)][N][M] (gemm.hpp:108-111) is used unchanged: one
 // 32-bit word holds M=2 fp16 (or M=4 int8) consecutive k of one output column, which is
-// exactly one A-fragment register of mma.m16n8k16.f16 (mma.m16n8k32.s8).  Row r of a stage
-// is one bulk copy of 128 contiguous words; rows are padded to 136 words in smem so the
-// fragment reads (row t, column g) hit 32 distinct banks.
+// exactly one A-fragment register of mma.m16n8k16.f16 (mma.m16n8k32.s8).  TMA writes each box
+// with the 128-byte swizzle; inside a k-step of 8 packed rows the MMA k-slot t reads smem row
+// 2t (and t+4 reads 2t+1) — a k permutation applied to both operands — which makes every
+// fragment read hit 32 distinct banks under that swizzle.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <type_traits>
+
+#include <cudaTypedefs.h>
 
 #include "common.h"
 #include "ptx.cuh"
@@ -33,8 +41,6 @@ struct Header {
   uint64_t full[kMaxStages];
   uint64_t empty[kMaxStages];
   float xscale[kMaxB];
-  float mean[kMaxB];
-  float rstd[kMaxB];
   float red[8];
 };
 static_assert(sizeof(Header) <= kHeaderBytes, "header too large");
@@ -75,8 +81,7 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 }
 
 // Per-token int8: q = clamp(rint(x / s), -127, 127) with IEEE division (bit-exact vs oracle).
-__device__ __forceinline__ uint32_t quant_byte(float x, float inv_unused, float scale) {
-  (void)inv_unused;
+__device__ __forceinline__ uint32_t quant_byte(float x, float scale) {
   int q = __float2int_rn(__fdiv_rn(x, scale));
   q = max(-127, min(127, q));
   return static_cast<uint32_t>(q) & 0xffu;
@@ -134,6 +139,7 @@ __device__ void prologue_ln(const Params& p, uint32_t* sx, Header& hd, int k0, i
   float c0 = 0.f, s1 = 0.f, s2 = 0.f;
   if (active) {
     c0 = rv.load4(b, 0).x;  // shift for a cancellation-free single pass
+#pragma unroll 4
     for (int c = j; c < K / 4; c += tpr) {
       const float4 v = rv.load4(b, 4 * c);
       if (write_res) *reinterpret_cast<float4*>(p.res_out + static_cast<size_t>(b) * K + 4 * c) = v;
@@ -167,6 +173,7 @@ __device__ void prologue_ln(const Params& p, uint32_t* sx, Header& hd, int k0, i
   } else {
     float mx = 0.f;
     if (active) {
+#pragma unroll 2
       for (int c = j; c < K / 4; c += tpr) {
         const float4 v = rv.load4(b, 4 * c);
         const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -190,7 +197,7 @@ __device__ void prologue_ln(const Params& p, uint32_t* sx, Header& hd, int k0, i
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float y = __half2float(__float2half_rn(ln_apply(vv[i], mean, rstd, p.ln_g, p.ln_b, k + i)));
-            word |= quant_byte(y, 0.f, scale) << (8 * i);
+            word |= quant_byte(y, scale) << (8 * i);
           }
         }
         row[w] = word;
@@ -257,7 +264,7 @@ __device__ void prologue_load(const Params& p, uint32_t* sx, Header& hd, int k0,
         const int k = k0 + 4 * w;
         uint32_t word = 0;
         for (int i = 0; i < 4; ++i)
-          if (k + i < K) word |= quant_byte(ldh(x, static_cast<size_t>(b) * p.x_ld + k + i), 0.f, scale) << (8 * i);
+          if (k + i < K) word |= quant_byte(ldh(x, static_cast<size_t>(b) * p.x_ld + k + i), scale) << (8 * i);
         sx[b * p.x_row_words + w] = word;
       }
     }
@@ -333,13 +340,18 @@ __device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, flo
 }
 
 // ------------------------------------------------------------------ kernel
+// Dynamic smem (base rounded up to 1024 B for the 128B swizzle):
+//   [ring: stages x 16 KB] [header 1 KB] [x slice: 8*kNB8 rows x x_row_words words]
+// After the main loop the ring is reused for the split-K partials part[b][n].
 
 template <bool kInt8, int kNB8>
 __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constant__ Params p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  Header& hd = *reinterpret_cast<Header*>(smem);
-  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + kHeaderBytes);
-  uint32_t* ring = sx + 8 * kNB8 * p.x_row_words;  // 16-byte aligned (x_row_words % 4 == 0)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int stages = p.stages;
+  uint8_t* ring = smem;
+  Header& hd = *reinterpret_cast<Header*>(smem + stages * kStageBytes);
+  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + stages * kStageBytes + kHeaderBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -350,11 +362,11 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   const int row_begin = split * p.rows_per_split;
   const int row_end = min(p.rows, row_begin + p.rows_per_split);
   const int n_iters = (row_end - row_begin + kRowsPerStage - 1) / kRowsPerStage;
-  const int stages = p.stages;
 
   ptx::pdl_trigger();  // dependents may launch and start streaming their own weights
 
   if (threadIdx.x == 0) {
+    ptx::prefetch_tensormap(&p.tmap);
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(&hd.full[s], 1);
       ptx::mbar_init(&hd.empty[s], kConsumerWarps);
@@ -364,39 +376,29 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   __syncthreads();
 
   if (warp == 0) {
-    // ================= producer: weight rows -> smem ring
-    const int ncols = min(kColTile, p.N - n0);
-    const uint32_t row_bytes = static_cast<uint32_t>(ncols) * 4u;
-    const uint64_t policy = ptx::policy_evict_first();
-    for (int it = 0; it < n_iters; ++it) {
-      const int s = it % stages;
-      if (it == stages) ptx::pdl_wait();  // (weights never depend on the previous grid)
-      if (it >= stages) ptx::mbar_wait(&hd.empty[s], ((it / stages) - 1) & 1);
-      uint32_t* dst = ring + s * kStageWords;
-      const int r0 = row_begin + it * kRowsPerStage;
-      const int valid = min(kRowsPerStage, row_end - r0);
-      if (lane >= valid) {  // K tail: zero rows so 0 * stale never yields NaN
-        uint4* z = reinterpret_cast<uint4*>(dst + lane * kRowWords);
-        for (int i = 0; i < kColTile / 4; ++i) z[i] = make_uint4(0, 0, 0, 0);
-        ptx::fence_proxy_async_smem();
-      }
-      if (p.aligned) {
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_expect_tx(&hd.full[s], row_bytes * valid);
-        __syncwarp();
-        if (lane < valid)
-          ptx::bulk_g2s(dst + lane * kRowWords, p.w + static_cast<size_t>(r0 + lane) * p.N + n0, row_bytes,
-                        &hd.full[s], policy);
-      } else {
-        for (int r = 0; r < valid; ++r) {
-          const uint32_t* src = p.w + static_cast<size_t>(r0 + r) * p.N + n0;
-          for (int c = lane; c < ncols; c += 32) dst[r * kRowWords + c] = __ldg(src + c);
+    // ================= producer: one elected thread issues 4 TMA boxes per stage
+    if (lane == 0) {
+      const uint64_t policy = ptx::policy_evict_first();
+      int s = 0;
+      uint32_t phase = 0;
+      for (int it = 0; it < n_iters; ++it) {
+        if (it == stages) ptx::pdl_wait();  // first `stages` loads run ahead of the dependency
+        if (it >= stages) ptx::mbar_wait(&hd.empty[s], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&hd.full[s], kStageBytes);
+        const int r0 = row_begin + it * kRowsPerStage;
+        uint8_t* dst = ring + s * kStageBytes;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w)
+          ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&hd.full[s]);
       }
+      if (n_iters <= stages) ptx::pdl_wait();
+    } else {
+      ptx::pdl_wait();
     }
-    if (n_iters <= stages) ptx::pdl_wait();
   } else {
     // ================= consumers
     const int cw = warp - 1;
@@ -421,34 +423,51 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[j][bt][e] = 0;
 
+    // x words: b0 = slice row 2t, b1 = row 2t+1 of each k-step (one 8-byte load)
     const uint32_t* xrow[kNB8];
     bool xvalid[kNB8];
 #pragma unroll
     for (int bt = 0; bt < kNB8; ++bt) {
       xvalid[bt] = bt * 8 + g < p.B;
-      xrow[bt] = sx + (bt * 8 + g) * p.x_row_words + t;
+      xrow[bt] = sx + (bt * 8 + g) * p.x_row_words + 2 * t;
     }
-    const int colw = cw * 32 + g;
+    // A words inside this warp's 128B-swizzled box: row r = 8*ks + 2t + par, column c = 16j + 8h + g
+    //   byte = r*128 + ((c/4) ^ (r%8))*16 + (c%4)*4, and r%8 = 2t + par does not depend on ks.
+    uint32_t aoff[2][2][2];  // [j][h][par]
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          const int r = 2 * t + par;
+          const int c = 16 * j + 8 * h + g;
+          aoff[j][h][par] = r * 128 + (((c >> 2) ^ r) << 4) + (c & 3) * 4;
+        }
+    const uint8_t* wbox = ring + cw * kBoxBytes;
+    int s = 0;
+    uint32_t phase = 0;
     for (int it = 0; it < n_iters; ++it) {
-      const int s = it % stages;
-      ptx::mbar_wait(&hd.full[s], (it / stages) & 1);
-      const uint32_t* sw = ring + s * kStageWords + t * kRowWords + colw;
+      ptx::mbar_wait(&hd.full[s], phase);
+      const uint8_t* sw = wbox + s * kStageBytes;
       const int xr0 = it * kRowsPerStage;
 #pragma unroll
       for (int ks = 0; ks < kRowsPerStage / 8; ++ks) {
         uint32_t b0[kNB8], b1[kNB8];
 #pragma unroll
         for (int bt = 0; bt < kNB8; ++bt) {
-          b0[bt] = xvalid[bt] ? xrow[bt][xr0 + ks * 8] : 0u;
-          b1[bt] = xvalid[bt] ? xrow[bt][xr0 + ks * 8 + 4] : 0u;
+          uint2 v = make_uint2(0u, 0u);
+          if (xvalid[bt]) v = *reinterpret_cast<const uint2*>(xrow[bt] + xr0 + ks * 8);
+          b0[bt] = v.x;
+          b1[bt] = v.y;
         }
-        const uint32_t* a = sw + ks * 8 * kRowWords;
+        const uint8_t* a = sw + ks * 8 * 128;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const uint32_t a0 = a[j * 16];
-          const uint32_t a1 = a[j * 16 + 8];
-          const uint32_t a2 = a[4 * kRowWords + j * 16];
-          const uint32_t a3 = a[4 * kRowWords + j * 16 + 8];
+          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][0]);
+          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][0]);
+          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][1]);
+          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt) {
             if constexpr (kInt8)
@@ -460,6 +479,10 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
     }
     consumer_bar();  // every consumer is done reading the ring
     // partials -> smem (reuses the ring): part[b][n]
@@ -468,7 +491,7 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int bt = 0; bt < kNB8; ++bt) {
-        const int n = cw * 32 + j * 16 + g;
+        const int n = cw * kWarpCols + j * 16 + g;
         const int b = bt * 8 + 2 * t;
         if (b < p.B) {
           part[b * kPartLd + n] = acc[j][bt][0];
@@ -490,7 +513,7 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   const int cols_per_rank = kColTile / nsplit;
   const int c_begin = rank * cols_per_rank;
   const int pairs = cols_per_rank / 2;
-  const uint8_t* part_base = reinterpret_cast<const uint8_t*>(ring);
+  const uint8_t* part_base = ring;
   for (int item = threadIdx.x; item < p.B * pairs; item += kThreads) {
     const int b = item / pairs;
     const int c = c_begin + 2 * (item - b * pairs);
@@ -555,7 +578,34 @@ void configure_one() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
 }  // namespace
+
+void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows) {
+  if (N % 4 != 0) throw ConfigError("sbi_gemm: out_dim must be a multiple of 4 (16-byte TMA row stride)");
+  if ((reinterpret_cast<uintptr_t>(w_packed) & 15) != 0) throw ConfigError("sbi_gemm: weights must be 16-byte aligned");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kWarpCols), static_cast<cuuint32_t>(kRowsPerStage)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(w_packed), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+}
 
 void configure() {
   configure_one<false, 1>();
@@ -564,6 +614,54 @@ void configure() {
   configure_one<true, 2>();
 }
 
+namespace {
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// Co-resident clusters of `split` CTAs for this kernel / smem (cached; 0 when unknown).
+int resident_clusters(bool int8_weights, int nb8, int split, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<bool, int, int, size_t>, int> cache;
+  const auto key = std::make_tuple(int8_weights, nb8, split, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const void* kern = nullptr;
+  if (int8_weights)
+    kern = nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2>);
+  else
+    kern = nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2>);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, split, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 1;
+  attr.val.clusterDim.y = split;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[key] = n;
+  return n;
+}
+
+}  // namespace
+
+// B200 launch plan (the device half of derive_schedule, gemm.hpp:65-96): like the reference it
+// splits K only when the output tiles alone cannot occupy the machine, but it sizes the split
+// so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
+// once, no tail wave) and reduces the split in-cluster.
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   const int m = int8_weights ? 4 : 2;
@@ -576,38 +674,51 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split) {
     int r = (rows + s - 1) / s;
     return (r + kRowsPerStage - 1) / kRowsPerStage * kRowsPerStage;
   };
-  auto x_bytes = [&](int rps) { return static_cast<size_t>(8 * pl.nb8) * (rps + 4) * 4; };
+  auto x_bytes = [&](int rps) { return static_cast<size_t>(B) * (rps + 8) * 4; };
   auto valid = [&](int s) {
     const int rps = rps_for(s);
     if ((rows + rps - 1) / rps != s) return false;  // no empty split
     return x_bytes(rps) <= x_budget;
   };
+  const int max_stages = std::max(1, std::min(kMaxStages, env_int("DSINF_STAGES", 4)));
+  auto smem_for = [&](int s, int* stages_out) {
+    const int rps = rps_for(s);
+    const int iters = rps / kRowsPerStage;
+    const size_t fixed = 1024 /*alignment slack*/ + kHeaderBytes + x_bytes(rps);
+    int st = std::min(max_stages, std::max(1, iters));
+    while (st > 2 && fixed + st * static_cast<size_t>(kStageBytes) > 110 * 1024) --st;
+    if (stages_out) *stages_out = st;
+    const size_t part_bytes = static_cast<size_t>(B) * kPartLd * 4;
+    return fixed + std::max(static_cast<size_t>(st) * kStageBytes, part_bytes);
+  };
   int chosen = 0;
+  if (forced_split <= 0) forced_split = env_int("DSINF_KSPLIT", 0);
   if (forced_split > 0) {
     if (forced_split != 1 && forced_split != 2 && forced_split != 4 && forced_split != 8 && forced_split != 16)
       throw ConfigError("ksplit must be one of {1, 2, 4, 8, 16}");
     if (!valid(forced_split)) throw ConfigError("ksplit not valid for this shape");
     chosen = forced_split;
   } else {
-    const int target = 2 * 148;  // >= 2 resident CTAs per SM keeps enough bytes in flight
+    // largest one-wave grid; if none fits in one wave, the smallest valid split
+    int best_units = -1;
     for (int s = 1; s <= 16; s <<= 1) {
       if (!valid(s)) continue;
-      chosen = s;
-      if (pl.col_tiles * s >= target) break;
+      const int units = pl.col_tiles * s;
+      const int clusters = resident_clusters(int8_weights, pl.nb8, s, smem_for(s, nullptr));
+      const int capacity = clusters > 0 ? clusters * s : 2 * 148;
+      if (units <= capacity && units > best_units) {
+        best_units = units;
+        chosen = s;
+      }
     }
+    if (chosen == 0)
+      for (int s = 1; s <= 16 && chosen == 0; s <<= 1)
+        if (valid(s)) chosen = s;
     if (chosen == 0) throw ConfigError("sbi_gemm: K too large for the x slice budget");
   }
   pl.ksplit = chosen;
   pl.rows_per_split = rps_for(chosen);
-  const int iters = pl.rows_per_split / kRowsPerStage;
-  const size_t stage_bytes = static_cast<size_t>(kStageWords) * 4;
-  const size_t fixed = kHeaderBytes + x_bytes(pl.rows_per_split);
-  // ring depth: up to 4 stages, bounded so ~2 CTAs fit per SM
-  int st = std::min(4, std::max(1, iters));
-  while (st > 2 && fixed + st * stage_bytes > 110 * 1024) --st;
-  pl.stages = st;
-  const size_t part_bytes = static_cast<size_t>(kMaxB) * kPartLd * 4;
-  pl.smem_bytes = fixed + std::max(static_cast<size_t>(st) * stage_bytes, part_bytes);
+  pl.smem_bytes = smem_for(chosen, &pl.stages);
   return pl;
 }
 
@@ -615,8 +726,7 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   Params p = p_in;
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
-  p.x_row_words = plan.rows_per_split + 4;
-  p.aligned = (p.N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.w) & 15) == 0;
+  p.x_row_words = plan.rows_per_split + 8;
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
   if (int8_weights) {

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -12,14 +13,15 @@ namespace gemm {
 
 constexpr int kConsumerWarps = 4;
 constexpr int kThreads = 32 * (kConsumerWarps + 1);
-constexpr int kColTile = 128;                    // output columns per CTA
-constexpr int kRowsPerStage = 32;                // packed rows per pipeline stage
-constexpr int kRowWords = kColTile + 8;          // 136 words: conflict-free fragment reads
-constexpr int kStageWords = kRowsPerStage * kRowWords;
+constexpr int kWarpCols = 32;                              // columns per consumer warp (one TMA box)
+constexpr int kColTile = kWarpCols * kConsumerWarps;       // 128 output columns per CTA
+constexpr int kRowsPerStage = 32;                          // packed rows per pipeline stage
+constexpr int kBoxBytes = kWarpCols * 4 * kRowsPerStage;   // 4 KB: one 128B-swizzled TMA box
+constexpr int kStageBytes = kBoxBytes * kConsumerWarps;    // 16 KB
 constexpr int kMaxStages = 8;
-constexpr int kMaxB = 16;                        // batch rows per launch
-constexpr int kPartLd = kColTile + 4;            // split-K partial row stride (floats)
-constexpr int kHeaderBytes = 1024;               // barriers + per-row scalars
+constexpr int kMaxB = 16;                                  // batch rows per launch
+constexpr int kPartLd = kColTile + 4;                      // split-K partial row stride (floats)
+constexpr int kHeaderBytes = 1024;                         // barriers + per-row scalars
 
 enum Prologue : int {
   PRO_F16 = 0,    // x fp16 [B][x_ld] from global
@@ -36,14 +38,14 @@ enum Epilogue : int {
 };
 
 struct Params {
-  // packed weights: word (row r, column n) at w[r * N + n]; a word holds pack_M k-values
-  const uint32_t* w;
+  // packed weights viewed by TMA as a 2-D tensor of 32-bit words [rows][N]; a word holds pack_M
+  // consecutive k of one output column (gemm.hpp:108-111)
+  alignas(64) CUtensorMap tmap;
   const float* w_scale;  // int8: per-output-row scale [N]
   int N, rows, K, B;
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
   int stages;
-  int x_row_words;       // smem stride of one x row (== 4 mod 32)
-  int aligned;           // N % 4 == 0 (bulk copies) else synchronous staging
+  int x_row_words;       // smem stride of one x row (== 8 mod 32)
   // prologue
   int pro;
   const void* x;
@@ -78,6 +80,9 @@ struct Plan {
   size_t smem_bytes;
 };
 
+// TMA descriptor of a packed weight matrix (N words per row, `rows` rows), 128B swizzle,
+// box = 32 words x kRowsPerStage rows.  Out-of-bounds rows / columns read as zero.
+void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 // Sets kernel attributes for every instantiation; call before graph capture.
 void configure();
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split);
