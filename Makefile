@@ -14,9 +14,9 @@ ORACLE_LIB := oracle/liboracle.so
 REF_LIB := oracle/_ref/libinfersim_ref.so
 
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xcompiler -ffp-contract=off \
              --expt-relaxed-constexpr -Iinclude -I$(CSRC) -Xptxas -warn-spills
-CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -Iinclude -I$(CSRC) -I/usr/local/cuda/include
+CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC) -I/usr/local/cuda/include
 
 CU_SRCS := $(CSRC)/sbi_gemm.cu $(CSRC)/attention.cu $(CSRC)/ops.cu $(CSRC)/model.cu $(CSRC)/capi.cu
 CPP_SRCS := $(CSRC)/host_api.cpp $(CSRC)/nccl_dl.cpp

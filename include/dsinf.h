@@ -252,6 +252,12 @@ int64_t dsinf_model_bytes_per_step(const dsinf_model* m, int64_t pos);
 /* Host-side generator (same bits the device generator writes). */
 int dsinf_synthetic_tensor(uint64_t seed, int32_t layer, int32_t tensor, int64_t rows,
                            int64_t cols, float* out_fp32_of_fp16);
+/* Rank `rank`'s tensor-parallel shard of one tensor, logical row-major [rows][cols] fp16
+ * values as fp32 (the map the device generator uses; out == NULL queries rows/cols).
+ * layer = -1 for the embedding / LM head (DSINF_T_WTE) and the final LayerNorm. */
+int dsinf_shard_tensor(const dsinf_model_config* cfg, int32_t tp, int32_t rank, int32_t layer,
+                       int32_t tensor, uint64_t seed, float* out, int64_t out_len, int64_t* rows,
+                       int64_t* cols);
 
 /* ---- NCCL (loaded with dlopen on first use; NCCL mode only) */
 int dsinf_nccl_get_unique_id(uint8_t id_out[128]);

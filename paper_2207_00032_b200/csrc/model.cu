@@ -16,6 +16,8 @@
 // also where the TP all-reduced partial is folded in, so t = 1 and t > 1 share one path.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -124,7 +126,7 @@ namespace {
 
 using Model = dsinf_model;
 
-ops::ShardMap make_map(const Model& m, int64_t N_local, int64_t K_local, int64_t N_global, int64_t K_global,
+ops::ShardMap make_map(uint64_t seed, int64_t N_local, int64_t K_local, int64_t N_global, int64_t K_global,
                        int64_t sec_local, int64_t sec_global, int64_t row_off, int64_t col_off, int layer,
                        int tensor, float amp, int64_t valid_rows = -1) {
   ops::ShardMap s{};
@@ -137,9 +139,48 @@ ops::ShardMap make_map(const Model& m, int64_t N_local, int64_t K_local, int64_t
   s.row_off = row_off;
   s.col_off = col_off;
   s.valid_rows = valid_rows < 0 ? N_global : valid_rows;
-  s.base = synth_base(m.rt.seed, layer, tensor);
+  s.base = synth_base(seed, layer, tensor);
   s.amp = amp;
   return s;
+}
+
+float tensor_amp(int tensor, float* offset) {
+  *offset = 0.f;
+  switch (tensor) {
+    case DSINF_T_QKV_BIAS:
+    case DSINF_T_O_BIAS:
+    case DSINF_T_UP_BIAS:
+    case DSINF_T_DOWN_BIAS: return SynthScale::kBias;
+    case DSINF_T_LN1_G:
+    case DSINF_T_LN2_G:
+    case DSINF_T_LNF_G: *offset = 1.f; return SynthScale::kLnGamma;
+    case DSINF_T_LN1_B:
+    case DSINF_T_LN2_B:
+    case DSINF_T_LNF_B: return SynthScale::kLnBeta;
+    default: return SynthScale::kWeight;
+  }
+}
+
+// Megatron tensor-parallel shard of one synthetic tensor for rank r of t:
+// QKV column-parallel by head (local rows [q_r | k_r | v_r]); attn-out row-parallel over this
+// rank's heads; MLP-up column-parallel; MLP-down row-parallel; LM head vocab-parallel over the
+// vocab padded to 128*t rows; biases / LayerNorm replicated.  The device generator and the host
+// dsinf_shard_tensor both use this map.
+ops::ShardMap tensor_map(int64_t h, int64_t H, int64_t V, int t, int r, uint64_t seed, int layer, int tensor) {
+  const int64_t d = h / H, Hl = H / t, F = 4 * h, Fl = F / t;
+  const int64_t vq = 128LL * t, Vpad = (V + vq - 1) / vq * vq, Vl = Vpad / t;
+  float off = 0.f;
+  const float amp = tensor_amp(tensor, &off);
+  switch (tensor) {
+    case DSINF_T_QKV: return make_map(seed, 3 * Hl * d, h, 3 * h, h, Hl * d, h, r * Hl * d, 0, layer, tensor, amp);
+    case DSINF_T_QKV_BIAS: return make_map(seed, 3 * Hl * d, 1, 3 * h, 1, Hl * d, h, r * Hl * d, 0, layer, tensor, amp);
+    case DSINF_T_O: return make_map(seed, h, Hl * d, h, h, h, h, 0, r * Hl * d, layer, tensor, amp);
+    case DSINF_T_UP: return make_map(seed, Fl, h, F, h, Fl, F, r * Fl, 0, layer, tensor, amp);
+    case DSINF_T_UP_BIAS: return make_map(seed, Fl, 1, F, 1, Fl, F, r * Fl, 0, layer, tensor, amp);
+    case DSINF_T_DOWN: return make_map(seed, h, Fl, h, F, h, h, 0, r * Fl, layer, tensor, amp);
+    case DSINF_T_WTE: return make_map(seed, Vl, h, Vpad, h, Vl, Vpad, r * Vl, 0, layer, tensor, amp, V);
+    default: return make_map(seed, h, 1, h, 1, h, h, 0, 0, layer, tensor, amp);  // replicated vectors
+  }
 }
 
 // Allocates and generates one GEMM weight in the packed layout (fp16 M=2 or int8 M=4).
@@ -169,39 +210,41 @@ __half* make_vec(Model& m, const ops::ShardMap& map, float offset, cudaStream_t 
 void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   const int r = sh.rank;
   const int64_t h = m.h, Hl = m.Hl, d = m.d, Fl = m.Fl;
-  const float aw = SynthScale::kWeight, ab = SynthScale::kBias;
   sh.layers.resize(m.L);
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = sh.layers[l];
-    // QKV: column parallel by head; local rows [q_r | k_r | v_r]
-    w.wqkv = make_weight(m, make_map(m, 3 * Hl * d, h, 3 * h, h, Hl * d, h, r * Hl * d, 0, l, DSINF_T_QKV, aw), &w.sqkv, s);
-    w.bqkv = make_vec(m, make_map(m, 3 * Hl * d, 1, 3 * h, 1, Hl * d, h, r * Hl * d, 0, l, DSINF_T_QKV_BIAS, ab), 0.f, s);
-    // attn-out: row parallel (K = this rank's heads)
-    w.wo = make_weight(m, make_map(m, h, Hl * d, h, h, h, h, 0, r * Hl * d, l, DSINF_T_O, aw), &w.so, s);
-    w.bo = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_O_BIAS, ab), 0.f, s);
-    // MLP: up column parallel, down row parallel
-    w.wup = make_weight(m, make_map(m, Fl, h, m.F, h, Fl, m.F, r * Fl, 0, l, DSINF_T_UP, aw), &w.sup, s);
-    w.bup = make_vec(m, make_map(m, Fl, 1, m.F, 1, Fl, m.F, r * Fl, 0, l, DSINF_T_UP_BIAS, ab), 0.f, s);
-    w.wdown = make_weight(m, make_map(m, h, Fl, h, m.F, h, h, 0, r * Fl, l, DSINF_T_DOWN, aw), &w.sdown, s);
-    w.bdown = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_DOWN_BIAS, ab), 0.f, s);
-    w.ln1g = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN1_G, SynthScale::kLnGamma), 1.f, s);
-    w.ln1b = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN1_B, SynthScale::kLnBeta), 0.f, s);
-    w.ln2g = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN2_G, SynthScale::kLnGamma), 1.f, s);
-    w.ln2b = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, l, DSINF_T_LN2_B, SynthScale::kLnBeta), 0.f, s);
+    auto map = [&](int tensor) { return tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, l, tensor); };
+    auto vec = [&](int tensor) {
+      float off = 0.f;
+      tensor_amp(tensor, &off);
+      return make_vec(m, map(tensor), off, s);
+    };
+    w.wqkv = make_weight(m, map(DSINF_T_QKV), &w.sqkv, s);
+    w.bqkv = vec(DSINF_T_QKV_BIAS);
+    w.wo = make_weight(m, map(DSINF_T_O), &w.so, s);
+    w.bo = vec(DSINF_T_O_BIAS);
+    w.wup = make_weight(m, map(DSINF_T_UP), &w.sup, s);
+    w.bup = vec(DSINF_T_UP_BIAS);
+    w.wdown = make_weight(m, map(DSINF_T_DOWN), &w.sdown, s);
+    w.bdown = vec(DSINF_T_DOWN_BIAS);
+    w.ln1g = vec(DSINF_T_LN1_G);
+    w.ln1b = vec(DSINF_T_LN1_B);
+    w.ln2g = vec(DSINF_T_LN2_G);
+    w.ln2b = vec(DSINF_T_LN2_B);
   }
   // LM head (tied with the embedding, fp16 in both modes): vocab parallel, padded rows are 0
   {
-    const ops::ShardMap lm = make_map(m, m.Vl, h, m.Vpad, h, m.Vl, m.Vpad, r * m.Vl, 0, -1, DSINF_T_WTE, aw, m.V);
+    const ops::ShardMap lm = tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, -1, DSINF_T_WTE);
     const int64_t words = (h + 1) / 2 * m.Vl;
     sh.wlm = m.alloc_n<uint32_t>(words);
     m.weight_bytes += words * 4;
     ops::init_packed_f16(lm, sh.wlm, s);
   }
-  sh.lnfg = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, -1, DSINF_T_LNF_G, SynthScale::kLnGamma), 1.f, s);
-  sh.lnfb = make_vec(m, make_map(m, h, 1, h, 1, h, h, 0, 0, -1, DSINF_T_LNF_B, SynthScale::kLnBeta), 0.f, s);
+  sh.lnfg = make_vec(m, tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, -1, DSINF_T_LNF_G), 1.f, s);
+  sh.lnfb = make_vec(m, tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, -1, DSINF_T_LNF_B), 0.f, s);
   if (r == 0 || m.rt.tp_mode == DSINF_TP_NCCL) {
     sh.wte = m.alloc_n<__half>(m.V * h);
-    ops::init_rowmajor_f16(synth_base(m.rt.seed, -1, DSINF_T_WTE), aw, m.V, h, sh.wte, s);
+    ops::init_rowmajor_f16(synth_base(m.rt.seed, -1, DSINF_T_WTE), SynthScale::kWeight, m.V, h, sh.wte, s);
   } else {
     sh.wte = m.shards[0].wte;
   }
@@ -247,8 +290,17 @@ struct Enqueuer {
   bool pdl;
   int64_t launches = 0;
 
-  void gemm_launch(const gemm::Params& p, const gemm::Plan& plan, bool int8_w) {
-    gemm::launch(p, plan, int8_w, s, pdl);
+  // DSINF_PDL_MASK bits: 0 qkv, 1 attention, 2 attn-out, 3 up, 4 down, 5 lm head, 6 the rest.
+  // Default: only the attn-out GEMM (its weight prefetch overlaps the latency-bound attention);
+  // early-launched dependents of the full-machine GEMMs steal SM slots and measured slower.
+  int mask = [] { const char* v = std::getenv("DSINF_PDL_MASK"); return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x04; }();
+  bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
+
+  int64_t pdl_launches = 0;
+
+  void gemm_launch(const gemm::Params& p, const gemm::Plan& plan, bool int8_w, int bit) {
+    pdl_launches += P(bit);
+    gemm::launch(p, plan, int8_w, s, P(bit));
     ++launches;
   }
 
@@ -274,7 +326,7 @@ struct Enqueuer {
     p.heads = static_cast<int>(m.Hl);
     p.head_dim = static_cast<int>(m.d);
     p.max_seq = m.max_ctx;
-    gemm_launch(p, sh.plan_qkv, m.int8);
+    gemm_launch(p, sh.plan_qkv, m.int8, 0);
   }
 
   void k2_attn(Shard& sh, int l) {
@@ -290,7 +342,7 @@ struct Enqueuer {
     a.d = static_cast<int>(m.d);
     a.max_seq = m.max_ctx;
     a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
-    ops::attention(a, m.attn_chunks, s, pdl);
+    ops::attention(a, m.attn_chunks, s, P(1));
     ++launches;
   }
 
@@ -302,7 +354,7 @@ struct Enqueuer {
     p.x_ld = static_cast<int>(m.Hl * m.d);
     p.epi = gemm::EPI_F32;
     p.out = sh.d_attn;
-    gemm_launch(p, sh.plan_o, m.int8);
+    gemm_launch(p, sh.plan_o, m.int8, 2);
   }
 
   void k4_up(Shard& sh, int l) {
@@ -318,7 +370,7 @@ struct Enqueuer {
     p.epi = gemm::EPI_GELU_F16;
     p.bias = w.bup;
     p.out = sh.u;
-    gemm_launch(p, sh.plan_up, m.int8);
+    gemm_launch(p, sh.plan_up, m.int8, 3);
   }
 
   void k5_down(Shard& sh, int l) {
@@ -329,7 +381,7 @@ struct Enqueuer {
     p.x_ld = static_cast<int>(m.Fl);
     p.epi = gemm::EPI_F32;
     p.out = sh.d_mlp;
-    gemm_launch(p, sh.plan_down, m.int8);
+    gemm_launch(p, sh.plan_down, m.int8, 4);
   }
 
   void lm_head(Shard& sh) {
@@ -343,7 +395,7 @@ struct Enqueuer {
     p.ln_b = sh.lnfb;
     p.epi = gemm::EPI_F32;
     p.out = sh.logits;
-    gemm_launch(p, sh.plan_lm, false);
+    gemm_launch(p, sh.plan_lm, false, 5);
     ops::ArgmaxParams ap{};
     ap.logits = sh.logits;
     ap.ld = static_cast<int>(m.Vl);
@@ -353,7 +405,7 @@ struct Enqueuer {
     ap.idx_offset = first;
     ap.out_val = m.am_val + sh.rank * m.B;
     ap.out_idx = m.am_idx + sh.rank * m.B;
-    ops::argmax(ap, s, pdl);
+    ops::argmax(ap, s, P(6));
     ++launches;
   }
 
@@ -369,7 +421,7 @@ struct Enqueuer {
       p.shards = m.t;
       p.count = count;
       for (int i = 0; i < m.t; ++i) p.buf[i] = which == 0 ? m.shards[i].d_attn : m.shards[i].d_mlp;
-      ops::local_allreduce(p, s, pdl);
+      ops::local_allreduce(p, s, P(6));
       ++launches;
     }
   }
@@ -389,7 +441,7 @@ struct Enqueuer {
       e.B = m.B;
       e.h = static_cast<int>(m.h);
       e.V = static_cast<int>(m.V);
-      ops::embed(e, s, pdl);
+      ops::embed(e, s, P(6));
       ++launches;
     }
     for (int l = 0; l < m.L; ++l) {
@@ -420,7 +472,7 @@ struct Enqueuer {
     sp.pos = m.pos;
     sp.hist = m.hist;
     sp.max_ctx = m.max_ctx;
-    ops::select_token(sp, s, pdl);
+    ops::select_token(sp, s, P(6));
     ++launches;
   }
 };
@@ -473,6 +525,7 @@ void ensure_graph(Model& m) {
   }
   DSINF_CUDA_CHECK(cudaStreamEndCapture(m.cap_stream, &m.graph));
   DSINF_CUDA_CHECK(cudaGraphInstantiate(&m.exec, m.graph, 0));
+  if (std::getenv("DSINF_DEBUG")) fprintf(stderr, "[dsinf] captured %lld launches, %lld gemm launches with PDL (mask 0x%x, pdl %d)\n", (long long)e.launches, (long long)e.pdl_launches, e.mask, (int)e.pdl);
   m.kernels_per_step = e.launches;
 }
 
@@ -677,24 +730,43 @@ int dsinf_synthetic_tensor(uint64_t seed, int32_t layer, int32_t tensor, int64_t
                            float* out) {
   return guarded([&] {
     require(out != nullptr && rows >= 0 && cols >= 0, "bad arguments");
-    float amp = SynthScale::kWeight, offset = 0.f;
-    switch (tensor) {
-      case DSINF_T_QKV_BIAS:
-      case DSINF_T_O_BIAS:
-      case DSINF_T_UP_BIAS:
-      case DSINF_T_DOWN_BIAS: amp = SynthScale::kBias; break;
-      case DSINF_T_LN1_G:
-      case DSINF_T_LN2_G:
-      case DSINF_T_LNF_G: amp = SynthScale::kLnGamma; offset = 1.f; break;
-      case DSINF_T_LN1_B:
-      case DSINF_T_LN2_B:
-      case DSINF_T_LNF_B: amp = SynthScale::kLnBeta; break;
-      default: break;
-    }
+    float offset = 0.f;
+    const float amp = tensor_amp(tensor, &offset);
     const uint64_t base = synth_base(seed, layer, tensor);
     for (int64_t i = 0; i < rows * cols; ++i) {
-      const float v = offset + synth_unit(base, static_cast<uint64_t>(i)) * amp;
-      out[i] = f16_bits_to_f32(f32_to_f16_bits(v));
+      const float t = synth_unit(base, static_cast<uint64_t>(i)) * amp;
+      out[i] = f16_bits_to_f32(f32_to_f16_bits(offset + t));
+    }
+  });
+}
+
+int dsinf_shard_tensor(const dsinf_model_config* cfg, int32_t tp, int32_t rank, int32_t layer, int32_t tensor,
+                       uint64_t seed, float* out, int64_t out_len, int64_t* rows, int64_t* cols) {
+  return guarded([&] {
+    require(cfg != nullptr, "null config");
+    require(tp >= 1 && rank >= 0 && rank < tp, "bad tp rank");
+    require(cfg->num_heads % tp == 0 && cfg->hidden_dim % cfg->num_heads == 0, "heads must divide by tp");
+    require(tensor >= DSINF_T_QKV && tensor <= DSINF_T_LNF_B, "unknown tensor id");
+    const ops::ShardMap mp =
+        tensor_map(cfg->hidden_dim, cfg->num_heads, cfg->vocab_size, tp, rank, seed, layer, tensor);
+    if (rows) *rows = mp.N_local;
+    if (cols) *cols = mp.K_local;
+    if (!out) return;  // size query
+    require(out_len == mp.N_local * mp.K_local, "output buffer size mismatch");
+    float offset = 0.f;
+    tensor_amp(tensor, &offset);
+    const bool vector = mp.K_global == 1;
+    for (int64_t n = 0; n < mp.N_local; ++n) {
+      const int64_t grow = (n / mp.sec_local) * mp.sec_global + mp.row_off + (n % mp.sec_local);
+      for (int64_t k = 0; k < mp.K_local; ++k) {
+        const int64_t gcol = mp.col_off + k;
+        float v = 0.f;
+        if (grow < mp.valid_rows && gcol < mp.K_global) {
+          const float t = synth_unit(mp.base, static_cast<uint64_t>(grow * mp.K_global + gcol)) * mp.amp;
+          v = f16_bits_to_f32(f32_to_f16_bits(vector ? offset + t : t));
+        }
+        out[n * mp.K_local + k] = v;
+      }
     }
   });
 }

@@ -363,8 +363,6 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   const int row_end = min(p.rows, row_begin + p.rows_per_split);
   const int n_iters = (row_end - row_begin + kRowsPerStage - 1) / kRowsPerStage;
 
-  ptx::pdl_trigger();  // dependents may launch and start streaming their own weights
-
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.tmap);
     for (int s = 0; s < stages; ++s) {
@@ -399,6 +397,10 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
     } else {
       ptx::pdl_wait();
     }
+    // All of this CTA's weight loads are issued: let the next kernel launch and start streaming
+    // its own weights into the tail of this one (triggering at kernel start instead lets a
+    // cascade of dependents occupy SMs and steal bandwidth from the critical kernel).
+    ptx::pdl_trigger();
   } else {
     // ================= consumers
     const int cw = warp - 1;
@@ -484,6 +486,7 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
         phase ^= 1;
       }
     }
+    ptx::pdl_trigger();
     consumer_bar();  // every consumer is done reading the ring
     // partials -> smem (reuses the ring): part[b][n]
     Acc* part = reinterpret_cast<Acc*>(ring);

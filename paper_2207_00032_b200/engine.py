@@ -219,6 +219,19 @@ def launch_plan(N: int, K: int, B: int, int8: bool = False) -> capi.LaunchPlan:
     return p
 
 
+def shard_tensor(hidden: int, heads: int, vocab: int, tp: int, rank: int, layer: int, tensor: int,
+                 seed: int) -> np.ndarray:
+    """Rank `rank`'s tensor-parallel shard of a synthetic tensor (logical row-major), host-side."""
+    cfg = capi.ModelConfig(hidden, 1, heads, vocab, 2048, 2)
+    rows, cols = C.c_int64(), C.c_int64()
+    capi.check(capi.lib.dsinf_shard_tensor(C.byref(cfg), tp, rank, layer, tensor, seed, None, 0, C.byref(rows),
+                                           C.byref(cols)))
+    out = np.zeros(rows.value * cols.value, dtype=np.float32)
+    capi.check(capi.lib.dsinf_shard_tensor(C.byref(cfg), tp, rank, layer, tensor, seed,
+                                           out.ctypes.data_as(C.POINTER(C.c_float)), out.size, None, None))
+    return out.reshape(rows.value, cols.value)
+
+
 def synthetic_tensor(seed: int, layer: int, tensor: int, rows: int, cols: int) -> np.ndarray:
     out = np.zeros(rows * cols, dtype=np.float32)
     capi.check(capi.lib.dsinf_synthetic_tensor(seed, layer, tensor, rows, cols,

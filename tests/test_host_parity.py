@@ -1,0 +1,96 @@
+"""Randomised parity of the host API and the oracle against the reference headers compiled live
+(oracle/_ref; skipped where the reference tree was not available to build it).  Seeds follow the
+reference tests' style (fixed std::mt19937-like seeds, test_fusion.cpp:149)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2207_00032_b200 import infersim as I
+
+
+def test_random_schedules(ref):
+    rng = np.random.default_rng(41)
+    for _ in range(400):
+        N = int(rng.integers(1, 60000))
+        K = int(rng.integers(1, 70000))
+        dt = int(rng.choice([1, 2, 4]))
+        sm = int(rng.choice([1, 16, 108, 132, 148, 1000]))
+        rc, s6 = O.ref_derive_schedule(N, K, 1, dt, sm)
+        s = I.derive_schedule(I.GemmShape(N, K, 1, dt), I.DeviceSpec(1, 1.0, sm))
+        assert [int(s.mode), s.output_tiles, s.input_tiles, s.warps_per_block, s.kernel_count, s.pack_M] == s6
+
+
+def test_random_pack_and_exec_bit_identical(ref):
+    rng = np.random.default_rng(7)
+    for _ in range(25):
+        N, K, B = (int(v) for v in rng.integers(1, 90, 3))
+        dt = int(rng.choice([1, 2, 4]))
+        W = rng.standard_normal((N, K))
+        x = rng.standard_normal((B, K))
+        rc, s6 = O.ref_derive_schedule(N, K, B, dt, 148)
+        ref_out = O.ref_exec_reference(W, dt, s6, x, B)
+        s = O.derive_schedule(N, K, B, dt)
+        packed = I.pack_weights(W, I.GemmShape(N, K, B, dt), s.pack_M)
+        got = O.exec_sameorder(packed.data, N, K, s.pack_M, s, x, B)
+        assert np.array_equal(got, ref_out)
+        got2 = O.gemm_f64(W.astype(np.float32), x, s)  # row-major fast path, same order
+        ref32 = O.ref_exec_reference(W.astype(np.float32).astype(np.float64), dt, s6, x, B)
+        assert np.array_equal(got2, ref32)
+
+
+def _random_chain(rng):
+    n = int(rng.integers(1, 13))
+    g = I.OpGraph()
+    for i in range(n):
+        g.nodes.append(I.OpNode(f"n{i}", I.OpKind.elementwise if rng.integers(0, 2) else I.OpKind.gemm, 32, 4))
+    for i in range(n - 1):
+        e = I.GraphEdge(i, i + 1)
+        one = bool(rng.integers(0, 2))
+        for t in range(4):
+            e.tile_dep[t] = {t} if one else {0, 1, 2, 3}
+        g.edges.append(e)
+    return g
+
+
+def test_random_graph_partitions_match_reference(ref):  # test_fusion.cpp:147-205
+    rng = np.random.default_rng(41)
+    for _ in range(100):
+        g = _random_chain(rng)
+        for regime in (I.BatchRegime.small_batch, I.BatchRegime.large_batch):
+            regions = I.partition_layer(g, regime)
+            sav = I.fusion_savings(regions, g)
+            fg = I._FlatGraph(g)
+            ro = (C.c_int32 * max(1, len(g.nodes)))()
+            nr, la, by = C.c_int32(), C.c_int64(), C.c_int64()
+            rc = ref.ref_lib().ref_partition_graph(
+                fg.c.num_nodes, fg.kind, fg.tiles, fg.elems, fg.c.num_edges, fg.efrom, fg.eto, fg.dep_off, fg.cons,
+                fg.prod_off, fg.prod, 2, int(regime), ro, C.byref(nr), C.byref(la), C.byref(by))
+            assert rc == 0
+            mine = [0] * len(g.nodes)
+            for r, reg in enumerate(regions):
+                for i in reg.node_ids:
+                    mine[i] = r
+            assert mine == list(ro)[: len(g.nodes)]
+            assert (sav.launches_saved, sav.bytes_saved) == (la.value, by.value)
+            # legality: every internal edge is fusable; greedy maximality in the small-batch regime
+            for reg in regions:
+                for e in g.edges:
+                    if e.from_ in reg.node_ids and e.to in reg.node_ids:
+                        assert I.fusable(g, e)
+
+
+def test_misordered_graph_rejected():  # test_fusion.cpp:253
+    g = I.OpGraph([I.OpNode("a", I.OpKind.elementwise, 8, 2), I.OpNode("b", I.OpKind.elementwise, 8, 2)],
+                  [I.GraphEdge(1, 0, {0: {0}, 1: {1}})])
+    with pytest.raises(I.ConfigError):
+        I.partition_layer(g, I.BatchRegime.small_batch)
+
+
+def test_fusability_rules():  # test_fusion.cpp:66-101
+    g = I.OpGraph([I.OpNode("p", I.OpKind.elementwise, 16, 4), I.OpNode("c", I.OpKind.reduction, 16, 4)])
+    assert I.fusable(g, I.GraphEdge(0, 1, {t: {t} for t in range(4)}))
+    assert not I.fusable(g, I.GraphEdge(0, 1, {0: {0, 1, 2, 3}, 1: {1}, 2: {2}, 3: {3}}))
+    assert not I.fusable(g, I.GraphEdge(0, 1, {}))  # missing consumer tiles block fusion
+    assert I.fusable(g, I.GraphEdge(0, 1, {i * 2 + j: {j * 2 + i} for i in range(2) for j in range(2)}))

@@ -1,0 +1,73 @@
+"""CPU checks of the oracle's numerics building blocks and of the host-side synthetic generator."""
+import numpy as np
+
+from oracle import oracle as O
+from paper_2207_00032_b200 import _capi as capi
+from paper_2207_00032_b200 import engine as E
+
+
+def test_fp16_rounding_matches_numpy():
+    rng = np.random.default_rng(3)
+    vals = np.concatenate([
+        rng.standard_normal(20000).astype(np.float32) * 10.0,
+        rng.standard_normal(5000).astype(np.float32) * 1e-5,     # subnormal half range
+        np.array([65504, 65519.99, 65520, 1e6, -1e6, 0.0, -0.0, 2.0 ** -24, 2.0 ** -25, 3 * 2.0 ** -26],
+                 dtype=np.float32),
+        (np.arange(-2048, 2048, dtype=np.float32) + 0.5) * 2.0 ** -10,   # exact ties
+    ])
+    ref = vals.astype(np.float16).view(np.uint16)
+    got = np.array([O.f32_to_f16_bits(float(v)) for v in vals], dtype=np.uint16)
+    assert np.array_equal(got, ref)
+
+
+def test_host_generator_matches_oracle_generator():
+    seed = 1234
+    host = E.synthetic_tensor(seed, 3, capi.T_QKV, 4, 257)
+    for flat in (0, 1, 100, 4 * 257 - 1):
+        u = O.synth_unit(seed, 3, capi.T_QKV, flat)
+        w = np.float32(u) * np.float32(0.034641016)
+        assert host.ravel()[flat] == np.float32(w).astype(np.float16).astype(np.float32)
+    g = E.synthetic_tensor(seed, 0, capi.T_LN1_G, 1, 64)
+    assert np.all(np.abs(g - 1.0) <= 0.1001)
+
+
+def test_quantisation_formula():
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((7, 301)) * 0.3).astype(np.float16).astype(np.float32)
+    x[3] = 0.0
+    q, s = O.quant_rows(x)
+    mx = np.abs(x).max(axis=1)
+    exp_s = np.where(mx > 0, (mx / np.float32(127.0)).astype(np.float32), np.float32(1.0))
+    assert np.array_equal(s, exp_s)
+    exp_q = np.clip(np.rint(x / s[:, None]), -127, 127).astype(np.int8)
+    assert np.array_equal(q, exp_q)
+    assert np.all(q[3] == 0) and s[3] == 1.0
+    assert np.abs(q).max() == 127
+
+
+def test_int8_gemm_exact():
+    rng = np.random.default_rng(9)
+    wq = rng.integers(-127, 128, (33, 515)).astype(np.int8)
+    xq = rng.integers(-127, 128, (5, 515)).astype(np.int8)
+    ws = rng.random(33).astype(np.float32)
+    xs = rng.random(5).astype(np.float32)
+    acc, y = O.gemm_i8(wq, ws, xq, xs)
+    exact = xq.astype(np.int64) @ wq.astype(np.int64).T
+    assert np.array_equal(acc, exact.astype(np.int32))
+    assert np.array_equal(y, (acc.astype(np.float32) * xs[:, None]).astype(np.float32) * ws[None, :])
+
+
+def test_oracle_model_is_deterministic_and_tp_consistent():
+    """TP sharding of the oracle (per-rank schedules, rank-ordered partial sums) stays within
+    fp32-reduction noise of the unsharded model (fp16 path)."""
+    cfg = dict(hidden=256, layers=2, heads=8, vocab=500, batch=2, max_ctx=8)
+    outs = []
+    for tp in (1, 2, 4):
+        m = O.OracleModel(**cfg, tp=tp)
+        lg = None
+        for pos, tok in enumerate([[1, 2], [3, 4], [5, 6]]):
+            lg, _ = m.step(np.array(tok, dtype=np.int32), pos)
+        outs.append(lg)
+        m.close()
+    for lg in outs[1:]:
+        assert np.abs(lg - outs[0]).max() < 2e-2 * outs[0].std()
