@@ -187,7 +187,7 @@ typedef struct dsinf_runtime_config {
   float ln_eps;
   float rope_base;
   int32_t device;       /* CUDA device ordinal */
-  int32_t reserved;
+  int32_t use_step_kernel; /* TP = 1: run each decode step as ONE persistent kernel */
 } dsinf_runtime_config;
 
 typedef struct dsinf_model dsinf_model;
@@ -230,6 +230,11 @@ typedef struct dsinf_model_info {
   int32_t graph_ready;
 } dsinf_model_info;
 int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out);
+/* Per-CTA phase timeline of the last persistent step (built with DSINF_STEP_TRACE=1):
+ * [grid][phases][4] globaltimer ns (wait begins, wait satisfied, phase done, producer's last
+ * weight load issued).  out == NULL queries the length; returns DSINF_ERR_CONFIG if not traced. */
+int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* needed, int32_t* grid,
+                           int32_t* phases);
 /* Bytes per step for an arbitrary position (ctx = pos + 1). */
 int64_t dsinf_model_bytes_per_step(const dsinf_model* m, int64_t pos);
 /* Copy one synthetic weight tensor of layer `layer` in logical row-major fp32 form

@@ -103,7 +103,7 @@ class RuntimeConfig(C.Structure):
     _fields_ = [("batch", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_mode", C.c_int32),
                 ("use_cuda_graph", C.c_int32), ("use_pdl", C.c_int32), ("max_ctx", C.c_int64),
                 ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float), ("device", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("use_step_kernel", C.c_int32)]
 
 
 class ModelInfo(C.Structure):
@@ -168,6 +168,7 @@ SIGNATURES = {
     "dsinf_model_read_tokens": (C.c_int, [vp, P(i32), P(i32), i64, vp]),
     "dsinf_model_get_info": (C.c_int, [vp, P(ModelInfo)]),
     "dsinf_model_bytes_per_step": (i64, [vp, i64]),
+    "dsinf_model_step_trace": (C.c_int, [vp, P(u64), i64, P(i64), P(i32), P(i32)]),
     "dsinf_synthetic_tensor": (C.c_int, [u64, i32, i32, i64, i64, P(C.c_float)]),
     "dsinf_shard_tensor": (C.c_int, [P(ModelConfig), i32, i32, i32, i32, u64, P(C.c_float), i64, P(i64), P(i64)]),
     "dsinf_nccl_get_unique_id": (C.c_int, [P(C.c_uint8)]),

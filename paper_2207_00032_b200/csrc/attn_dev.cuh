@@ -1,0 +1,137 @@
+// Device building block of decode attention (paper region 2; fusion.hpp:271-277):
+// one chunk of context positions of one (batch row, head) reduced to an online-softmax partial
+// (max, sum, unnormalised output).  Shared by the standalone attention kernel (chunks merged
+// in-cluster through DSMEM) and the persistent step kernel (chunks merged through L2).
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+#include <cuda_fp16.h>
+
+#include "ops.cuh"
+#include "ptx.cuh"
+
+namespace dsinf {
+namespace ops {
+namespace dev {
+
+constexpr int kAttnThreads = 128;
+constexpr int kAttnUnroll = 4;
+
+__device__ __forceinline__ void h8_to_f(const uint4& u, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __half22float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+
+template <int TPP>
+__host__ __device__ constexpr size_t attn_scratch_floats(int d) {
+  return static_cast<size_t>(kAttnThreads / TPP) * d + 2 * (kAttnThreads / TPP) + d + 4;
+}
+
+// Computes the partial of positions [j0, j1) into co[0..d) (output, unnormalised) and
+// cst[0] = max, cst[1] = sum.  Called by kAttnThreads threads (tid in [0, 128)); `bar` is the
+// barrier among them.  Loads use ld.global.cg: q / K / V may have been written by other CTAs.
+template <int TPP, class Bar>
+__device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1, int tid, float* scratch,
+                           Bar bar) {
+  constexpr int PPR = kAttnThreads / TPP;
+  const int d = p.d;
+  float* so = scratch;       // [PPR][d]
+  float* sm = so + PPR * d;  // [PPR]
+  float* sl = sm + PPR;      // [PPR]
+  float* co = sl + PPR;      // [d]
+  float* cst = co + d;       // [2]
+  const int slot = tid / TPP, lane_in = tid % TPP;
+  const int dim0 = lane_in * 8;
+  const bool has_dims = dim0 < d;
+  const int len = max(0, j1 - j0);
+  const int rounds = (len + PPR - 1) / PPR;
+  const int hd = p.H * d;
+  float q[8];
+  if (has_dims) {
+    const uint4 qu = __ldcg(reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(b) * hd + head * d + dim0));
+    h8_to_f(qu, q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] *= p.scale;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = 0.f;
+  }
+  const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d + dim0;
+  const __half* kb = p.kc + kv_base;
+  const __half* vb = p.vc + kv_base;
+  float m = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = 0.f;
+  for (int r0 = 0; r0 < rounds; r0 += kAttnUnroll) {  // warp-uniform trip count
+    uint4 kr[kAttnUnroll], vr[kAttnUnroll];
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      const int j = j0 + (r0 + u) * PPR + slot;
+      if (j < j1 && has_dims) {
+        kr[u] = __ldcg(reinterpret_cast<const uint4*>(kb + static_cast<size_t>(j) * d));
+        vr[u] = __ldcg(reinterpret_cast<const uint4*>(vb + static_cast<size_t>(j) * d));
+      } else {
+        kr[u] = make_uint4(0, 0, 0, 0);
+        vr[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      float kf[8];
+      h8_to_f(kr[u], kf);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = fmaf(q[i], kf[i], s);
+#pragma unroll
+      for (int off = TPP / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const int j = j0 + (r0 + u) * PPR + slot;
+      if (j < j1) {
+        const float mn = fmaxf(m, s);
+        const float corr = expf(m - mn);
+        const float pj = expf(s - mn);
+        float vf[8];
+        h8_to_f(vr[u], vf);
+        l = l * corr + pj;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i] * corr);
+        m = mn;
+      }
+    }
+  }
+  if (has_dims) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) so[slot * d + dim0 + i] = o[i];
+  }
+  if (lane_in == 0) {
+    sm[slot] = m;
+    sl[slot] = l;
+  }
+  bar();
+  float M = -INFINITY;
+  for (int s = 0; s < PPR; ++s) M = fmaxf(M, sm[s]);
+  for (int i = tid; i < d; i += kAttnThreads) {
+    float acc = 0.f;
+    for (int s = 0; s < PPR; ++s) {
+      const float w = sm[s] == -INFINITY ? 0.f : expf(sm[s] - M);
+      acc = fmaf(w, so[s * d + i], acc);
+    }
+    co[i] = acc;
+  }
+  if (tid == 0) {
+    float L = 0.f;
+    for (int s = 0; s < PPR; ++s) L += sm[s] == -INFINITY ? 0.f : sl[s] * expf(sm[s] - M);
+    cst[0] = M;
+    cst[1] = L;
+  }
+  bar();
+}
+
+}  // namespace dev
+}  // namespace ops
+}  // namespace dsinf

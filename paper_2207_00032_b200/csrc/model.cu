@@ -27,6 +27,7 @@
 #include "nccl_dl.h"
 #include "ops.cuh"
 #include "sbi_gemm.cuh"
+#include "step_kernel.cuh"
 #include "synth.h"
 
 namespace dsinf {
@@ -101,6 +102,7 @@ struct dsinf_model {
   int64_t weight_bytes = 0;
   int64_t kernels_per_step = 0;
   int attn_chunks = 1;
+  dsinf::step::StepProgram step_prog;  // persistent whole-step kernel (TP = 1)
 
   void* alloc(size_t bytes) {
     void* p = nullptr;
@@ -284,6 +286,116 @@ gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int
   return p;
 }
 
+ops::EmbedParams embed_params(const Model& m, const Shard& sh) {
+  ops::EmbedParams e{};
+  e.wte = sh.wte;
+  e.prompt = m.prompt;
+  e.prompt_len = m.prompt_len;
+  e.prompt_ld = m.prompt_cap;
+  e.next_tok = m.next_tok;
+  e.pos = m.pos;
+  e.hist = m.hist;
+  e.max_ctx = m.max_ctx;
+  e.res = sh.res[0];
+  e.B = m.B;
+  e.h = static_cast<int>(m.h);
+  e.V = static_cast<int>(m.V);
+  return e;
+}
+
+ops::AttnParams attn_params(const Model& m, const Shard& sh, int l) {
+  ops::AttnParams a{};
+  const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+  a.q = sh.q;
+  a.kc = sh.kc + l * layer_kv;
+  a.vc = sh.vc + l * layer_kv;
+  a.pos = m.pos;
+  a.out = sh.a;
+  a.B = m.B;
+  a.H = static_cast<int>(m.Hl);
+  a.d = static_cast<int>(m.d);
+  a.max_seq = m.max_ctx;
+  a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+  return a;
+}
+
+// The persistent whole-step kernel's program (TP = 1): one fp32 residual stream updated in place by
+// the attn-out / MLP-down epilogues (EPI_RESID), LayerNorm prologues without a pending delta.
+void build_step_program(Model& m) {
+  Shard& sh = m.shards[0];
+  step::StepDesc D;
+  D.B = m.B;
+  D.L = static_cast<int>(m.L);
+  D.H = static_cast<int>(m.Hl);
+  D.d = static_cast<int>(m.d);
+  D.max_ctx = m.max_ctx;
+  D.V = static_cast<int>(m.V);
+  D.Vl = static_cast<int>(m.Vl);
+  D.int8 = m.int8;
+  float* r = sh.res[0];
+  const int h = static_cast<int>(m.h), HD = static_cast<int>(m.Hl * m.d), Fl = static_cast<int>(m.Fl);
+  const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = sh.layers[l];
+    gemm::Params q = base_params(m, w.wqkv, w.sqkv, 3 * HD, h, m.int8);
+    q.pro = gemm::PRO_LN;
+    q.res_in = r;
+    q.ln_g = w.ln1g;
+    q.ln_b = w.ln1b;
+    q.epi = gemm::EPI_QKV;
+    q.bias = w.bqkv;
+    q.q_out = sh.q;
+    q.k_cache = sh.kc + l * layer_kv;
+    q.v_cache = sh.vc + l * layer_kv;
+    q.rope = m.rope;
+    q.pos = m.pos;
+    q.heads = static_cast<int>(m.Hl);
+    q.head_dim = static_cast<int>(m.d);
+    q.max_seq = m.max_ctx;
+    gemm::Params o = base_params(m, w.wo, w.so, h, HD, m.int8);
+    o.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    o.x = sh.a;
+    o.x_ld = HD;
+    o.epi = gemm::EPI_RESID;
+    o.out = r;
+    o.bias = w.bo;
+    gemm::Params u = base_params(m, w.wup, w.sup, Fl, h, m.int8);
+    u.pro = gemm::PRO_LN;
+    u.res_in = r;
+    u.ln_g = w.ln2g;
+    u.ln_b = w.ln2b;
+    u.epi = gemm::EPI_GELU_F16;
+    u.bias = w.bup;
+    u.out = sh.u;
+    gemm::Params dn = base_params(m, w.wdown, w.sdown, h, Fl, m.int8);
+    dn.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    dn.x = sh.u;
+    dn.x_ld = Fl;
+    dn.epi = gemm::EPI_RESID;
+    dn.out = r;
+    dn.bias = w.bdown;
+    D.gemms.push_back(q);
+    D.gemms.push_back(o);
+    D.gemms.push_back(u);
+    D.gemms.push_back(dn);
+    D.attn.push_back(attn_params(m, sh, l));
+  }
+  gemm::Params lm = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), h, false);
+  lm.pro = gemm::PRO_LN;
+  lm.res_in = r;
+  lm.ln_g = sh.lnfg;
+  lm.ln_b = sh.lnfb;
+  lm.epi = gemm::EPI_F32;
+  lm.out = sh.logits;
+  D.gemms.push_back(lm);
+  D.embed = embed_params(m, sh);
+  D.logits = sh.logits;
+  D.next_tok = m.next_tok;
+  D.hist = m.hist;
+  D.pos = m.pos;
+  m.step_prog.build(D);
+}
+
 struct Enqueuer {
   Model& m;
   cudaStream_t s;
@@ -427,6 +539,11 @@ struct Enqueuer {
   }
 
   void step() {
+    if (m.step_prog.ready()) {  // TP = 1: the whole step is one persistent kernel
+      m.step_prog.launch(s);
+      ++launches;
+      return;
+    }
     for (Shard& sh : m.shards) {
       ops::EmbedParams e{};
       e.wte = sh.wte;
@@ -588,6 +705,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     DSINF_CUDA_CHECK(cudaMemsetAsync(m->pos, 0, sizeof(int), s));
     for (auto& sh : m->shards) build_shard(*m, sh, s);
     DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (m->t == 1 && rt->use_step_kernel) build_step_program(*m);
     *out = m.release();
   });
 }
@@ -608,6 +726,7 @@ static void set_prompt_common(dsinf_model* m, const int32_t* src, int64_t prompt
   }
   (void)bytes;
   m->prompt_len = static_cast<int>(prompt_len);
+  if (m->step_prog.ready()) m->step_prog.set_embed(embed_params(*m, m->shards[0]));
   DSINF_CUDA_CHECK(cudaMemsetAsync(m->pos, 0, sizeof(int), s));
   DSINF_CUDA_CHECK(cudaMemsetAsync(m->next_tok, 0, sizeof(int32_t) * m->B, s));
   m->host_pos = 0;
@@ -660,6 +779,20 @@ int dsinf_decode_step_host(dsinf_model* m, const int32_t* tokens_in, int32_t* to
     if (rc != DSINF_OK) throw CudaError(dsinf_last_error());
     DSINF_CUDA_CHECK(cudaMemcpyAsync(tokens_out, m->next_tok, sizeof(int32_t) * m->B, cudaMemcpyDeviceToHost, s));
     DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* needed, int32_t* grid,
+                           int32_t* phases) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    require(m->step_prog.ready(), "the persistent step kernel is not in use");
+    const size_t n = m->step_prog.trace(nullptr, 0);
+    require(n > 0, "step trace disabled (set DSINF_STEP_TRACE=1 before model creation)");
+    if (needed) *needed = static_cast<int64_t>(n);
+    if (grid) *grid = m->step_prog.grid();
+    if (phases) *phases = m->step_prog.phases();
+    if (out) m->step_prog.trace(reinterpret_cast<unsigned long long*>(out), static_cast<size_t>(len));
   });
 }
 

@@ -35,6 +35,7 @@ enum Epilogue : int {
   EPI_F16 = 1,       // out fp16 = y (+ bias)
   EPI_GELU_F16 = 2,  // out fp16 = gelu(y + bias)
   EPI_QKV = 3,       // q/k/v = y + bias, RoPE on q,k, q -> q_out, k/v -> KV cache at pos
+  EPI_RESID = 4,     // out fp32 += y + bias (residual stream; one writer per column)
 };
 
 struct Params {

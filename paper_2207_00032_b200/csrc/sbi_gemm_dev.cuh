@@ -1,0 +1,479 @@
+// Device building blocks of SBI-GeMM (infersim gemm.hpp:147-202) shared by the
+// standalone kernel (sbi_gemm.cu) and the persistent decode-step kernel (step_kernel.cu):
+//   * Deep-Fusion prologues that fill a CTA's x slice in shared memory (LayerNorm with the
+//     residual add folded in, per-token int8 quantisation, plain fp16 / int8 loads);
+//   * the consumer loop over the TMA ring (warp MMAs on the reference packed layout);
+//   * the epilogues (bias, GeLU, residual add, RoPE + KV-cache append, fp16/fp32 stores).
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <type_traits>
+
+#include "ptx.cuh"
+#include "sbi_gemm.cuh"
+
+namespace dsinf {
+namespace gemm {
+namespace dev {
+
+struct Header {
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
+  float xscale[kMaxB];
+  float mean[kMaxB];
+  float rstd[kMaxB];
+  float red[8];
+  int flag[4];
+};
+static_assert(sizeof(Header) <= kHeaderBytes, "header too large");
+
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ int next_pow2(int b) {
+  int p = 1;
+  while (p < b) p <<= 1;
+  return p;
+}
+
+// Consumer-thread -> (batch row, lane-in-row) map used by every per-row reduction: `tpr`
+// consecutive consumer threads own one row.
+struct RowMap {
+  int tpr, b, j;
+  bool active;
+  __device__ __forceinline__ RowMap(int B, int ctid) {
+    tpr = 128 / next_pow2(B);
+    b = ctid / tpr;
+    j = ctid % tpr;
+    active = b < B;
+  }
+};
+
+// Sum (or max) over the `tpr` threads of a row.  All threads of the row get the same bits
+// (symmetric butterfly, then an in-order warp sum), so results are run-to-run deterministic.
+template <bool kMax>
+__device__ __forceinline__ float row_reduce(float v, int tpr, float* scratch, int cw, int lane) {
+  const int width = tpr < 32 ? tpr : 32;
+  for (int o = width >> 1; o > 0; o >>= 1) {
+    const float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, u) : v + u;
+  }
+  if (tpr > 32) {
+    consumer_bar();
+    if (lane == 0) scratch[cw] = v;
+    consumer_bar();
+    const int wpr = tpr >> 5;
+    const int first = (cw / wpr) * wpr;
+    float t = scratch[first];
+    for (int i = 1; i < wpr; ++i) t = kMax ? fmaxf(t, scratch[first + i]) : t + scratch[first + i];
+    v = t;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Per-token int8: q = clamp(rint(x / s), -127, 127) with IEEE division (bit-exact vs oracle).
+__device__ __forceinline__ uint32_t quant_byte(float x, float scale) {
+  int q = __float2int_rn(__fdiv_rn(x, scale));
+  q = max(-127, min(127, q));
+  return static_cast<uint32_t>(q) & 0xffu;
+}
+
+__device__ __forceinline__ float act_scale(float maxabs) {
+  return maxabs > 0.0f ? __fdiv_rn(maxabs, 127.0f) : 1.0f;
+}
+
+// Residual-stream element: r + (delta + delta_bias)  (delta optional).
+struct ResidualView {
+  const float* r;
+  const float* d;
+  const __half* db;
+  int K;
+  __device__ __forceinline__ float4 load4(int b, int k) const {
+    float4 v = __ldcg(reinterpret_cast<const float4*>(r + static_cast<size_t>(b) * K + k));
+    if (d) {
+      float4 t = __ldcg(reinterpret_cast<const float4*>(d + static_cast<size_t>(b) * K + k));
+      if (db) {
+        const __half2 b01 = *reinterpret_cast<const __half2*>(db + k);
+        const __half2 b23 = *reinterpret_cast<const __half2*>(db + k + 2);
+        t.x = __fadd_rn(t.x, __low2float(b01));
+        t.y = __fadd_rn(t.y, __high2float(b01));
+        t.z = __fadd_rn(t.z, __low2float(b23));
+        t.w = __fadd_rn(t.w, __high2float(b23));
+      }
+      v.x = __fadd_rn(v.x, t.x);
+      v.y = __fadd_rn(v.y, t.y);
+      v.z = __fadd_rn(v.z, t.z);
+      v.w = __fadd_rn(v.w, t.w);
+    }
+    return v;
+  }
+};
+
+__device__ __forceinline__ float ln_apply(float v, float mean, float rstd, const __half* g, const __half* bta,
+                                          int k) {
+  return (v - mean) * rstd * __half2float(g[k]) + __half2float(bta[k]);
+}
+
+// ------------------------------------------------------------------ per-row statistics
+// LayerNorm statistics of the full row (single shifted pass) -> hd.mean / hd.rstd; with int8
+// weights also the per-token scale of the fp16-rounded normalised row -> hd.xscale.
+// `write_res` stores the residual (r + delta + bias) once (one CTA per launch / phase).
+template <bool kInt8>
+__device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int lane, bool write_res) {
+  const RowMap rm(p.B, ctid);
+  const int K = p.K;
+  const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
+  float c0 = 0.f, s1 = 0.f, s2 = 0.f;
+  if (rm.active) {
+    c0 = rv.load4(rm.b, 0).x;  // shift for a cancellation-free single pass
+#pragma unroll 4
+    for (int c = rm.j; c < K / 4; c += rm.tpr) {
+      const float4 v = rv.load4(rm.b, 4 * c);
+      if (write_res) *reinterpret_cast<float4*>(p.res_out + static_cast<size_t>(rm.b) * K + 4 * c) = v;
+      const float d0 = v.x - c0, d1 = v.y - c0, d2 = v.z - c0, d3 = v.w - c0;
+      s1 += (d0 + d1) + (d2 + d3);
+      s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+  }
+  s1 = row_reduce<false>(s1, rm.tpr, hd.red, cw, lane);
+  s2 = row_reduce<false>(s2, rm.tpr, hd.red, cw, lane);
+  const float inv_k = 1.0f / static_cast<float>(K);
+  const float m1 = s1 * inv_k;
+  const float var = fmaxf(s2 * inv_k - m1 * m1, 0.0f);
+  const float mean = c0 + m1;
+  const float rstd = 1.0f / sqrtf(var + p.ln_eps);
+  if (kInt8) {
+    float mx = 0.f;
+    if (rm.active) {
+#pragma unroll 2
+      for (int c = rm.j; c < K / 4; c += rm.tpr) {
+        const float4 v = rv.load4(rm.b, 4 * c);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float y = __half2float(__float2half_rn(ln_apply(vv[i], mean, rstd, p.ln_g, p.ln_b, 4 * c + i)));
+          mx = fmaxf(mx, fabsf(y));
+        }
+      }
+    }
+    mx = row_reduce<true>(mx, rm.tpr, hd.red, cw, lane);
+    if (rm.active && rm.j == 0) hd.xscale[rm.b] = act_scale(mx);
+  }
+  if (rm.active && rm.j == 0) {
+    hd.mean[rm.b] = mean;
+    hd.rstd[rm.b] = rstd;
+  }
+}
+
+// Per-token scale of an fp16 activation row (PRO_QUANT) -> hd.xscale.
+__device__ __forceinline__ void quant_row_scale(const Params& p, Header& hd, int ctid, int cw, int lane) {
+  const RowMap rm(p.B, ctid);
+  const __half* x = static_cast<const __half*>(p.x);
+  float mx = 0.f;
+  if (rm.active)
+  {
+    const __half* row = x + static_cast<size_t>(rm.b) * p.x_ld;
+    const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 7) == 0;
+    if (vec) {
+#pragma unroll 4
+      for (int c = rm.j; c < p.K / 4; c += rm.tpr) {
+        const uint2 u = __ldcg(reinterpret_cast<const uint2*>(row + 4 * c));
+        const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x);
+        const __half2 h23 = *reinterpret_cast<const __half2*>(&u.y);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(__low2float(h01)), fabsf(__high2float(h01))),
+                             fmaxf(fabsf(__low2float(h23)), fabsf(__high2float(h23)))));
+      }
+      for (int k = (p.K / 4) * 4 + rm.j; k < p.K; k += rm.tpr) mx = fmaxf(mx, fabsf(__half2float(__ldcg(row + k))));
+    } else {
+      for (int k = rm.j; k < p.K; k += rm.tpr) mx = fmaxf(mx, fabsf(__half2float(__ldcg(row + k))));
+    }
+  }
+  mx = row_reduce<true>(mx, rm.tpr, hd.red, cw, lane);
+  if (rm.active && rm.j == 0) hd.xscale[rm.b] = act_scale(mx);
+}
+
+// ------------------------------------------------------------------ x slice
+// Writes packed rows [row0, row0 + nrows) of x into sx[b * xrw + w] (w = row - row0), one 32-bit
+// word per (row, b) holding M = 2 (fp16) or 4 (int8) consecutive k.  Requires the statistics
+// of ln_row_stats / quant_row_scale in `hd` for PRO_LN / PRO_QUANT.
+template <bool kInt8>
+__device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, int row0, int nrows, int ctid) {
+  const int K = p.K;
+  const int M = kInt8 ? 4 : 2;
+  const int xrw = p.x_row_words;
+  if (p.pro == PRO_LN) {
+    const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
+    for (int b = 0; b < p.B; ++b) {
+      const float mean = hd.mean[b], rstd = hd.rstd[b];
+#pragma unroll 4
+      for (int w = ctid; w < nrows; w += 128) {
+        const int k = (row0 + w) * M;
+        uint32_t word = 0;
+        if (k < K) {  // K % 8 == 0 on this path
+          const float4 v = rv.load4(b, k & ~3);
+          if (!kInt8) {
+            const float va = (k & 2) ? v.z : v.x, vb = (k & 2) ? v.w : v.y;
+            word = pack_h2(ln_apply(va, mean, rstd, p.ln_g, p.ln_b, k), ln_apply(vb, mean, rstd, p.ln_g, p.ln_b, k + 1));
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            const float scale = hd.xscale[b];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float y = __half2float(__float2half_rn(ln_apply(vv[i], mean, rstd, p.ln_g, p.ln_b, k + i)));
+              word |= quant_byte(y, scale) << (8 * i);
+            }
+          }
+        }
+        sx[b * xrw + w] = word;
+      }
+    }
+  } else if (p.pro == PRO_F16) {
+    const __half* x = static_cast<const __half*>(p.x);
+    const bool vec = (p.x_ld % 2) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
+    for (int b = 0; b < p.B; ++b)
+      for (int w = ctid; w < nrows; w += 128) {
+        const int k = (row0 + w) * 2;
+        uint32_t word = 0;
+        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+        if (k + 1 < K && vec) {
+          word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
+        } else if (k < K) {
+          const __half lo = __ldcg(x + base);
+          const __half hi = (k + 1 < K) ? __ldcg(x + base + 1) : __float2half(0.f);
+          word = static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
+        }
+        sx[b * xrw + w] = word;
+      }
+  } else if (p.pro == PRO_I8) {
+    const int8_t* x = static_cast<const int8_t*>(p.x);
+    const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
+    for (int b = 0; b < p.B; ++b)
+      for (int w = ctid; w < nrows; w += 128) {
+        const int k = (row0 + w) * 4;
+        uint32_t word = 0;
+        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+        if (k + 3 < K && vec) {
+          word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
+        } else {
+          for (int i = 0; i < 4; ++i)
+            if (k + i < K) word |= (static_cast<uint32_t>(static_cast<uint8_t>(__ldcg(reinterpret_cast<const signed char*>(x) + base + i)))) << (8 * i);
+        }
+        sx[b * xrw + w] = word;
+      }
+  } else {  // PRO_QUANT
+    const __half* x = static_cast<const __half*>(p.x);
+    const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 7) == 0;
+    for (int b = 0; b < p.B; ++b) {
+      const float scale = hd.xscale[b];
+#pragma unroll 4
+      for (int w = ctid; w < nrows; w += 128) {
+        const int k = (row0 + w) * 4;
+        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+        uint32_t word = 0;
+        if (vec && k + 3 < K) {
+          const uint2 u = __ldcg(reinterpret_cast<const uint2*>(x + base));
+          const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x);
+          const __half2 h23 = *reinterpret_cast<const __half2*>(&u.y);
+          word = quant_byte(__low2float(h01), scale) | (quant_byte(__high2float(h01), scale) << 8) |
+                 (quant_byte(__low2float(h23), scale) << 16) | (quant_byte(__high2float(h23), scale) << 24);
+        } else {
+          for (int i = 0; i < 4; ++i)
+            if (k + i < K) word |= quant_byte(__half2float(__ldcg(x + base + i)), scale) << (8 * i);
+        }
+        sx[b * xrw + w] = word;
+      }
+    }
+  }
+  (void)M;
+}
+
+// ------------------------------------------------------------------ consumer loop
+// Accumulates `n_iters` ring stages into acc[j][bt][*] (warp `cw` owns 32 output columns).
+// The ring position (s, phase) persists across calls.  Inside a k-step of 8 packed rows the MMA
+// k-slot t reads smem row 2t (t+4 reads 2t+1), a k permutation applied to both operands that
+// keeps every fragment read conflict-free under the 128-byte TMA swizzle.
+template <bool kInt8, int kNB8>
+struct Consumer {
+  using Acc = typename std::conditional<kInt8, int, float>::type;
+  Acc acc[2][kNB8][4];
+  uint32_t aoff[2][2][2];  // [j][h][par]
+  int g, t;
+
+  __device__ __forceinline__ void init(int lane) {
+    g = lane >> 2;
+    t = lane & 3;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          const int r = 2 * t + par;
+          const int c = 16 * j + 8 * h + g;
+          aoff[j][h][par] = r * 128 + (((c >> 2) ^ r) << 4) + (c & 3) * 4;
+        }
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int bt = 0; bt < kNB8; ++bt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][bt][e] = 0;
+  }
+  __device__ __forceinline__ void run(const uint8_t* ring, Header& hd, int stages, int& s, uint32_t& phase,
+                                      int n_iters, const uint32_t* sx, int xrw, int B, int cw, int lane) {
+    const uint32_t* xrow[kNB8];
+    bool xvalid[kNB8];
+#pragma unroll
+    for (int bt = 0; bt < kNB8; ++bt) {
+      xvalid[bt] = bt * 8 + g < B;
+      xrow[bt] = sx + (bt * 8 + g) * xrw + 2 * t;
+    }
+    const uint8_t* wbox = ring + cw * kBoxBytes;
+    for (int it = 0; it < n_iters; ++it) {
+      ptx::mbar_wait(&hd.full[s], phase);
+      const uint8_t* sw = wbox + s * kStageBytes;
+      const int xr0 = it * kRowsPerStage;
+#pragma unroll
+      for (int ks = 0; ks < kRowsPerStage / 8; ++ks) {
+        uint32_t b0[kNB8], b1[kNB8];
+#pragma unroll
+        for (int bt = 0; bt < kNB8; ++bt) {
+          uint2 v = make_uint2(0u, 0u);
+          if (xvalid[bt]) v = *reinterpret_cast<const uint2*>(xrow[bt] + xr0 + ks * 8);
+          b0[bt] = v.x;
+          b1[bt] = v.y;
+        }
+        const uint8_t* a = sw + ks * 8 * 128;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][0]);
+          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][0]);
+          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][1]);
+          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
+#pragma unroll
+          for (int bt = 0; bt < kNB8; ++bt) {
+            if constexpr (kInt8)
+              ptx::mma_s8(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
+            else
+              ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  // part[b * ld + n] for this warp's 32 columns (n relative to the CTA tile).
+  __device__ __forceinline__ void store(Acc* part, int ld, int B, int cw) const {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int bt = 0; bt < kNB8; ++bt) {
+        const int n = cw * kWarpCols + j * 16 + g;
+        const int b = bt * 8 + 2 * t;
+        if (b < B) {
+          part[b * ld + n] = acc[j][bt][0];
+          part[b * ld + n + 8] = acc[j][bt][2];
+        }
+        if (b + 1 < B) {
+          part[(b + 1) * ld + n] = acc[j][bt][1];
+          part[(b + 1) * ld + n + 8] = acc[j][bt][3];
+        }
+      }
+  }
+};
+
+// ------------------------------------------------------------------ epilogue
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+
+__device__ __forceinline__ void dequant_pair(const Params& p, const Header& hd, int b, int n, int s0, int s1,
+                                             float& y0, float& y1) {
+  const float xs = hd.xscale[b];
+  y0 = __fmul_rn(__fmul_rn(static_cast<float>(s0), xs), p.w_scale[n]);
+  y1 = (n + 1 < p.N) ? __fmul_rn(__fmul_rn(static_cast<float>(s1), xs), p.w_scale[n + 1]) : 0.f;
+}
+
+__device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, float y0, float y1, bool has1) {
+  if (p.bias) {
+    y0 = __fadd_rn(y0, __half2float(p.bias[n]));
+    if (has1) y1 = __fadd_rn(y1, __half2float(p.bias[n + 1]));
+  }
+  switch (p.epi) {
+    case EPI_F32: {
+      float* o = static_cast<float*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
+      if (has1 && ((reinterpret_cast<uintptr_t>(o) & 7) == 0)) {
+        *reinterpret_cast<float2*>(o) = make_float2(y0, y1);
+      } else {
+        o[0] = y0;
+        if (has1) o[1] = y1;
+      }
+      break;
+    }
+    case EPI_RESID: {  // residual stream += y + bias (fp32, this column's only writer)
+      float* o = static_cast<float*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
+      o[0] = __fadd_rn(__ldcg(o), y0);
+      if (has1) o[1] = __fadd_rn(__ldcg(o + 1), y1);
+      break;
+    }
+    case EPI_F16:
+    case EPI_GELU_F16: {
+      if (p.epi == EPI_GELU_F16) {
+        y0 = gelu_tanh(y0);
+        y1 = gelu_tanh(y1);
+      }
+      __half* o = static_cast<__half*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
+      if (has1 && ((reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
+        *reinterpret_cast<__half2*>(o) = __floats2half2_rn(y0, y1);
+      } else {
+        o[0] = __float2half_rn(y0);
+        if (has1) o[1] = __float2half_rn(y1);
+      }
+      break;
+    }
+    case EPI_QKV: {
+      // column n (even) -> section (0 q, 1 k, 2 v), head, dim i; (i, i+1) is a rotary pair
+      const int hd = p.heads * p.head_dim;
+      const int sec = n / hd;
+      const int rem = n - sec * hd;
+      const int head = rem / p.head_dim;
+      const int i = rem - head * p.head_dim;
+      const int pos = *p.pos;
+      if (sec < 2) {  // GPT-J interleaved rotary embedding over the full head dim
+        const float2 cs = p.rope[static_cast<size_t>(pos) * (p.head_dim / 2) + i / 2];
+        const float r0 = __fsub_rn(__fmul_rn(y0, cs.x), __fmul_rn(y1, cs.y));
+        const float r1 = __fadd_rn(__fmul_rn(y0, cs.y), __fmul_rn(y1, cs.x));
+        y0 = r0;
+        y1 = r1;
+      }
+      const __half2 h = __floats2half2_rn(y0, y1);
+      if (sec == 0) {
+        *reinterpret_cast<__half2*>(p.q_out + static_cast<size_t>(b) * hd + rem) = h;
+      } else {
+        __half* cache = sec == 1 ? p.k_cache : p.v_cache;
+        const size_t off = ((static_cast<size_t>(b) * p.heads + head) * p.max_seq + pos) * p.head_dim + i;
+        *reinterpret_cast<__half2*>(cache + off) = h;
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+}  // namespace dev
+}  // namespace gemm
+}  // namespace dsinf

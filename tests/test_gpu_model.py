@@ -22,13 +22,14 @@ SEED = 20220701
 
 
 def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, prompt_len=6, gen=4,
-               use_graph=True, use_pdl=True, max_ctx=32):
+               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=True):
     tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
     rng = np.random.default_rng(hidden + layers + batch)
     prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
     mode = capi.TP_LOCAL if tp > 1 else capi.TP_NONE
     gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx,
-                       tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED)
+                       tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED,
+                       use_step_kernel=step_kernel)
     ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=batch, max_ctx=max_ctx,
                         seed=SEED)
     gpu.set_prompt(prompt)
@@ -57,24 +58,54 @@ def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, pr
     return worst
 
 
-def test_small_fp16_b1():
-    run_parity(256, 2, 4, 1000)
+PATHS = pytest.mark.parametrize("step_kernel", [True, False], ids=["step_kernel", "per_kernel"])
 
 
-def test_small_fp16_batch3_eager():
-    run_parity(256, 2, 4, 1000, batch=3, use_graph=False, use_pdl=False)
+@PATHS
+def test_small_fp16_b1(step_kernel):
+    run_parity(256, 2, 4, 1000, step_kernel=step_kernel)
 
 
-def test_small_fp16_batch16():
-    run_parity(512, 2, 8, 2000, batch=16)
+@PATHS
+def test_small_fp16_batch3_eager(step_kernel):
+    run_parity(256, 2, 4, 1000, batch=3, use_graph=False, use_pdl=False, step_kernel=step_kernel)
 
 
-def test_small_int8_b1():
-    run_parity(256, 2, 4, 1000, dtype_bytes=1)
+@PATHS
+def test_small_fp16_batch16(step_kernel):
+    run_parity(512, 2, 8, 2000, batch=16, step_kernel=step_kernel)
 
 
-def test_small_int8_batch8():
-    run_parity(512, 2, 8, 2000, batch=8, dtype_bytes=1)
+@PATHS
+def test_small_int8_b1(step_kernel):
+    run_parity(256, 2, 4, 1000, dtype_bytes=1, step_kernel=step_kernel)
+
+
+@PATHS
+def test_small_int8_batch8(step_kernel):
+    run_parity(512, 2, 8, 2000, batch=8, dtype_bytes=1, step_kernel=step_kernel)
+
+
+@PATHS
+def test_gpt2_shape_two_layers(step_kernel):
+    """GPT-2 1.5B widths (h=1600, 25 heads, d=64): N and K not multiples of 128, TPP=8 attention."""
+    run_parity(1600, 2, 25, 50257, prompt_len=4, gen=3, max_ctx=16, step_kernel=step_kernel)
+
+
+def test_step_kernel_matches_per_kernel_path():
+    """Both TP=1 paths give the same greedy tokens and logits within fp32 split-K reordering."""
+    prompt = np.random.default_rng(3).integers(0, 2000, (4, 9)).astype(np.int32)
+    res = []
+    for sk in (True, False):
+        m = DecoderModel(512, 3, 8, 2000, batch=4, max_ctx=32, seed=SEED, use_step_kernel=sk)
+        m.set_prompt(prompt)
+        m.step(20)
+        _, hist = m.read_tokens()
+        res.append((hist.copy(), m.full_logits().copy(), m.get_info().kernels_per_step))
+        m.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.abs(res[0][1] - res[1][1]).max() <= 1e-3 * np.abs(res[1][1]).max()
+    assert res[0][2] == 1 and res[1][2] > 1
 
 
 @pytest.mark.parametrize("tp", [2, 4])
