@@ -235,6 +235,11 @@ int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out);
  * weight load issued).  out == NULL queries the length; returns DSINF_ERR_CONFIG if not traced. */
 int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* needed, int32_t* grid,
                            int32_t* phases);
+/* Per-launch timeline of the last per-kernel decode step when the model was created with
+ * DSINF_LAUNCH_TRACE=1: out[2*i], out[2*i+1] = globaltimer ns of launch i's first CTA start and
+ * last CTA end, in enqueue order (embed, then per layer qkv, attention, attn-out, up, down, then
+ * lm head, argmax).  out == NULL queries the launch count. */
+int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches);
 /* Bytes per step for an arbitrary position (ctx = pos + 1). */
 int64_t dsinf_model_bytes_per_step(const dsinf_model* m, int64_t pos);
 /* Copy one synthetic weight tensor of layer `layer` in logical row-major fp32 form

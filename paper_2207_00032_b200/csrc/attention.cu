@@ -10,6 +10,7 @@
 #include "common.h"
 #include "launch.cuh"
 #include "ops.cuh"
+#include "sbi_gemm.cuh"
 #include "ptx.cuh"
 
 namespace dsinf {
@@ -28,6 +29,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   float* cst = co + d;
   const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
   const int tid = threadIdx.x;
+  ptx::trace_begin(p.trace);
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int ctx = *p.pos + 1;
@@ -53,12 +55,21 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   }
   const float inv = 1.0f / LL;
   const int hd = p.H * d;
+  float amax = 0.f;
   for (int i = c + C * tid; i < d; i += C * kAttnThreads) {
     float acc = 0.f;
     for (int r = 0; r < C; ++r) acc = fmaf(wts[r], ptx::ld_dsmem_f(ptx::map_shared_rank(&co[i], r)), acc);
-    p.out[static_cast<size_t>(b) * hd + head * d + i] = __float2half_rn(acc * inv);
+    const __half o = __float2half_rn(acc * inv);
+    p.out[static_cast<size_t>(b) * hd + head * d + i] = o;
+    amax = fmaxf(amax, fabsf(__half2float(o)));
+  }
+  if (p.amax_out != nullptr) {  // per-token int8 scale input of the attn-out GEMM
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
+    if ((tid & 31) == 0 && m != 0)
+      atomicMax(p.amax_out + ((head + c) % gemm::kStatStripes) * 32 + b, m);
   }
   if (C > 1) ptx::cluster_sync();
+  ptx::trace_end(p.trace);
 }
 
 }  // namespace

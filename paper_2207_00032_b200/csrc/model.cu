@@ -26,6 +26,7 @@
 #include "common.h"
 #include "nccl_dl.h"
 #include "ops.cuh"
+#include "ptx.cuh"
 #include "sbi_gemm.cuh"
 #include "step_kernel.cuh"
 #include "synth.h"
@@ -71,6 +72,8 @@ struct Shard {
   float* logits = nullptr;
   __half* kc = nullptr;
   __half* vc = nullptr;
+  long long* lnstats = nullptr;  // [2L+1][kLnSlotWords]: LayerNorm row sums from the producing epilogue
+  unsigned* amax = nullptr;      // [2L][kAmaxSlotWords]: int8 activation row max from the producer
   gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
 };
 
@@ -103,6 +106,11 @@ struct dsinf_model {
   int64_t kernels_per_step = 0;
   int attn_chunks = 1;
   dsinf::step::StepProgram step_prog;  // persistent whole-step kernel (TP = 1)
+  // TP = 1: the attn-out / MLP-down epilogues add the residual and emit the next LayerNorm's
+  // row sums, so the LN prologues skip their full-row statistics pass (DSINF_FUSE_STATS=0: off)
+  bool fuse_ln = false;
+  unsigned long long* ltrace = nullptr;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
+  int64_t ltrace_n = 0;
 
   void* alloc(size_t bytes) {
     void* p = nullptr;
@@ -265,6 +273,8 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.kc, 0, kv * 2, s));
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.vc, 0, kv * 2, s));
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.d_mlp, 0, B * h * 4, s));
+  if (m.fuse_ln) sh.lnstats = m.alloc_n<long long>((2 * m.L + 1) * gemm::kLnSlotWords);
+  if (m.int8) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
   const bool i8 = m.int8;
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0);
   sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0);
@@ -410,7 +420,19 @@ struct Enqueuer {
 
   int64_t pdl_launches = 0;
 
-  void gemm_launch(const gemm::Params& p, const gemm::Plan& plan, bool int8_w, int bit) {
+  // DSINF_LAUNCH_TRACE: per-launch [first CTA start, last CTA end] stamps, in launch order
+  int slot = 0;
+  unsigned long long* tslot() {
+    if (!m.ltrace || slot >= ptx::kTraceEnd) return nullptr;
+    return m.ltrace + slot++;
+  }
+
+  long long* lnslot(Shard& sh, int i) const { return sh.lnstats ? sh.lnstats + static_cast<int64_t>(i) * gemm::kLnSlotWords : nullptr; }
+  unsigned* amslot(Shard& sh, int i) const { return sh.amax ? sh.amax + static_cast<int64_t>(i) * gemm::kAmaxSlotWords : nullptr; }
+
+  void gemm_launch(const gemm::Params& p_in, const gemm::Plan& plan, bool int8_w, int bit) {
+    gemm::Params p = p_in;
+    p.trace = tslot();
     pdl_launches += P(bit);
     gemm::launch(p, plan, int8_w, s, P(bit));
     ++launches;
@@ -422,9 +444,13 @@ struct Enqueuer {
     gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8);
     p.pro = gemm::PRO_LN;
     p.res_in = sh.res[0];
-    p.res_delta = l > 0 ? sh.d_mlp : nullptr;
-    p.delta_bias = l > 0 ? sh.layers[l - 1].bdown : nullptr;
-    p.res_out = sh.res[1];
+    if (m.fuse_ln) {
+      p.ln_stats_in = lnslot(sh, 2 * l);
+    } else {
+      p.res_delta = l > 0 ? sh.d_mlp : nullptr;
+      p.delta_bias = l > 0 ? sh.layers[l - 1].bdown : nullptr;
+      p.res_out = sh.res[1];
+    }
     p.ln_g = w.ln1g;
     p.ln_b = w.ln1b;
     p.epi = gemm::EPI_QKV;
@@ -454,6 +480,8 @@ struct Enqueuer {
     a.d = static_cast<int>(m.d);
     a.max_seq = m.max_ctx;
     a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+    a.amax_out = amslot(sh, 2 * l);
+    a.trace = tslot();
     ops::attention(a, m.attn_chunks, s, P(1));
     ++launches;
   }
@@ -464,8 +492,16 @@ struct Enqueuer {
     p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.a;
     p.x_ld = static_cast<int>(m.Hl * m.d);
-    p.epi = gemm::EPI_F32;
-    p.out = sh.d_attn;
+    p.amax_in = amslot(sh, 2 * l);
+    if (m.fuse_ln) {  // residual += attn-out + bias; emits LN2's row sums
+      p.epi = gemm::EPI_RESID;
+      p.out = sh.res[0];
+      p.bias = w.bo;
+      p.ln_stats_out = lnslot(sh, 2 * l + 1);
+    } else {
+      p.epi = gemm::EPI_F32;
+      p.out = sh.d_attn;
+    }
     gemm_launch(p, sh.plan_o, m.int8, 2);
   }
 
@@ -473,15 +509,21 @@ struct Enqueuer {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
     p.pro = gemm::PRO_LN;
-    p.res_in = sh.res[1];
-    p.res_delta = sh.d_attn;
-    p.delta_bias = w.bo;
-    p.res_out = sh.res[0];
+    if (m.fuse_ln) {
+      p.res_in = sh.res[0];
+      p.ln_stats_in = lnslot(sh, 2 * l + 1);
+    } else {
+      p.res_in = sh.res[1];
+      p.res_delta = sh.d_attn;
+      p.delta_bias = w.bo;
+      p.res_out = sh.res[0];
+    }
     p.ln_g = w.ln2g;
     p.ln_b = w.ln2b;
     p.epi = gemm::EPI_GELU_F16;
     p.bias = w.bup;
     p.out = sh.u;
+    p.amax_out = amslot(sh, 2 * l + 1);
     gemm_launch(p, sh.plan_up, m.int8, 3);
   }
 
@@ -491,8 +533,16 @@ struct Enqueuer {
     p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.u;
     p.x_ld = static_cast<int>(m.Fl);
-    p.epi = gemm::EPI_F32;
-    p.out = sh.d_mlp;
+    p.amax_in = amslot(sh, 2 * l + 1);
+    if (m.fuse_ln) {  // residual += mlp-down + bias; emits the next LayerNorm's row sums
+      p.epi = gemm::EPI_RESID;
+      p.out = sh.res[0];
+      p.bias = w.bdown;
+      p.ln_stats_out = lnslot(sh, 2 * l + 2);
+    } else {
+      p.epi = gemm::EPI_F32;
+      p.out = sh.d_mlp;
+    }
     gemm_launch(p, sh.plan_down, m.int8, 4);
   }
 
@@ -500,8 +550,12 @@ struct Enqueuer {
     gemm::Params p = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), static_cast<int>(m.h), false);
     p.pro = gemm::PRO_LN;
     p.res_in = sh.res[0];
-    p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
-    p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
+    if (m.fuse_ln) {
+      p.ln_stats_in = lnslot(sh, 2 * static_cast<int>(m.L));
+    } else {
+      p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
+      p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
+    }
     p.res_out = nullptr;
     p.ln_g = sh.lnfg;
     p.ln_b = sh.lnfb;
@@ -517,6 +571,7 @@ struct Enqueuer {
     ap.idx_offset = first;
     ap.out_val = m.am_val + sh.rank * m.B;
     ap.out_idx = m.am_idx + sh.rank * m.B;
+    ap.trace = tslot();
     ops::argmax(ap, s, P(6));
     ++launches;
   }
@@ -544,6 +599,16 @@ struct Enqueuer {
       ++launches;
       return;
     }
+    if (m.ltrace) {
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace, 0xff, ptx::kTraceEnd * sizeof(unsigned long long), s));
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + ptx::kTraceEnd, 0, ptx::kTraceEnd * sizeof(unsigned long long), s));
+    }
+    for (Shard& sh : m.shards) {  // per-step statistics slots
+      if (sh.lnstats)
+        DSINF_CUDA_CHECK(cudaMemsetAsync(sh.lnstats, 0, (2 * m.L + 1) * gemm::kLnSlotWords * sizeof(long long), s));
+      if (sh.amax)
+        DSINF_CUDA_CHECK(cudaMemsetAsync(sh.amax, 0, std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords * sizeof(unsigned), s));
+    }
     for (Shard& sh : m.shards) {
       ops::EmbedParams e{};
       e.wte = sh.wte;
@@ -558,6 +623,8 @@ struct Enqueuer {
       e.B = m.B;
       e.h = static_cast<int>(m.h);
       e.V = static_cast<int>(m.V);
+      e.ln_stats_out = lnslot(sh, 0);
+      e.trace = tslot();
       ops::embed(e, s, P(6));
       ++launches;
     }
@@ -591,6 +658,7 @@ struct Enqueuer {
     sp.max_ctx = m.max_ctx;
     ops::select_token(sp, s, P(6));
     ++launches;
+    m.ltrace_n = slot;
   }
 };
 
@@ -682,6 +750,10 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     m->max_ctx = static_cast<int>(rt->max_ctx);
     m->int8 = cfg->dtype_bytes == 1;
     m->attn_chunks = ops::attention_chunks(m->B, static_cast<int>(m->Hl));
+    {
+      const char* fs = std::getenv("DSINF_FUSE_STATS");
+      m->fuse_ln = m->t == 1 && (fs == nullptr || std::atoi(fs) != 0);
+    }
     if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
       require(nccl_comm != nullptr, "NCCL mode needs a communicator");
       m->comm = static_cast<nccl::Comm>(nccl_comm);
@@ -706,6 +778,8 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     for (auto& sh : m->shards) build_shard(*m, sh, s);
     DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
     if (m->t == 1 && rt->use_step_kernel) build_step_program(*m);
+    if (const char* lt = std::getenv("DSINF_LAUNCH_TRACE"); lt && std::atoi(lt) != 0)
+      m->ltrace = m->alloc_n<unsigned long long>(2 * ptx::kTraceEnd);
     *out = m.release();
   });
 }
@@ -793,6 +867,25 @@ int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* 
     if (grid) *grid = m->step_prog.grid();
     if (phases) *phases = m->step_prog.phases();
     if (out) m->step_prog.trace(reinterpret_cast<unsigned long long*>(out), static_cast<size_t>(len));
+  });
+}
+
+int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    require(m->ltrace != nullptr, "launch trace disabled (set DSINF_LAUNCH_TRACE=1 before model creation)");
+    if (launches) *launches = m->ltrace_n;
+    if (out) {
+      require(len >= 2 * m->ltrace_n, "trace buffer too small");
+      std::vector<unsigned long long> st(m->ltrace_n), en(m->ltrace_n);
+      DSINF_CUDA_CHECK(cudaDeviceSynchronize());
+      DSINF_CUDA_CHECK(cudaMemcpy(st.data(), m->ltrace, m->ltrace_n * 8, cudaMemcpyDeviceToHost));
+      DSINF_CUDA_CHECK(cudaMemcpy(en.data(), m->ltrace + ptx::kTraceEnd, m->ltrace_n * 8, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < m->ltrace_n; ++i) {
+        out[2 * i] = st[i];
+        out[2 * i + 1] = en[i];
+      }
+    }
   });
 }
 

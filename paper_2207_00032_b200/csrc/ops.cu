@@ -6,6 +6,7 @@
 #include "common.h"
 #include "launch.cuh"
 #include "ops.cuh"
+#include "sbi_gemm.cuh"
 #include "ptx.cuh"
 #include "synth.h"
 
@@ -166,6 +167,7 @@ __global__ void quant_act_kernel(const __half* x, int64_t K, int8_t* q, float* s
 
 // ---------------------------------------------------------------- step boundary
 __global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
+  ptx::trace_begin(p.trace);
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int b = blockIdx.x;
@@ -173,12 +175,48 @@ __global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
   int tok = pos < p.prompt_len ? p.prompt[static_cast<size_t>(b) * p.prompt_ld + pos] : p.next_tok[b];
   if (tok < 0 || tok >= p.V) tok = 0;
   if (threadIdx.x == 0 && pos < p.max_ctx) p.hist[static_cast<size_t>(b) * p.max_ctx + pos] = tok;
-  const __half* row = p.wte + static_cast<size_t>(tok) * p.h;
-  float* out = p.res + static_cast<size_t>(b) * p.h;
-  for (int k = threadIdx.x; k < p.h; k += blockDim.x) out[k] = __half2float(row[k]);
+  const uint4* row = reinterpret_cast<const uint4*>(p.wte + static_cast<size_t>(tok) * p.h);  // h % 8 == 0
+  float4* out = reinterpret_cast<float4*>(p.res + static_cast<size_t>(b) * p.h);
+  long long s1 = 0, s2 = 0;
+  for (int k = threadIdx.x; k < p.h / 8; k += blockDim.x) {
+    const uint4 u = __ldg(row + k);
+    const __half2* hh = reinterpret_cast<const __half2*>(&u);
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __low2float(hh[i]);
+      v[2 * i + 1] = __high2float(hh[i]);
+    }
+    out[2 * k] = make_float4(v[0], v[1], v[2], v[3]);
+    out[2 * k + 1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s1 += __float2ll_rn(__fmul_rn(v[i], gemm::kSumScale));
+      s2 += __float2ll_rn(__fmul_rn(__fmul_rn(v[i], v[i]), gemm::kSqScale));
+    }
+  }
+  if (p.ln_stats_out != nullptr) {  // LayerNorm statistics of the first layer (integer sums: exact)
+    __shared__ long long red[2][32];
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = s1;
+      red[1][threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      long long t = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.ln_stats_out) + b * 2 + threadIdx.x, static_cast<unsigned long long>(t));
+    }
+  }
+  ptx::trace_end(p.trace);
 }
 
 __global__ void argmax_kernel(const __grid_constant__ ArgmaxParams p) {
+  ptx::trace_begin(p.trace);
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int b = blockIdx.x;
@@ -218,6 +256,7 @@ __global__ void argmax_kernel(const __grid_constant__ ArgmaxParams p) {
     p.out_val[b] = bv;
     p.out_idx[b] = static_cast<int32_t>(bx + p.idx_offset);
   }
+  ptx::trace_end(p.trace);
 }
 
 __global__ void select_kernel(const __grid_constant__ SelectParams p) {

@@ -45,6 +45,8 @@ struct AttnParams {
   __half* out;            // [B][H*d]
   int B, H, d, max_seq;
   float scale;
+  unsigned* amax_out;         // row max |out| stripes for the int8 attn-out prologue, or null
+  unsigned long long* trace;  // launch timeline slot or null
 };
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
@@ -62,6 +64,8 @@ struct EmbedParams {
   int max_ctx;
   float* res;             // [B][h]
   int B, h, V;
+  long long* ln_stats_out;  // fixed-point row sums of res for the first LayerNorm, or null
+  unsigned long long* trace;
 };
 void embed(const EmbedParams& p, cudaStream_t s, bool pdl);
 
@@ -71,6 +75,7 @@ struct ArgmaxParams {
   int64_t idx_offset;   // global vocab index of local column 0
   float* out_val;       // [B]
   int32_t* out_idx;     // [B]
+  unsigned long long* trace;
 };
 void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl);
 

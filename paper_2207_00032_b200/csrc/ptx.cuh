@@ -128,6 +128,21 @@ __device__ __forceinline__ float ld_dsmem_f(uint32_t addr) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- launch timeline (DSINF_LAUNCH_TRACE)
+// slot[0] = earliest CTA start, slot[kTraceEnd] = latest CTA end of one launch (globaltimer ns).
+constexpr int kTraceEnd = 1024;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_begin(unsigned long long* slot) {
+  if (slot != nullptr && threadIdx.x == 0) atomicMin(slot, gtimer());
+}
+__device__ __forceinline__ void trace_end(unsigned long long* slot) {
+  if (slot != nullptr && threadIdx.x == 0) atomicMax(slot + kTraceEnd, gtimer());
+}
+
 // ---------------------------------------------------------------- warp MMA (legacy tensor path)
 // D(16x8,f32) += A(16x16,f16,row) * B(16x8,f16,col)
 __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,

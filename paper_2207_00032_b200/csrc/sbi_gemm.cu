@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   const int row_end = min(p.rows, row_begin + p.rows_per_split);
   const int n_iters = (row_end - row_begin + kRowsPerStage - 1) / kRowsPerStage;
 
+  __shared__ dev::EpiStats es;
+  ptx::trace_begin(p.trace);
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.tmap);
     for (int s = 0; s < stages; ++s) {
@@ -83,6 +85,15 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w)
           ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
+        if (it == stages - 1) {
+          // ring full: warm the next stages into L2 so HBM keeps streaming while the consumers
+          // run the Deep-Fusion prologue (LayerNorm / quantisation statistics)
+          const int pf_end = min(n_iters, stages + p.l2_ahead);
+          for (int j = stages; j < pf_end; ++j)
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w)
+              ptx::tma_prefetch_l2_2d(&p.tmap, n0 + w * kWarpCols, row_begin + j * kRowsPerStage);
+        }
         if (++s == stages) {
           s = 0;
           phase ^= 1;
@@ -131,34 +142,51 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
   const int c_begin = rank * cols_per_rank;
   const int pairs = cols_per_rank / 2;
   const uint8_t* part_base = ring;
-  for (int item = threadIdx.x; item < p.B * pairs; item += kThreads) {
-    const int b = item / pairs;
-    const int c = c_begin + 2 * (item - b * pairs);
-    const int n = n0 + c;
-    if (n >= p.N) continue;
-    const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
-    float y0, y1;
-    if constexpr (kInt8) {
-      int s0 = 0, s1 = 0;
-      for (int r = 0; r < nsplit; ++r) {
-        const int2 v = ptx::ld_dsmem_i2(ptx::map_shared_rank(part_base + off, r));
-        s0 += v.x;
-        s1 += v.y;
+  const bool want_stats = p.ln_stats_out != nullptr || p.amax_out != nullptr;
+  // one warp per batch row (lanes over column pairs) so row statistics reduce with shuffles
+  for (int b = warp; b < p.B; b += kThreads / 32) {
+    dev::RowStat st;
+    for (int q = lane; q < pairs; q += 32) {
+      const int c = c_begin + 2 * q;
+      const int n = n0 + c;
+      if (n >= p.N) continue;
+      const bool has1 = n + 1 < p.N;
+      float2 rin = make_float2(0.f, 0.f);  // issue the residual read ahead of the DSMEM reads
+      if (p.epi == EPI_RESID) {
+        const float* o = static_cast<const float*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
+        rin.x = __ldcg(o);
+        if (has1) rin.y = __ldcg(o + 1);
       }
-      dev::dequant_pair(p, hd, b, n, s0, s1, y0, y1);
-    } else {
-      float2 acc2 = make_float2(0.f, 0.f);
-      for (int r = 0; r < nsplit; ++r) {
-        const float2 v = ptx::ld_dsmem_f2(ptx::map_shared_rank(part_base + off, r));
-        acc2.x += v.x;
-        acc2.y += v.y;
+      const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
+      float y0, y1;
+      if constexpr (kInt8) {
+        int s0 = 0, s1 = 0;
+        for (int r = 0; r < nsplit; ++r) {
+          const int2 v = ptx::ld_dsmem_i2(ptx::map_shared_rank(part_base + off, r));
+          s0 += v.x;
+          s1 += v.y;
+        }
+        dev::dequant_pair(p, hd, b, n, s0, s1, y0, y1);
+      } else {
+        float2 acc2 = make_float2(0.f, 0.f);
+        for (int r = 0; r < nsplit; ++r) {
+          const float2 v = ptx::ld_dsmem_f2(ptx::map_shared_rank(part_base + off, r));
+          acc2.x += v.x;
+          acc2.y += v.y;
+        }
+        y0 = acc2.x;
+        y1 = acc2.y;
       }
-      y0 = acc2.x;
-      y1 = acc2.y;
+      dev::epilogue_pair(p, b, n, y0, y1, has1, &st, p.epi == EPI_RESID ? &rin : nullptr);
     }
-    dev::epilogue_pair(p, b, n, y0, y1, n + 1 < p.N);
+    if (want_stats) dev::row_stat_commit(st, es, b, lane);
+  }
+  if (want_stats) {
+    __syncthreads();
+    dev::stats_flush(p, es, (tile + split) % kStatStripes);
   }
   if (nsplit > 1) ptx::cluster_sync();  // keep our smem alive for remote readers
+  ptx::trace_end(p.trace);
 }
 
 template <bool kInt8, int kNB8>
@@ -337,6 +365,18 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   Params p = p_in;
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
+  p.l2_ahead = env_int("DSINF_L2_AHEAD", 0);
+  if (env_int("DSINF_FAKE_PRO", 0) && p.pro == PRO_LN && !int8_weights) {  // timing experiment only
+    p.pro = PRO_F16;
+    p.x = p.ln_g;
+    p.x_ld = 0;
+  }
+  if (env_int("DSINF_FAKE_EPI", 0) && p.epi != EPI_F32) {  // timing experiment only
+    static float* scratch = nullptr;
+    if (!scratch) cudaMalloc(&scratch, 16 * 65536 * 4);
+    p.epi = EPI_F32;
+    p.out = scratch;
+  }
   p.x_row_words = plan.rows_per_split + 8;
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");

@@ -23,6 +23,17 @@ constexpr int kMaxB = 16;                                  // batch rows per lau
 constexpr int kPartLd = kColTile + 4;                      // split-K partial row stride (floats)
 constexpr int kHeaderBytes = 1024;                         // barriers + per-row scalars
 
+// Row statistics handed from a producing epilogue to the next kernel's prologue (TP = 1 path):
+//   LayerNorm: per row, sum(y) and sum(y*y) in fixed point (int64; y * 2^32 and y^2 * 2^28,
+//   rounded per element), so the integer atomics make them independent of CTA order;
+//   int8 activations: per row, max |x| as fp32 bits (u32 atomicMax; order-independent).
+// Each is striped over kStatStripes 128-byte-aligned copies to spread same-address atomics.
+constexpr int kStatStripes = 8;
+constexpr int kLnSlotWords = kStatStripes * kMaxB * 2;  // int64 words per LayerNorm slot
+constexpr int kAmaxSlotWords = kStatStripes * 32;       // u32 words per amax slot
+constexpr float kSumScale = 4294967296.0f;               // 2^32
+constexpr float kSqScale = 268435456.0f;                 // 2^28
+
 enum Prologue : int {
   PRO_F16 = 0,    // x fp16 [B][x_ld] from global
   PRO_I8 = 1,     // x int8 [B][x_ld] + scales from global (already quantised)
@@ -46,6 +57,7 @@ struct Params {
   int N, rows, K, B;
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
   int stages;
+  int l2_ahead;          // stages warmed into L2 beyond the smem ring while the prologue runs
   int x_row_words;       // smem stride of one x row (== 8 mod 32)
   // prologue
   int pro;
@@ -59,6 +71,8 @@ struct Params {
   const __half* ln_g;
   const __half* ln_b;
   float ln_eps;
+  const long long* ln_stats_in;  // PRO_LN: row sums from the producer (else a full-row pass)
+  const unsigned* amax_in;       // PRO_QUANT: row max |x| from the producer (else a full-row pass)
   // epilogue
   int epi;
   const __half* bias;
@@ -70,6 +84,9 @@ struct Params {
   const float2* rope;  // [max_seq][head_dim/2] (cos, sin)
   const int* pos;
   int heads, head_dim, max_seq;
+  long long* ln_stats_out;  // EPI_RESID: accumulate the new residual's row sums (slot, zeroed per step)
+  unsigned* amax_out;       // EPI_F16 / EPI_GELU_F16: accumulate row max |out|
+  unsigned long long* trace;  // launch timeline slot (ptx::trace_begin / trace_end) or null
 };
 
 struct Plan {

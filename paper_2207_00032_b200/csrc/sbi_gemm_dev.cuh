@@ -26,6 +26,12 @@ struct Header {
   float red[8];
   int flag[4];
 };
+
+// Epilogue statistics of one CTA's columns (static smem of the standalone kernel).
+struct EpiStats {
+  unsigned long long esum[kMaxB][2];  // row sums (fixed point)
+  unsigned emax[kMaxB];               // row max |out| (fp32 bits)
+};
 static_assert(sizeof(Header) <= kHeaderBytes, "header too large");
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -123,11 +129,54 @@ __device__ __forceinline__ float ln_apply(float v, float mean, float rstd, const
 // LayerNorm statistics of the full row (single shifted pass) -> hd.mean / hd.rstd; with int8
 // weights also the per-token scale of the fp16-rounded normalised row -> hd.xscale.
 // `write_res` stores the residual (r + delta + bias) once (one CTA per launch / phase).
+// Mean / rstd of row b from the producer's fixed-point sums (kStatStripes stripes).
+__device__ __forceinline__ void ln_from_sums(const long long* st, int b, int K, float eps, float& mean, float& rstd) {
+  long long s1 = 0, s2 = 0;
+#pragma unroll
+  for (int s = 0; s < kStatStripes; ++s) {
+    s1 += __ldcg(st + (s * kMaxB + b) * 2);
+    s2 += __ldcg(st + (s * kMaxB + b) * 2 + 1);
+  }
+  const double m = static_cast<double>(s1) / (static_cast<double>(kSumScale) * K);
+  const double e2 = static_cast<double>(s2) / (static_cast<double>(kSqScale) * K);
+  const double var = fmax(e2 - m * m, 0.0);
+  mean = static_cast<float>(m);
+  rstd = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+}
+
+// Row max |x| from the producer's stripes.
+__device__ __forceinline__ float amax_from_stripes(const unsigned* a, int b) {
+  unsigned m = 0;
+#pragma unroll
+  for (int s = 0; s < kStatStripes; ++s) m = max(m, __ldcg(a + s * 32 + b));
+  return __uint_as_float(m);
+}
+
 template <bool kInt8>
 __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int lane, bool write_res) {
   const RowMap rm(p.B, ctid);
   const int K = p.K;
   const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
+  if (p.ln_stats_in != nullptr) {  // statistics from the producing epilogue: no full-row pass
+    if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, K, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+    if (!kInt8) return;
+    consumer_bar();
+    const float mean = rm.active ? hd.mean[rm.b] : 0.f, rstd = rm.active ? hd.rstd[rm.b] : 0.f;
+    float mx = 0.f;
+    if (rm.active) {
+#pragma unroll 4
+      for (int c = rm.j; c < K / 4; c += rm.tpr) {
+        const float4 v = rv.load4(rm.b, 4 * c);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          mx = fmaxf(mx, fabsf(__half2float(__float2half_rn(ln_apply(vv[i], mean, rstd, p.ln_g, p.ln_b, 4 * c + i)))));
+      }
+    }
+    mx = row_reduce<true>(mx, rm.tpr, hd.red, cw, lane);
+    if (rm.active && rm.j == 0) hd.xscale[rm.b] = act_scale(mx);
+    return;
+  }
   float c0 = 0.f, s1 = 0.f, s2 = 0.f;
   if (rm.active) {
     c0 = rv.load4(rm.b, 0).x;  // shift for a cancellation-free single pass
@@ -172,6 +221,10 @@ __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int 
 
 // Per-token scale of an fp16 activation row (PRO_QUANT) -> hd.xscale.
 __device__ __forceinline__ void quant_row_scale(const Params& p, Header& hd, int ctid, int cw, int lane) {
+  if (p.amax_in != nullptr) {  // row max from the producing epilogue
+    if (ctid < p.B) hd.xscale[ctid] = act_scale(amax_from_stripes(p.amax_in, ctid));
+    return;
+  }
   const RowMap rm(p.B, ctid);
   const __half* x = static_cast<const __half*>(p.x);
   float mx = 0.f;
@@ -407,7 +460,44 @@ __device__ __forceinline__ void dequant_pair(const Params& p, const Header& hd, 
   y1 = (n + 1 < p.N) ? __fmul_rn(__fmul_rn(static_cast<float>(s1), xs), p.w_scale[n + 1]) : 0.f;
 }
 
-__device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, float y0, float y1, bool has1) {
+// Epilogue row statistics of one thread's outputs (registers), reduced per warp by row_stat_commit.
+struct RowStat {
+  long long s1 = 0, s2 = 0;  // fixed point, see kSumScale / kSqScale
+  float amax = 0.f;
+  __device__ __forceinline__ void add(float y) {
+    s1 += __float2ll_rn(__fmul_rn(y, kSumScale));
+    s2 += __float2ll_rn(__fmul_rn(__fmul_rn(y, y), kSqScale));
+  }
+};
+
+// The whole warp holds row b's statistics of this CTA: reduce and store them (lane 0).
+__device__ __forceinline__ void row_stat_commit(RowStat st, EpiStats& es, int b, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    st.s1 += __shfl_xor_sync(0xffffffffu, st.s1, o);
+    st.s2 += __shfl_xor_sync(0xffffffffu, st.s2, o);
+  }
+  const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(st.amax));
+  if (lane == 0) {
+    es.esum[b][0] = static_cast<unsigned long long>(st.s1);
+    es.esum[b][1] = static_cast<unsigned long long>(st.s2);
+    es.emax[b] = m;
+  }
+}
+
+// One CTA's epilogue statistics -> the global stripes (after a block-wide barrier).
+__device__ __forceinline__ void stats_flush(const Params& p, const EpiStats& es, int stripe) {
+  if (p.ln_stats_out != nullptr && threadIdx.x < 2 * p.B) {
+    const int b = threadIdx.x >> 1, j = threadIdx.x & 1;
+    atomicAdd(reinterpret_cast<unsigned long long*>(p.ln_stats_out) + (stripe * kMaxB + b) * 2 + j, es.esum[b][j]);
+  }
+  if (p.amax_out != nullptr && threadIdx.x < p.B) atomicMax(p.amax_out + stripe * 32 + threadIdx.x, es.emax[threadIdx.x]);
+}
+
+// `st` (nullable) accumulates the statistics requested by p.ln_stats_out / p.amax_out;
+// `rin` (nullable) holds the two residual values of EPI_RESID when the caller preloaded them.
+__device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, float y0, float y1, bool has1,
+                                              RowStat* st = nullptr, const float2* rin = nullptr) {
   if (p.bias) {
     y0 = __fadd_rn(y0, __half2float(p.bias[n]));
     if (has1) y1 = __fadd_rn(y1, __half2float(p.bias[n + 1]));
@@ -425,8 +515,14 @@ __device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, flo
     }
     case EPI_RESID: {  // residual stream += y + bias (fp32, this column's only writer)
       float* o = static_cast<float*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
-      o[0] = __fadd_rn(__ldcg(o), y0);
-      if (has1) o[1] = __fadd_rn(__ldcg(o + 1), y1);
+      const float r0 = __fadd_rn(rin ? rin->x : __ldcg(o), y0);
+      o[0] = r0;
+      if (st) st->add(r0);
+      if (has1) {
+        const float r1 = __fadd_rn(rin ? rin->y : __ldcg(o + 1), y1);
+        o[1] = r1;
+        if (st) st->add(r1);
+      }
       break;
     }
     case EPI_F16:
@@ -436,11 +532,16 @@ __device__ __forceinline__ void epilogue_pair(const Params& p, int b, int n, flo
         y1 = gelu_tanh(y1);
       }
       __half* o = static_cast<__half*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
+      const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
       if (has1 && ((reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
-        *reinterpret_cast<__half2*>(o) = __floats2half2_rn(y0, y1);
+        *reinterpret_cast<__half2*>(o) = __halves2half2(h0, h1);
       } else {
-        o[0] = __float2half_rn(y0);
-        if (has1) o[1] = __float2half_rn(y1);
+        o[0] = h0;
+        if (has1) o[1] = h1;
+      }
+      if (st) {
+        st->amax = fmaxf(st->amax, fabsf(__half2float(h0)));
+        if (has1) st->amax = fmaxf(st->amax, fabsf(__half2float(h1)));
       }
       break;
     }
