@@ -40,7 +40,7 @@ using dev::Header;
 //   [ring: stages x 16 KB] [header 1 KB] [x slice: B rows x x_row_words words]
 // After the main loop the ring is reused for the split-K partials part[b][n].
 template <bool kInt8, int kNB8>
-__global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
@@ -85,15 +85,6 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w)
           ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
-        if (it == stages - 1) {
-          // ring full: warm the next stages into L2 so HBM keeps streaming while the consumers
-          // run the Deep-Fusion prologue (LayerNorm / quantisation statistics)
-          const int pf_end = min(n_iters, stages + p.l2_ahead);
-          for (int j = stages; j < pf_end; ++j)
-#pragma unroll
-            for (int w = 0; w < kConsumerWarps; ++w)
-              ptx::tma_prefetch_l2_2d(&p.tmap, n0 + w * kWarpCols, row_begin + j * kRowsPerStage);
-        }
         if (++s == stages) {
           s = 0;
           phase ^= 1;
@@ -111,14 +102,18 @@ __global__ void __launch_bounds__(kThreads) sbi_gemm_kernel(const __grid_constan
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
     ptx::pdl_wait();
-    if (p.pro == PRO_LN)
-      dev::ln_row_stats<kInt8>(p, hd, ctid, cw, lane, p.res_out != nullptr && tile == 0 && split == 0);
-    else if (p.pro == PRO_QUANT)
-      dev::quant_row_scale(p, hd, ctid, cw, lane);
-    else if (p.pro == PRO_I8 && ctid < p.B)
-      hd.xscale[ctid] = p.x_scale[ctid];
-    dev::consumer_bar();
-    dev::fill_x_slice<kInt8>(p, sx, hd, row_begin, p.rows_per_split, ctid);
+    if (!kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr) {
+      dev::fill_x_ln_f16_pre(p, sx, hd, row_begin, p.rows_per_split, ctid);
+    } else {
+      if (p.pro == PRO_LN)
+        dev::ln_row_stats<kInt8>(p, hd, ctid, cw, lane, p.res_out != nullptr && tile == 0 && split == 0);
+      else if (p.pro == PRO_QUANT)
+        dev::quant_row_scale(p, hd, ctid, cw, lane);
+      else if (p.pro == PRO_I8 && ctid < p.B)
+        hd.xscale[ctid] = p.x_scale[ctid];
+      dev::consumer_bar();
+      dev::fill_x_slice<kInt8>(p, sx, hd, row_begin, p.rows_per_split, ctid);
+    }
     dev::consumer_bar();
 
     dev::Consumer<kInt8, kNB8> c;
@@ -365,18 +360,6 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   Params p = p_in;
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
-  p.l2_ahead = env_int("DSINF_L2_AHEAD", 0);
-  if (env_int("DSINF_FAKE_PRO", 0) && p.pro == PRO_LN && !int8_weights) {  // timing experiment only
-    p.pro = PRO_F16;
-    p.x = p.ln_g;
-    p.x_ld = 0;
-  }
-  if (env_int("DSINF_FAKE_EPI", 0) && p.epi != EPI_F32) {  // timing experiment only
-    static float* scratch = nullptr;
-    if (!scratch) cudaMalloc(&scratch, 16 * 65536 * 4);
-    p.epi = EPI_F32;
-    p.out = scratch;
-  }
   p.x_row_words = plan.rows_per_split + 8;
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");

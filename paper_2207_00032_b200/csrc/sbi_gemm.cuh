@@ -57,7 +57,6 @@ struct Params {
   int N, rows, K, B;
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
   int stages;
-  int l2_ahead;          // stages warmed into L2 beyond the smem ring while the prologue runs
   int x_row_words;       // smem stride of one x row (== 8 mod 32)
   // prologue
   int pro;

@@ -254,6 +254,57 @@ __device__ __forceinline__ void quant_row_scale(const Params& p, Header& hd, int
 // Writes packed rows [row0, row0 + nrows) of x into sx[b * xrw + w] (w = row - row0), one 32-bit
 // word per (row, b) holding M = 2 (fp16) or 4 (int8) consecutive k.  Requires the statistics
 // of ln_row_stats / quant_row_scale in `hd` for PRO_LN / PRO_QUANT.
+// PRO_LN, fp16, statistics from the producer (p.ln_stats_in): the first residual / gamma / beta
+// loads are issued BEFORE the statistics are read, so the two L2 round trips overlap.  Replaces
+// ln_row_stats + consumer_bar + fill_x_slice for this case (all 128 consumer threads call it).
+__device__ __forceinline__ void fill_x_ln_f16_pre(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows, int ctid) {
+  constexpr int kPre = 8;
+  const int K = p.K;
+  const int xrw = p.x_row_words;
+  const int total = p.B * nrows;
+  float2 r[kPre];
+  __half2 g[kPre], be[kPre];
+  const __half2 zero2 = __floats2half2_rn(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < kPre; ++j) {
+    const int i = ctid + 128 * j;
+    r[j] = make_float2(0.f, 0.f);
+    g[j] = be[j] = zero2;
+    if (i < total) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 2;
+      if (k < K) {  // K % 8 == 0 on this path
+        r[j] = __ldcg(reinterpret_cast<const float2*>(p.res_in + static_cast<size_t>(b) * K + k));
+        g[j] = *reinterpret_cast<const __half2*>(p.ln_g + k);
+        be[j] = *reinterpret_cast<const __half2*>(p.ln_b + k);
+      }
+    }
+  }
+  if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, K, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+  consumer_bar();
+#pragma unroll
+  for (int j = 0; j < kPre; ++j) {
+    const int i = ctid + 128 * j;
+    if (i < total) {
+      const int b = i / nrows, w = i - b * nrows;
+      const float mean = hd.mean[b], rstd = hd.rstd[b];
+      sx[b * xrw + w] = pack_h2((r[j].x - mean) * rstd * __low2float(g[j]) + __low2float(be[j]),
+                                (r[j].y - mean) * rstd * __high2float(g[j]) + __high2float(be[j]));
+    }
+  }
+  for (int i = ctid + 128 * kPre; i < total; i += 128) {
+    const int b = i / nrows, w = i - b * nrows;
+    const int k = (row0 + w) * 2;
+    uint32_t word = 0;
+    if (k < K) {
+      const float2 v = __ldcg(reinterpret_cast<const float2*>(p.res_in + static_cast<size_t>(b) * K + k));
+      word = pack_h2(ln_apply(v.x, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k),
+                     ln_apply(v.y, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k + 1));
+    }
+    sx[b * xrw + w] = word;
+  }
+}
+
 template <bool kInt8>
 __device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, int row0, int nrows, int ctid) {
   const int K = p.K;
