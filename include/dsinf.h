@@ -240,6 +240,8 @@ int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* 
  * last CTA end, in enqueue order (embed, then per layer qkv, attention, attn-out, up, down, then
  * lm head, argmax).  out == NULL queries the launch count. */
 int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches);
+/* Turn the per-launch timeline on (1) or off (0) after creation; re-captures the step graph. */
+int dsinf_model_set_launch_trace(dsinf_model* m, int on);
 /* Bytes per step for an arbitrary position (ctx = pos + 1). */
 int64_t dsinf_model_bytes_per_step(const dsinf_model* m, int64_t pos);
 /* Copy one synthetic weight tensor of layer `layer` in logical row-major fp32 form

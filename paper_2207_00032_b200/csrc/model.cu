@@ -870,6 +870,23 @@ int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* 
   });
 }
 
+int dsinf_model_set_launch_trace(dsinf_model* m, int on) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    if (on && !m->ltrace) m->ltrace = m->alloc_n<unsigned long long>(2 * ptx::kTraceEnd);
+    if (!on) m->ltrace = nullptr;  // the buffer stays owned by the model until destroy
+    m->ltrace_n = 0;
+    if (m->exec) {  // launch parameters changed: re-capture the step graph
+      cudaGraphExecDestroy(m->exec);
+      m->exec = nullptr;
+    }
+    if (m->graph) {
+      cudaGraphDestroy(m->graph);
+      m->graph = nullptr;
+    }
+  });
+}
+
 int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches) {
   return guarded([&] {
     require(m != nullptr, "null model");

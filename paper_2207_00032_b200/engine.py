@@ -130,6 +130,24 @@ class DecoderModel:
                                                     _stream_ptr(stream)))
         return nxt, hist
 
+    def launch_trace(self, steps: int = 8, stream=None):
+        """Per-launch device timeline of `steps` more decode steps: array [steps][launches][2] of
+        globaltimer ns (first CTA start, last CTA end), launch order = the step's enqueue order."""
+        capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 1))
+        out = []
+        try:
+            for _ in range(steps):
+                self.step(1, stream=stream)
+                n = C.c_int64()
+                capi.check(capi.lib.dsinf_model_launch_trace(self._h, None, 0, C.byref(n)))
+                buf = np.zeros(2 * n.value, dtype=np.uint64)
+                capi.check(capi.lib.dsinf_model_launch_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                             buf.size, None))
+                out.append(buf.reshape(-1, 2))
+        finally:
+            capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 0))
+        return np.stack(out)
+
     def bytes_per_step(self, pos: int) -> int:
         return int(capi.lib.dsinf_model_bytes_per_step(self._h, pos))
 
