@@ -233,12 +233,10 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
     """Per-launch device timeline (globaltimer: first CTA start -> last CTA end) of `steps` decode
     steps replayed right after the timed region from the same CUDA graph (re-captured with two
     timestamp atomics per CTA).  Returns (sbi_gemm byte-weighted GB/s, per-kind table) or None."""
+    from paper_2207_00032_b200 import _capi as capi
+
     tr = model.launch_trace(steps, stream=stream).astype(np.float64)
-    L = preset.layers
-    kinds = ["embed"] + [k for _ in range(L) for k in ("qkv", "attn", "attn_out", "mlp_up", "mlp_down")] + \
-        ["lm_head", "argmax"]
-    if tr.shape[1] != len(kinds):
-        return None
+    kinds = [capi.LK_NAMES[int(k)] for k in tr[0, :, 2]]
     dur = (tr[:, :, 1] - tr[:, :, 0]) / 1e3
     span = float(np.median((tr[:, -1, 1] - tr[:, 0, 0]) / 1e3))
     layer, lm = gemm_shapes(preset, tp)
@@ -259,6 +257,8 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
             tot_b += b * d.size
             tot_us += float(d.sum())
         table[k] = row
+    if tot_us == 0:
+        return None
     return tot_b / (tot_us * 1e-6) / 1e9, {"step_span_us": round(span, 1), "kinds": table}
 
 

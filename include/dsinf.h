@@ -235,10 +235,19 @@ int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out);
  * weight load issued).  out == NULL queries the length; returns DSINF_ERR_CONFIG if not traced. */
 int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* needed, int32_t* grid,
                            int32_t* phases);
-/* Per-launch timeline of the last per-kernel decode step when the model was created with
- * DSINF_LAUNCH_TRACE=1: out[2*i], out[2*i+1] = globaltimer ns of launch i's first CTA start and
- * last CTA end, in enqueue order (embed, then per layer qkv, attention, attn-out, up, down, then
- * lm head, argmax).  out == NULL queries the launch count. */
+/* Per-launch timeline of the last per-kernel decode step when launch tracing is on
+ * (DSINF_LAUNCH_TRACE=1 at creation, or dsinf_model_set_launch_trace): for launch i in enqueue
+ * order, out[3*i] / out[3*i+1] = globaltimer ns of its first CTA start / last CTA end and
+ * out[3*i+2] = its kind (DSINF_LK_*).  out == NULL queries the launch count. */
+#define DSINF_LK_EMBED 0
+#define DSINF_LK_QKV 1
+#define DSINF_LK_ATTN 2
+#define DSINF_LK_O 3
+#define DSINF_LK_UP 4
+#define DSINF_LK_DOWN 5
+#define DSINF_LK_LM 6
+#define DSINF_LK_ARGMAX 7
+#define DSINF_LK_PREP 8 /* row preparation (LayerNorm / quantisation) of the x-streaming plan */
 int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches);
 /* Turn the per-launch timeline on (1) or off (0) after creation; re-captures the step graph. */
 int dsinf_model_set_launch_trace(dsinf_model* m, int on);

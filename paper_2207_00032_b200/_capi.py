@@ -209,3 +209,6 @@ def check(status: int) -> None:
         return
     exc = _ERRORS.get(status, DsinfError)
     raise exc(last_error())
+
+# launch kinds of dsinf_model_launch_trace (DSINF_LK_*)
+LK_NAMES = ["embed", "qkv", "attn", "attn_out", "mlp_up", "mlp_down", "lm_head", "argmax", "prep"]

@@ -35,7 +35,11 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
   const int N = static_cast<int>(a.N), K = static_cast<int>(a.K);
   for (int64_t b0 = 0; b0 < a.B; b0 += gemm::kMaxB) {
     const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
-    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit);
+    const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
+    const void* xb = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;
+    const bool ready_x = !i8w || a.x_dtype == DSINF_DT_I8;  // GEMM-ready x (no on-the-fly quantisation)
+    const bool xs = ready_x && gemm::prefer_x_stream(nb) && gemm::x_streamable(xb, K, K, i8w);
+    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs);
     gemm::Params p{};
     p.w_scale = a.w_scales;
     p.N = N;
@@ -43,8 +47,7 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     p.rows = (K + (i8w ? 3 : 1)) / (i8w ? 4 : 2);
     gemm::make_weight_map(&p.tmap, a.w_packed, N, p.rows);
     p.B = nb;
-    const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
-    p.x = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;
+    p.x = xb;
     p.x_ld = K;
     if (i8w)
       p.pro = a.x_dtype == DSINF_DT_I8 ? gemm::PRO_I8 : gemm::PRO_QUANT;
@@ -85,8 +88,10 @@ int dsinf_gemm_launch_plan(int64_t N, int64_t K, int64_t B, int32_t w_dtype, dsi
   return guarded([&] {
     require(out != nullptr, "null out");
     require(N >= 1 && K >= 1 && B >= 1, "gemm shape dims must be positive");
-    const gemm::Plan p = gemm::make_plan(static_cast<int>(N), static_cast<int>(K),
-                                         static_cast<int>(std::min<int64_t>(B, gemm::kMaxB)), w_dtype == DSINF_DT_I8, 0);
+    const int nb = static_cast<int>(std::min<int64_t>(B, gemm::kMaxB));
+    // the plan dsinf_gemm uses with fp16 x (int8 weights then quantise x on the fly: no streaming)
+    const bool xs = w_dtype != DSINF_DT_I8 && gemm::prefer_x_stream(nb);
+    const gemm::Plan p = gemm::make_plan(static_cast<int>(N), static_cast<int>(K), nb, w_dtype == DSINF_DT_I8, 0, xs);
     out->col_tile = gemm::kColTile;
     out->ksplit = p.ksplit;
     out->rows_per_split = p.rows_per_split;

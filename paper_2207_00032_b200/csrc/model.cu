@@ -72,6 +72,9 @@ struct Shard {
   float* logits = nullptr;
   __half* kc = nullptr;
   __half* vc = nullptr;
+  __half* xn = nullptr;    // x-streaming plan: LayerNorm output fp16 [B][h]
+  int8_t* xq = nullptr;    // x-streaming plan, int8: quantised x [B][max(h, F/t)]
+  float* xsc = nullptr;    // its per-token scales [B]
   long long* lnstats = nullptr;  // [2L+1][kLnSlotWords]: LayerNorm row sums from the producing epilogue
   unsigned* amax = nullptr;      // [2L][kAmaxSlotWords]: int8 activation row max from the producer
   gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
@@ -109,7 +112,12 @@ struct dsinf_model {
   // TP = 1: the attn-out / MLP-down epilogues add the residual and emit the next LayerNorm's
   // row sums, so the LN prologues skip their full-row statistics pass (DSINF_FUSE_STATS=0: off)
   bool fuse_ln = false;
-  unsigned long long* ltrace = nullptr;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
+  // x-streaming GEMM plans (gemm::Plan::x_stream): x reaches each stage by TMA next to the
+  // weights instead of a per-CTA smem slice.  xs_ln: the LayerNorm GEMMs (QKV, MLP-up, LM head)
+  // take x from a row_prep launch; xs_od: attn-out / MLP-down (int8: after a quantise prep).
+  bool xs_ln = false, xs_od = false, xs_lm = false;
+  unsigned long long* ltrace = nullptr;
+  std::vector<int> ltrace_kinds;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
   int64_t ltrace_n = 0;
 
   void* alloc(size_t bytes) {
@@ -274,13 +282,18 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.vc, 0, kv * 2, s));
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.d_mlp, 0, B * h * 4, s));
   if (m.fuse_ln) sh.lnstats = m.alloc_n<long long>((2 * m.L + 1) * gemm::kLnSlotWords);
+  if (m.xs_ln || m.xs_lm) sh.xn = m.alloc_n<__half>(static_cast<int64_t>(B) * h);
+  if (m.int8 && (m.xs_ln || m.xs_od)) {
+    sh.xq = m.alloc_n<int8_t>(static_cast<int64_t>(B) * std::max(h, Fl));
+    sh.xsc = m.alloc_n<float>(B);
+  }
   if (m.int8) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
   const bool i8 = m.int8;
-  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0);
-  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0);
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0);
-  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0);
-  sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0);
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln);
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od);
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln);
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od);
+  sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm);
 }
 
 gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w) {
@@ -412,19 +425,60 @@ struct Enqueuer {
   bool pdl;
   int64_t launches = 0;
 
-  // DSINF_PDL_MASK bits: 0 qkv, 1 attention, 2 attn-out, 3 up, 4 down, 5 lm head, 6 the rest.
-  // Default: only the attn-out GEMM (its weight prefetch overlaps the latency-bound attention);
-  // early-launched dependents of the full-machine GEMMs steal SM slots and measured slower.
-  int mask = [] { const char* v = std::getenv("DSINF_PDL_MASK"); return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x04; }();
+  // DSINF_PDL_MASK bits: 0 qkv, 1 attention, 2 attn-out, 3 up, 4 down, 5 lm head, 6 the rest,
+  // 7 row_prep.
+  // Default 0x8d: QKV, attn-out, MLP-up and row_prep launch early (their weight streams / launch
+  // latency overlap the small kernels before them); early dependents of the full-machine GEMMs
+  // (MLP-down, LM head after a GEMM) steal SM slots and measured slower.
+  int mask = [] { const char* v = std::getenv("DSINF_PDL_MASK"); return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x8d; }();
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
   int64_t pdl_launches = 0;
 
   // DSINF_LAUNCH_TRACE: per-launch [first CTA start, last CTA end] stamps, in launch order
   int slot = 0;
-  unsigned long long* tslot() {
+  unsigned long long* tslot(int kind) {
     if (!m.ltrace || slot >= ptx::kTraceEnd) return nullptr;
+    if (static_cast<int>(m.ltrace_kinds.size()) <= slot) m.ltrace_kinds.resize(slot + 1);
+    m.ltrace_kinds[slot] = kind;
     return m.ltrace + slot++;
+  }
+
+  void prep(Shard& sh, int mode, const float* res, const long long* stats, const float* delta, const __half* dbias,
+            float* res_out, const __half* g, const __half* b, const __half* x, int x_ld, const unsigned* amax, int K,
+            bool to_int8) {
+    ops::PrepParams pp{};
+    pp.mode = mode;
+    pp.res = res;
+    pp.ln_stats = stats;
+    pp.res_delta = delta;
+    pp.delta_bias = dbias;
+    pp.res_out = res_out;
+    pp.ln_g = g;
+    pp.ln_b = b;
+    pp.eps = m.rt.ln_eps;
+    pp.x = x;
+    pp.x_ld = x_ld;
+    pp.amax = amax;
+    pp.out = to_int8 ? static_cast<void*>(sh.xq) : static_cast<void*>(sh.xn);
+    pp.out_scale = sh.xsc;
+    pp.B = m.B;
+    pp.K = K;
+    pp.trace = tslot(DSINF_LK_PREP);
+    ops::row_prep(pp, s, P(7));
+    ++launches;
+  }
+
+  // LayerNorm GEMM x via row_prep (x-streaming plan): fp16 xn, or int8 xq + scales
+  void ln_x(Shard& sh, gemm::Params& p, const float* res, const long long* stats, const float* delta,
+            const __half* dbias, float* res_out, const __half* g, const __half* b, bool int8_w) {
+    const int h = static_cast<int>(m.h);
+    prep(sh, int8_w ? ops::PREP_LN_I8 : ops::PREP_LN_F16, res, stats, delta, dbias, res_out, g, b, nullptr, 0, nullptr,
+         h, int8_w);
+    p.pro = int8_w ? gemm::PRO_I8 : gemm::PRO_F16;
+    p.x = int8_w ? static_cast<const void*>(sh.xq) : static_cast<const void*>(sh.xn);
+    p.x_ld = h;
+    p.x_scale = sh.xsc;
   }
 
   long long* lnslot(Shard& sh, int i) const { return sh.lnstats ? sh.lnstats + static_cast<int64_t>(i) * gemm::kLnSlotWords : nullptr; }
@@ -432,7 +486,8 @@ struct Enqueuer {
 
   void gemm_launch(const gemm::Params& p_in, const gemm::Plan& plan, bool int8_w, int bit) {
     gemm::Params p = p_in;
-    p.trace = tslot();
+    p.trace = tslot(bit == 0 ? DSINF_LK_QKV : bit == 2 ? DSINF_LK_O : bit == 3 ? DSINF_LK_UP : bit == 4 ? DSINF_LK_DOWN
+                                                                                                  : DSINF_LK_LM);
     pdl_launches += P(bit);
     gemm::launch(p, plan, int8_w, s, P(bit));
     ++launches;
@@ -442,17 +497,23 @@ struct Enqueuer {
     const LayerW& w = sh.layers[l];
     const int N = static_cast<int>(3 * m.Hl * m.d);
     gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8);
-    p.pro = gemm::PRO_LN;
-    p.res_in = sh.res[0];
-    if (m.fuse_ln) {
-      p.ln_stats_in = lnslot(sh, 2 * l);
+    if (m.xs_ln) {
+      ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l), m.fuse_ln || l == 0 ? nullptr : sh.d_mlp,
+           m.fuse_ln || l == 0 ? nullptr : sh.layers[l - 1].bdown, m.fuse_ln ? nullptr : sh.res[1], w.ln1g, w.ln1b,
+           m.int8);
     } else {
-      p.res_delta = l > 0 ? sh.d_mlp : nullptr;
-      p.delta_bias = l > 0 ? sh.layers[l - 1].bdown : nullptr;
-      p.res_out = sh.res[1];
+      p.pro = gemm::PRO_LN;
+      p.res_in = sh.res[0];
+      if (m.fuse_ln) {
+        p.ln_stats_in = lnslot(sh, 2 * l);
+      } else {
+        p.res_delta = l > 0 ? sh.d_mlp : nullptr;
+        p.delta_bias = l > 0 ? sh.layers[l - 1].bdown : nullptr;
+        p.res_out = sh.res[1];
+      }
+      p.ln_g = w.ln1g;
+      p.ln_b = w.ln1b;
     }
-    p.ln_g = w.ln1g;
-    p.ln_b = w.ln1b;
     p.epi = gemm::EPI_QKV;
     p.bias = w.bqkv;
     p.q_out = sh.q;
@@ -481,7 +542,7 @@ struct Enqueuer {
     a.max_seq = m.max_ctx;
     a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
     a.amax_out = amslot(sh, 2 * l);
-    a.trace = tslot();
+    a.trace = tslot(DSINF_LK_ATTN);
     ops::attention(a, m.attn_chunks, s, P(1));
     ++launches;
   }
@@ -493,6 +554,13 @@ struct Enqueuer {
     p.x = sh.a;
     p.x_ld = static_cast<int>(m.Hl * m.d);
     p.amax_in = amslot(sh, 2 * l);
+    if (m.xs_od && m.int8) {  // quantise once (row max from attention), then stream int8 x
+      prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.a, p.x_ld,
+           amslot(sh, 2 * l), p.x_ld, true);
+      p.pro = gemm::PRO_I8;
+      p.x = sh.xq;
+      p.x_scale = sh.xsc;
+    }
     if (m.fuse_ln) {  // residual += attn-out + bias; emits LN2's row sums
       p.epi = gemm::EPI_RESID;
       p.out = sh.res[0];
@@ -508,18 +576,25 @@ struct Enqueuer {
   void k4_up(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
-    p.pro = gemm::PRO_LN;
-    if (m.fuse_ln) {
-      p.res_in = sh.res[0];
-      p.ln_stats_in = lnslot(sh, 2 * l + 1);
+    if (m.xs_ln) {
+      if (m.fuse_ln)
+        ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.int8);
+      else
+        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.int8);
     } else {
-      p.res_in = sh.res[1];
-      p.res_delta = sh.d_attn;
-      p.delta_bias = w.bo;
-      p.res_out = sh.res[0];
+      p.pro = gemm::PRO_LN;
+      if (m.fuse_ln) {
+        p.res_in = sh.res[0];
+        p.ln_stats_in = lnslot(sh, 2 * l + 1);
+      } else {
+        p.res_in = sh.res[1];
+        p.res_delta = sh.d_attn;
+        p.delta_bias = w.bo;
+        p.res_out = sh.res[0];
+      }
+      p.ln_g = w.ln2g;
+      p.ln_b = w.ln2b;
     }
-    p.ln_g = w.ln2g;
-    p.ln_b = w.ln2b;
     p.epi = gemm::EPI_GELU_F16;
     p.bias = w.bup;
     p.out = sh.u;
@@ -534,6 +609,13 @@ struct Enqueuer {
     p.x = sh.u;
     p.x_ld = static_cast<int>(m.Fl);
     p.amax_in = amslot(sh, 2 * l + 1);
+    if (m.xs_od && m.int8) {
+      prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.u, p.x_ld,
+           amslot(sh, 2 * l + 1), p.x_ld, true);
+      p.pro = gemm::PRO_I8;
+      p.x = sh.xq;
+      p.x_scale = sh.xsc;
+    }
     if (m.fuse_ln) {  // residual += mlp-down + bias; emits the next LayerNorm's row sums
       p.epi = gemm::EPI_RESID;
       p.out = sh.res[0];
@@ -548,17 +630,22 @@ struct Enqueuer {
 
   void lm_head(Shard& sh) {
     gemm::Params p = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), static_cast<int>(m.h), false);
-    p.pro = gemm::PRO_LN;
-    p.res_in = sh.res[0];
-    if (m.fuse_ln) {
-      p.ln_stats_in = lnslot(sh, 2 * static_cast<int>(m.L));
+    if (m.xs_lm) {
+      ln_x(sh, p, sh.res[0], lnslot(sh, 2 * static_cast<int>(m.L)), m.fuse_ln || m.L == 0 ? nullptr : sh.d_mlp,
+           m.fuse_ln || m.L == 0 ? nullptr : sh.layers[m.L - 1].bdown, nullptr, sh.lnfg, sh.lnfb, false);
     } else {
-      p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
-      p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
+      p.pro = gemm::PRO_LN;
+      p.res_in = sh.res[0];
+      if (m.fuse_ln) {
+        p.ln_stats_in = lnslot(sh, 2 * static_cast<int>(m.L));
+      } else {
+        p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
+        p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
+      }
+      p.res_out = nullptr;
+      p.ln_g = sh.lnfg;
+      p.ln_b = sh.lnfb;
     }
-    p.res_out = nullptr;
-    p.ln_g = sh.lnfg;
-    p.ln_b = sh.lnfb;
     p.epi = gemm::EPI_F32;
     p.out = sh.logits;
     gemm_launch(p, sh.plan_lm, false, 5);
@@ -571,7 +658,7 @@ struct Enqueuer {
     ap.idx_offset = first;
     ap.out_val = m.am_val + sh.rank * m.B;
     ap.out_idx = m.am_idx + sh.rank * m.B;
-    ap.trace = tslot();
+    ap.trace = tslot(DSINF_LK_ARGMAX);
     ops::argmax(ap, s, P(6));
     ++launches;
   }
@@ -624,7 +711,7 @@ struct Enqueuer {
       e.h = static_cast<int>(m.h);
       e.V = static_cast<int>(m.V);
       e.ln_stats_out = lnslot(sh, 0);
-      e.trace = tslot();
+      e.trace = tslot(DSINF_LK_EMBED);
       ops::embed(e, s, P(6));
       ++launches;
     }
@@ -753,6 +840,15 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     {
       const char* fs = std::getenv("DSINF_FUSE_STATS");
       m->fuse_ln = m->t == 1 && (fs == nullptr || std::atoi(fs) != 0);
+      // x-streaming plans need 16-byte rows of GEMM-ready x
+      const int64_t Fl = 4 * m->h / m->t, Ol = m->h / m->t;
+      const bool rows16 = m->int8 ? (m->h % 16 == 0 && Fl % 16 == 0 && Ol % 16 == 0) : (Ol % 8 == 0 && Fl % 8 == 0);
+      m->xs_ln = rows16 && gemm::prefer_x_stream(m->B);
+      const char* od = std::getenv("DSINF_XS_OD");
+      const int od_v = od ? std::atoi(od) : -1;
+      m->xs_od = rows16 && (m->int8 ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
+      const char* lm = std::getenv("DSINF_XS_LM");
+      m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
     }
     if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
       require(nccl_comm != nullptr, "NCCL mode needs a communicator");
@@ -893,14 +989,15 @@ int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t
     require(m->ltrace != nullptr, "launch trace disabled (set DSINF_LAUNCH_TRACE=1 before model creation)");
     if (launches) *launches = m->ltrace_n;
     if (out) {
-      require(len >= 2 * m->ltrace_n, "trace buffer too small");
+      require(len >= 3 * m->ltrace_n, "trace buffer too small");
       std::vector<unsigned long long> st(m->ltrace_n), en(m->ltrace_n);
       DSINF_CUDA_CHECK(cudaDeviceSynchronize());
       DSINF_CUDA_CHECK(cudaMemcpy(st.data(), m->ltrace, m->ltrace_n * 8, cudaMemcpyDeviceToHost));
       DSINF_CUDA_CHECK(cudaMemcpy(en.data(), m->ltrace + ptx::kTraceEnd, m->ltrace_n * 8, cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < m->ltrace_n; ++i) {
-        out[2 * i] = st[i];
-        out[2 * i + 1] = en[i];
+        out[3 * i] = st[i];
+        out[3 * i + 1] = en[i];
+        out[3 * i + 2] = i < static_cast<int64_t>(m->ltrace_kinds.size()) ? m->ltrace_kinds[i] : ~0ull;
       }
     }
   });

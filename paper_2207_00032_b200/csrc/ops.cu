@@ -281,6 +281,153 @@ __global__ void select_kernel(const __grid_constant__ SelectParams p) {
   if (threadIdx.x == 0) *p.pos = pos + 1;
 }
 
+// ---------------------------------------------------------------- row preparation (x streaming)
+constexpr int kPrepThreads = 512;
+constexpr int kPrepVec = 8;  // float4 per thread held in registers: K <= 16384
+
+__device__ __forceinline__ uint32_t prep_q(float y, float s) {
+  int q = __float2int_rn(__fdiv_rn(y, s));
+  q = max(-127, min(127, q));
+  return static_cast<uint32_t>(q) & 0xffu;
+}
+
+__global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_constant__ PrepParams p) {
+  ptx::trace_begin(p.trace);
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int b = blockIdx.x;
+  const int K4 = p.K / 4;
+  __shared__ float red[kPrepThreads / 32];
+  if (p.mode == PREP_QUANT_I8) {
+    float mx = 0.f;
+    for (int s = 0; s < gemm::kStatStripes; ++s) mx = fmaxf(mx, __uint_as_float(__ldcg(p.amax + s * 32 + b)));
+    const float scale = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+    if (threadIdx.x == 0) p.out_scale[b] = scale;
+    const __half* row = p.x + static_cast<size_t>(b) * p.x_ld;
+    uint32_t* out = reinterpret_cast<uint32_t*>(static_cast<int8_t*>(p.out) + static_cast<size_t>(b) * p.K);
+#pragma unroll 4
+    for (int c = threadIdx.x; c < K4; c += kPrepThreads) {
+      const uint2 u = __ldcg(reinterpret_cast<const uint2*>(row) + c);
+      const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x), h23 = *reinterpret_cast<const __half2*>(&u.y);
+      out[c] = prep_q(__low2float(h01), scale) | (prep_q(__high2float(h01), scale) << 8) |
+               (prep_q(__low2float(h23), scale) << 16) | (prep_q(__high2float(h23), scale) << 24);
+    }
+    ptx::trace_end(p.trace);
+    return;
+  }
+  // LayerNorm of the residual row (same expression as the fused GEMM prologue, so both plans
+  // produce identical x); statistics from the producer or summed here in the same fixed point
+  const size_t rb = static_cast<size_t>(b) * p.K;
+  float4 v[kPrepVec];
+  long long s1 = 0, s2 = 0;
+#pragma unroll
+  for (int u = 0; u < kPrepVec; ++u) {
+    const int c = threadIdx.x + u * kPrepThreads;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < K4) {
+      v[u] = __ldcg(reinterpret_cast<const float4*>(p.res + rb) + c);
+      if (p.res_delta) {
+        float4 t = __ldcg(reinterpret_cast<const float4*>(p.res_delta + rb) + c);
+        if (p.delta_bias) {
+          const __half2 d01 = *reinterpret_cast<const __half2*>(p.delta_bias + 4 * c);
+          const __half2 d23 = *reinterpret_cast<const __half2*>(p.delta_bias + 4 * c + 2);
+          t.x = __fadd_rn(t.x, __low2float(d01));
+          t.y = __fadd_rn(t.y, __high2float(d01));
+          t.z = __fadd_rn(t.z, __low2float(d23));
+          t.w = __fadd_rn(t.w, __high2float(d23));
+        }
+        v[u].x = __fadd_rn(v[u].x, t.x);
+        v[u].y = __fadd_rn(v[u].y, t.y);
+        v[u].z = __fadd_rn(v[u].z, t.z);
+        v[u].w = __fadd_rn(v[u].w, t.w);
+      }
+      if (p.res_out) reinterpret_cast<float4*>(p.res_out + rb)[c] = v[u];
+      if (!p.ln_stats) {
+        const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          s1 += __float2ll_rn(__fmul_rn(e[i], gemm::kSumScale));
+          s2 += __float2ll_rn(__fmul_rn(__fmul_rn(e[i], e[i]), gemm::kSqScale));
+        }
+      }
+    }
+  }
+  __shared__ long long lred[2][kPrepThreads / 32];
+  if (p.ln_stats) {
+    for (int s = 0; s < gemm::kStatStripes; ++s) {
+      s1 += __ldcg(p.ln_stats + (s * gemm::kMaxB + b) * 2);
+      s2 += __ldcg(p.ln_stats + (s * gemm::kMaxB + b) * 2 + 1);
+    }
+  } else {  // integer block sum: exact, order-independent
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      lred[0][threadIdx.x >> 5] = s1;
+      lred[1][threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    s1 = s2 = 0;
+    for (int w = 0; w < kPrepThreads / 32; ++w) {
+      s1 += lred[0][w];
+      s2 += lred[1][w];
+    }
+  }
+  const double m = static_cast<double>(s1) / (static_cast<double>(gemm::kSumScale) * p.K);
+  const double e2 = static_cast<double>(s2) / (static_cast<double>(gemm::kSqScale) * p.K);
+  const float mean = static_cast<float>(m);
+  const float rstd = static_cast<float>(1.0 / sqrt(fmax(e2 - m * m, 0.0) + static_cast<double>(p.eps)));
+  uint2 hv[kPrepVec];
+  float mx = 0.f;
+#pragma unroll
+  for (int u = 0; u < kPrepVec; ++u) {
+    const int c = threadIdx.x + u * kPrepThreads;
+    if (c < K4) {
+      const uint2 g = *reinterpret_cast<const uint2*>(p.ln_g + 4 * c);
+      const uint2 be = *reinterpret_cast<const uint2*>(p.ln_b + 4 * c);
+      const __half2 g01 = *reinterpret_cast<const __half2*>(&g.x), g23 = *reinterpret_cast<const __half2*>(&g.y);
+      const __half2 b01 = *reinterpret_cast<const __half2*>(&be.x), b23 = *reinterpret_cast<const __half2*>(&be.y);
+      const __half2 h01 = __floats2half2_rn((v[u].x - mean) * rstd * __low2float(g01) + __low2float(b01),
+                                            (v[u].y - mean) * rstd * __high2float(g01) + __high2float(b01));
+      const __half2 h23 = __floats2half2_rn((v[u].z - mean) * rstd * __low2float(g23) + __low2float(b23),
+                                            (v[u].w - mean) * rstd * __high2float(g23) + __high2float(b23));
+      hv[u].x = *reinterpret_cast<const uint32_t*>(&h01);
+      hv[u].y = *reinterpret_cast<const uint32_t*>(&h23);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(__low2float(h01)), fabsf(__high2float(h01))),
+                           fmaxf(fabsf(__low2float(h23)), fabsf(__high2float(h23)))));
+    }
+  }
+  if (p.mode == PREP_LN_F16) {
+    uint2* out = reinterpret_cast<uint2*>(static_cast<__half*>(p.out) + static_cast<size_t>(b) * p.K);
+#pragma unroll
+    for (int u = 0; u < kPrepVec; ++u) {
+      const int c = threadIdx.x + u * kPrepThreads;
+      if (c < K4) out[c] = hv[u];
+    }
+    ptx::trace_end(p.trace);
+    return;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < kPrepThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  const float scale = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+  if (threadIdx.x == 0) p.out_scale[b] = scale;
+  uint32_t* out = reinterpret_cast<uint32_t*>(static_cast<int8_t*>(p.out) + static_cast<size_t>(b) * p.K);
+#pragma unroll
+  for (int u = 0; u < kPrepVec; ++u) {
+    const int c = threadIdx.x + u * kPrepThreads;
+    if (c < K4) {
+      const __half2 h01 = *reinterpret_cast<const __half2*>(&hv[u].x), h23 = *reinterpret_cast<const __half2*>(&hv[u].y);
+      out[c] = prep_q(__low2float(h01), scale) | (prep_q(__high2float(h01), scale) << 8) |
+               (prep_q(__low2float(h23), scale) << 16) | (prep_q(__high2float(h23), scale) << 24);
+    }
+  }
+  ptx::trace_end(p.trace);
+}
+
 __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams p) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
@@ -293,6 +440,13 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
 }
 
 }  // namespace
+
+void row_prep(const PrepParams& p, cudaStream_t s, bool pdl) {
+  if (p.K % 8 != 0 || p.K / 4 > kPrepThreads * kPrepVec) throw ConfigError("row_prep: K must be a multiple of 8, <= 16384");
+  if (p.mode == PREP_QUANT_I8 && (p.x_ld % 4 != 0 || (reinterpret_cast<uintptr_t>(p.x) & 7) != 0))
+    throw ConfigError("row_prep: x rows must be 8-byte aligned");
+  launch_pdl(row_prep_kernel, dim3(p.B), dim3(kPrepThreads), 0, s, pdl, p);
+}
 
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s) {
   const int64_t total = (m.K_local + 1) / 2 * m.N_local;

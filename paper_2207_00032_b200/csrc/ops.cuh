@@ -53,6 +53,34 @@ int attention_chunks(int B, int H);
 void configure();
 void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl);
 
+// Row preparation for the x-streaming GEMM plan (large batch): one CTA per batch row writes the
+// GEMM-ready x of the next SBI-GeMM.
+enum PrepMode : int {
+  PREP_LN_F16 = 0,    // out fp16 = LayerNorm(res) with the producer's row sums
+  PREP_LN_I8 = 1,     // out int8 = quantise(fp16 LayerNorm(res)), scale = row max / 127
+  PREP_QUANT_I8 = 2,  // out int8 = quantise(x fp16), scale from the producer's row max
+};
+struct PrepParams {
+  int mode;
+  const float* res;            // LN: residual [B][K] fp32
+  const float* res_delta;      // LN, optional: residual = res + (res_delta + delta_bias) ...
+  const __half* delta_bias;
+  float* res_out;              // ... stored here (this kernel is the row's only writer)
+  const long long* ln_stats;   // LN: fixed-point row sums (gemm::kLnSlotWords layout), or null:
+                               // computed here with the same fixed-point scheme
+  const __half* ln_g;
+  const __half* ln_b;
+  float eps;
+  const __half* x;             // QUANT: fp16 [B][x_ld]
+  int x_ld;
+  const unsigned* amax;        // QUANT: row max stripes (gemm::kAmaxSlotWords layout)
+  void* out;                   // [B][K] fp16 or int8 (row stride K)
+  float* out_scale;            // int8: [B]
+  int B, K;
+  unsigned long long* trace;
+};
+void row_prep(const PrepParams& p, cudaStream_t s, bool pdl);
+
 // Step-boundary kernels.
 struct EmbedParams {
   const __half* wte;      // [V][h]

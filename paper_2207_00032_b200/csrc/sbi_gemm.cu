@@ -39,14 +39,16 @@ using dev::Header;
 // Dynamic smem (base rounded up to 1024 B for the 128B swizzle):
 //   [ring: stages x 16 KB] [header 1 KB] [x slice: B rows x x_row_words words]
 // After the main loop the ring is reused for the split-K partials part[b][n].
-template <bool kInt8, int kNB8>
+// kXS (x-streaming, large batch): stages are 18 KB (weights + the x box), no x slice.
+template <bool kInt8, int kNB8, bool kXS>
 __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
+  constexpr int kSB = kXS ? kStageBytesXS : kStageBytes;
   uint8_t* ring = smem;
-  Header& hd = *reinterpret_cast<Header*>(smem + stages * kStageBytes);
-  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + stages * kStageBytes + kHeaderBytes);
+  Header& hd = *reinterpret_cast<Header*>(smem + stages * kSB);
+  uint32_t* sx = reinterpret_cast<uint32_t*>(smem + stages * kSB + kHeaderBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -62,6 +64,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   ptx::trace_begin(p.trace);
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.tmap);
+    if (kXS) ptx::prefetch_tensormap(&p.xmap);
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(&hd.full[s], 1);
       ptx::mbar_init(&hd.empty[s], kConsumerWarps);
@@ -72,7 +75,40 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 
   if (warp == 0) {
     // ================= producer: one elected thread issues 4 TMA boxes per stage
-    if (lane == 0) {
+    if (kXS && lane == 0) {
+      // weights of the first `stages` stages before the dependency, their x boxes after it
+      const uint64_t policy = ptx::policy_evict_first();
+      const uint64_t xpolicy = ptx::policy_evict_last();  // x is re-read by every column tile
+      const uint32_t tx = kStageBytes + p.B * 128;
+      const int pre = min(stages, n_iters);
+      for (int it = 0; it < pre; ++it) {
+        ptx::mbar_arrive_expect_tx(&hd.full[it], tx);
+        const int r0 = row_begin + it * kRowsPerStage;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w)
+          ptx::tma_load_2d(ring + it * kSB + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[it], policy);
+      }
+      ptx::pdl_wait();
+      for (int it = 0; it < pre; ++it)
+        ptx::tma_load_2d(ring + it * kSB + kStageBytes, &p.xmap, row_begin + it * kRowsPerStage, 0, &hd.full[it],
+                         xpolicy);
+      int s = pre % stages;
+      uint32_t phase = pre == stages ? 1u : 0u;
+      for (int it = pre; it < n_iters; ++it) {
+        ptx::mbar_wait(&hd.empty[s], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&hd.full[s], tx);
+        const int r0 = row_begin + it * kRowsPerStage;
+        uint8_t* dst = ring + s * kSB;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w)
+          ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
+        ptx::tma_load_2d(dst + kStageBytes, &p.xmap, r0, 0, &hd.full[s], xpolicy);
+        if (++s == stages) {
+          s = 0;
+          phase ^= 1;
+        }
+      }
+    } else if (lane == 0) {
       const uint64_t policy = ptx::policy_evict_first();
       int s = 0;
       uint32_t phase = 0;
@@ -102,8 +138,15 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
     ptx::pdl_wait();
-    if (!kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr) {
+    if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
+      if (kInt8 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
+    } else if (!kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr) {
       dev::fill_x_ln_f16_pre(p, sx, hd, row_begin, p.rows_per_split, ctid);
+    } else if (kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr && dev::ln_i8_fits(p.B, p.K)) {
+      dev::fill_x_ln_i8_regs(p, sx, hd, row_begin, p.rows_per_split, ctid, cw, lane);
+    } else if (kInt8 && p.pro == PRO_QUANT && p.amax_in != nullptr && (p.x_ld % 4) == 0 && (p.K % 4) == 0 &&
+               (reinterpret_cast<uintptr_t>(p.x) & 7) == 0) {
+      dev::fill_x_quant_pre(p, sx, hd, row_begin, p.rows_per_split, ctid);
     } else {
       if (p.pro == PRO_LN)
         dev::ln_row_stats<kInt8>(p, hd, ctid, cw, lane, p.res_out != nullptr && tile == 0 && split == 0);
@@ -121,7 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     c.zero();
     int s = 0;
     uint32_t phase = 0;
-    c.run(ring, hd, stages, s, phase, n_iters, sx, p.x_row_words, p.B, cw, lane);
+    if constexpr (kXS)
+      c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane);
+    else
+      c.run(ring, hd, stages, s, phase, n_iters, sx, p.x_row_words, p.B, cw, lane);
     ptx::pdl_trigger();
     dev::consumer_bar();  // every consumer is done reading the ring
     c.store(reinterpret_cast<typename dev::Consumer<kInt8, kNB8>::Acc*>(ring), kPartLd, p.B, cw);
@@ -146,11 +192,16 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       const int n = n0 + c;
       if (n >= p.N) continue;
       const bool has1 = n + 1 < p.N;
-      float2 rin = make_float2(0.f, 0.f);  // issue the residual read ahead of the DSMEM reads
+      float2 rin = make_float2(0.f, 0.f);  // issue the residual / scale reads ahead of the DSMEM reads
       if (p.epi == EPI_RESID) {
         const float* o = static_cast<const float*>(p.out) + static_cast<size_t>(b) * p.out_ld + n;
         rin.x = __ldcg(o);
         if (has1) rin.y = __ldcg(o + 1);
+      }
+      float2 ws = make_float2(0.f, 0.f);
+      if constexpr (kInt8) {
+        ws.x = __ldg(p.w_scale + n);
+        if (has1) ws.y = __ldg(p.w_scale + n + 1);
       }
       const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
       float y0, y1;
@@ -161,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           s0 += v.x;
           s1 += v.y;
         }
-        dev::dequant_pair(p, hd, b, n, s0, s1, y0, y1);
+        dev::dequant_pair_ws(hd, b, s0, s1, ws, has1, y0, y1);
       } else {
         float2 acc2 = make_float2(0.f, 0.f);
         for (int r = 0; r < nsplit; ++r) {
@@ -184,9 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   ptx::trace_end(p.trace);
 }
 
-template <bool kInt8, int kNB8>
+template <bool kInt8, int kNB8, bool kXS>
 void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pdl) {
-  auto kern = sbi_gemm_kernel<kInt8, kNB8>;
+  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(plan.col_tiles, plan.ksplit, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -209,9 +260,9 @@ void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pd
   DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
 }
 
-template <bool kInt8, int kNB8>
+template <bool kInt8, int kNB8, bool kXS>
 void configure_one() {
-  auto kern = sbi_gemm_kernel<kInt8, kNB8>;
+  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS>;
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
@@ -236,20 +287,27 @@ int env_int(const char* name, int dflt) {
 }
 
 // Co-resident clusters of `split` CTAs for this kernel / smem (cached; 0 when unknown).
-int resident_clusters(bool int8_weights, int nb8, int split, size_t smem) {
+const void* kernel_ptr(bool int8_weights, int nb8, bool xs) {
+  if (int8_weights) {
+    if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, true>)
+                            : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, true>);
+    return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, false>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, false>);
+  }
+  if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, true>)
+                          : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, true>);
+  return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, false>)
+                  : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, false>);
+}
+
+int resident_clusters(bool int8_weights, int nb8, bool xs, int split, size_t smem) {
   static std::mutex mu;
-  static std::map<std::tuple<bool, int, int, size_t>, int> cache;
-  const auto key = std::make_tuple(int8_weights, nb8, split, smem);
+  static std::map<std::tuple<bool, int, bool, int, size_t>, int> cache;
+  const auto key = std::make_tuple(int8_weights, nb8, xs, split, smem);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const void* kern = nullptr;
-  if (int8_weights)
-    kern = nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1>)
-                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2>);
-  else
-    kern = nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1>)
-                    : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2>);
+  const void* kern = kernel_ptr(int8_weights, nb8, xs);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, split, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -286,44 +344,77 @@ void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows) {
 }
 
 void configure() {
-  configure_one<false, 1>();
-  configure_one<false, 2>();
-  configure_one<true, 1>();
-  configure_one<true, 2>();
+  configure_one<false, 1, false>();
+  configure_one<false, 2, false>();
+  configure_one<true, 1, false>();
+  configure_one<true, 2, false>();
+  configure_one<false, 1, true>();
+  configure_one<false, 2, true>();
+  configure_one<true, 1, true>();
+  configure_one<true, 2, true>();
+}
+
+void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words) {
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (ld_words % 4) != 0)
+    throw ConfigError("sbi_gemm: streamed x needs a 16-byte aligned base and row stride");
+  if (B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(words), static_cast<cuuint64_t>(B)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_words) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kRowsPerStage), static_cast<cuuint32_t>(B)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(x), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (x) failed: " + std::to_string(static_cast<int>(r)));
+}
+
+bool prefer_x_stream(int B) {
+  const int v = env_int("DSINF_XS", -1);
+  return v < 0 ? B >= kXsMinBatch : v != 0;
+}
+
+bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
+  const int m = int8_x ? 4 : 2;
+  const size_t row_bytes = static_cast<size_t>(x_ld) * (int8_x ? 1 : 2);
+  return x != nullptr && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (row_bytes % 16) == 0 && (K % m) == 0;
 }
 
 // B200 launch plan (the device half of derive_schedule, gemm.hpp:65-96): like the reference it
 // splits K only when the output tiles alone cannot occupy the machine, but it sizes the split
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split) {
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   const int m = int8_weights ? 4 : 2;
   const int rows = (K + m - 1) / m;
   Plan pl{};
+  pl.x_stream = x_stream ? 1 : 0;
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
   const size_t x_budget = 64 * 1024;
+  const size_t stage_bytes = x_stream ? kStageBytesXS : kStageBytes;
   auto rps_for = [&](int s) {
     int r = (rows + s - 1) / s;
     return (r + kRowsPerStage - 1) / kRowsPerStage * kRowsPerStage;
   };
-  auto x_bytes = [&](int rps) { return static_cast<size_t>(B) * (rps + 8) * 4; };
+  // smem x slice of the non-streaming mode (the streaming mode keeps x in the ring stages)
+  auto x_bytes = [&](int rps) { return x_stream ? size_t{0} : static_cast<size_t>(B) * (rps + 8) * 4; };
   auto valid = [&](int s) {
     const int rps = rps_for(s);
     if ((rows + rps - 1) / rps != s) return false;  // no empty split
     return x_bytes(rps) <= x_budget;
   };
   const int max_stages = std::max(1, std::min(kMaxStages, env_int("DSINF_STAGES", 4)));
+  const int cap_per_sm = env_int("DSINF_CTA_PER_SM", 0);
   auto smem_for = [&](int s, int* stages_out) {
     const int rps = rps_for(s);
     const int iters = rps / kRowsPerStage;
     const size_t fixed = 1024 /*alignment slack*/ + kHeaderBytes + x_bytes(rps);
     int st = std::min(max_stages, std::max(1, iters));
-    while (st > 2 && fixed + st * static_cast<size_t>(kStageBytes) > 110 * 1024) --st;
+    while (st > 2 && fixed + st * stage_bytes > 110 * 1024) --st;
     if (stages_out) *stages_out = st;
     const size_t part_bytes = static_cast<size_t>(B) * kPartLd * 4;
-    return fixed + std::max(static_cast<size_t>(st) * kStageBytes, part_bytes);
+    return fixed + std::max(static_cast<size_t>(st) * stage_bytes, part_bytes);
   };
   int chosen = 0;
   if (forced_split <= 0) forced_split = env_int("DSINF_KSPLIT", 0);
@@ -338,8 +429,9 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split) {
     for (int s = 1; s <= 16; s <<= 1) {
       if (!valid(s)) continue;
       const int units = pl.col_tiles * s;
-      const int clusters = resident_clusters(int8_weights, pl.nb8, s, smem_for(s, nullptr));
-      const int capacity = clusters > 0 ? clusters * s : 2 * 148;
+      const int clusters = resident_clusters(int8_weights, pl.nb8, x_stream, s, smem_for(s, nullptr));
+      int capacity = clusters > 0 ? clusters * s : 2 * 148;
+      if (cap_per_sm > 0) capacity = std::min(capacity, cap_per_sm * 148);  // leave room for PDL overlap
       if (units <= capacity && units > best_units) {
         best_units = units;
         chosen = s;
@@ -363,17 +455,28 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.x_row_words = plan.rows_per_split + 8;
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
-  if (int8_weights) {
-    if (plan.nb8 == 1)
-      launch_impl<true, 1>(p, plan, stream, pdl);
-    else
-      launch_impl<true, 2>(p, plan, stream, pdl);
-  } else {
-    if (plan.nb8 == 1)
-      launch_impl<false, 1>(p, plan, stream, pdl);
-    else
-      launch_impl<false, 2>(p, plan, stream, pdl);
+  const bool xs = plan.x_stream != 0;
+  if (xs) {
+    if (p.pro != (int8_weights ? PRO_I8 : PRO_F16))
+      throw ConfigError("sbi_gemm: the x-streaming plan needs GEMM-ready x (fp16 for fp16 weights, int8 for int8)");
+    if (!x_streamable(p.x, p.x_ld, p.K, int8_weights)) throw ConfigError("sbi_gemm: x cannot be streamed (alignment)");
+    make_x_map(&p.xmap, p.x, p.rows, p.B, p.x_ld / (int8_weights ? 4 : 2));
   }
+#define DSINF_LAUNCH(I8, NB, XS) launch_impl<I8, NB, XS>(p, plan, stream, pdl)
+  if (int8_weights) {
+    if (plan.nb8 == 1) {
+      if (xs) DSINF_LAUNCH(true, 1, true); else DSINF_LAUNCH(true, 1, false);
+    } else {
+      if (xs) DSINF_LAUNCH(true, 2, true); else DSINF_LAUNCH(true, 2, false);
+    }
+  } else {
+    if (plan.nb8 == 1) {
+      if (xs) DSINF_LAUNCH(false, 1, true); else DSINF_LAUNCH(false, 1, false);
+    } else {
+      if (xs) DSINF_LAUNCH(false, 2, true); else DSINF_LAUNCH(false, 2, false);
+    }
+  }
+#undef DSINF_LAUNCH
 }
 
 }  // namespace gemm

@@ -22,6 +22,9 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxB = 16;                                  // batch rows per launch
 constexpr int kPartLd = kColTile + 4;                      // split-K partial row stride (floats)
 constexpr int kHeaderBytes = 1024;                         // barriers + per-row scalars
+// x-streaming mode (large batch): each stage also carries the B x 32-word x tile by TMA
+constexpr int kXBoxBytes = kMaxB * 128;                    // 2 KB (B rows x 128 B, 128B swizzle)
+constexpr int kStageBytesXS = kStageBytes + kXBoxBytes;    // 18 KB, multiple of 1024
 
 // Row statistics handed from a producing epilogue to the next kernel's prologue (TP = 1 path):
 //   LayerNorm: per row, sum(y) and sum(y*y) in fixed point (int64; y * 2^32 and y^2 * 2^28,
@@ -53,6 +56,9 @@ struct Params {
   // packed weights viewed by TMA as a 2-D tensor of 32-bit words [rows][N]; a word holds pack_M
   // consecutive k of one output column (gemm.hpp:108-111)
   alignas(64) CUtensorMap tmap;
+  // x-streaming mode: x as a 2-D tensor of 32-bit words [B][ceil(K/M)] (GEMM-ready fp16 pairs
+  // or int8 quads); each stage loads one box of 32 words x B rows next to the weight boxes
+  alignas(64) CUtensorMap xmap;
   const float* w_scale;  // int8: per-output-row scale [N]
   int N, rows, K, B;
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
@@ -89,6 +95,7 @@ struct Params {
 };
 
 struct Plan {
+  int x_stream;  // 1: x streamed per stage by TMA (PRO_F16 / PRO_I8 only), no smem x slice
   int col_tiles;
   int ksplit;
   int rows_per_split;
@@ -102,7 +109,15 @@ struct Plan {
 void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 // Sets kernel attributes for every instantiation; call before graph capture.
 void configure();
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split);
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false);
+// TMA descriptor of x for the x-streaming mode: `words` 32-bit words per row, `B` rows, row
+// stride ld_words (ld_words * 4 must be a multiple of 16 and x 16-byte aligned).
+void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words);
+// Whether x (fp16 [B][x_ld] or int8) can be streamed: alignment of base and row stride.
+bool x_streamable(const void* x, int x_ld, int K, bool int8_x);
+// Batch sizes that use the x-streaming plan (DSINF_XS=0 never, =1 always; default B >= kXsMinBatch).
+constexpr int kXsMinBatch = 4;
+bool prefer_x_stream(int B);
 void launch(const Params& p, const Plan& plan, bool int8_weights, cudaStream_t stream, bool pdl);
 
 }  // namespace gemm

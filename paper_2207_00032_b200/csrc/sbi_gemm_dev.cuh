@@ -164,7 +164,7 @@ __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int 
     const float mean = rm.active ? hd.mean[rm.b] : 0.f, rstd = rm.active ? hd.rstd[rm.b] : 0.f;
     float mx = 0.f;
     if (rm.active) {
-#pragma unroll 4
+#pragma unroll 8
       for (int c = rm.j; c < K / 4; c += rm.tpr) {
         const float4 v = rv.load4(rm.b, 4 * c);
         const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -180,7 +180,7 @@ __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int 
   float c0 = 0.f, s1 = 0.f, s2 = 0.f;
   if (rm.active) {
     c0 = rv.load4(rm.b, 0).x;  // shift for a cancellation-free single pass
-#pragma unroll 4
+#pragma unroll 8
     for (int c = rm.j; c < K / 4; c += rm.tpr) {
       const float4 v = rv.load4(rm.b, 4 * c);
       if (write_res) *reinterpret_cast<float4*>(p.res_out + static_cast<size_t>(rm.b) * K + 4 * c) = v;
@@ -199,7 +199,7 @@ __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int 
   if (kInt8) {
     float mx = 0.f;
     if (rm.active) {
-#pragma unroll 2
+#pragma unroll 8
       for (int c = rm.j; c < K / 4; c += rm.tpr) {
         const float4 v = rv.load4(rm.b, 4 * c);
         const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -233,7 +233,7 @@ __device__ __forceinline__ void quant_row_scale(const Params& p, Header& hd, int
     const __half* row = x + static_cast<size_t>(rm.b) * p.x_ld;
     const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 7) == 0;
     if (vec) {
-#pragma unroll 4
+#pragma unroll 8
       for (int c = rm.j; c < p.K / 4; c += rm.tpr) {
         const uint2 u = __ldcg(reinterpret_cast<const uint2*>(row + 4 * c));
         const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x);
@@ -254,6 +254,22 @@ __device__ __forceinline__ void quant_row_scale(const Params& p, Header& hd, int
 // Writes packed rows [row0, row0 + nrows) of x into sx[b * xrw + w] (w = row - row0), one 32-bit
 // word per (row, b) holding M = 2 (fp16) or 4 (int8) consecutive k.  Requires the statistics
 // of ln_row_stats / quant_row_scale in `hd` for PRO_LN / PRO_QUANT.
+// Runs store(i, load(i)) for i = ctid, ctid + 128, ... < total with kChunk loads issued before
+// the first store: the slice loads are L2 round trips, so independence (ILP) is what matters.
+template <int kChunk = 8, class Load, class Store>
+__device__ __forceinline__ void chunked(int ctid, int total, Load load, Store store) {
+  using T = decltype(load(0));
+  for (int base = ctid; base < total; base += 128 * kChunk) {
+    T r[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (base + 128 * j < total) r[j] = load(base + 128 * j);
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (base + 128 * j < total) store(base + 128 * j, r[j]);
+  }
+}
+
 // PRO_LN, fp16, statistics from the producer (p.ln_stats_in): the first residual / gamma / beta
 // loads are issued BEFORE the statistics are read, so the two L2 round trips overlap.  Replaces
 // ln_row_stats + consumer_bar + fill_x_slice for this case (all 128 consumer threads call it).
@@ -292,108 +308,225 @@ __device__ __forceinline__ void fill_x_ln_f16_pre(const Params& p, uint32_t* sx,
                                 (r[j].y - mean) * rstd * __high2float(g[j]) + __high2float(be[j]));
     }
   }
-  for (int i = ctid + 128 * kPre; i < total; i += 128) {
-    const int b = i / nrows, w = i - b * nrows;
-    const int k = (row0 + w) * 2;
-    uint32_t word = 0;
-    if (k < K) {
-      const float2 v = __ldcg(reinterpret_cast<const float2*>(p.res_in + static_cast<size_t>(b) * K + k));
-      word = pack_h2(ln_apply(v.x, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k),
-                     ln_apply(v.y, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k + 1));
-    }
-    sx[b * xrw + w] = word;
-  }
+  if (total > 128 * kPre)
+    chunked(ctid + 128 * kPre, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 2;
+      return k < K ? __ldcg(reinterpret_cast<const float2*>(p.res_in + static_cast<size_t>(b) * K + k))
+                   : make_float2(0.f, 0.f);
+    }, [&](int i, float2 v) {
+      const int b = i / nrows, w = i - b * nrows;
+      const int k = (row0 + w) * 2;
+      sx[b * xrw + w] = k < K ? pack_h2(ln_apply(v.x, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k),
+                                        ln_apply(v.y, hd.mean[b], hd.rstd[b], p.ln_g, p.ln_b, k + 1))
+                              : 0u;
+    });
 }
 
-template <bool kInt8>
+// PRO_LN with int8 weights and producer statistics, when the row fits in registers
+// (K/4 <= tpr * kLnRegVec float4 per thread): the residual row, gamma, beta and the statistics
+// are loaded in ONE L2 round trip; the fp16-rounded normalised row gives the per-token scale
+// (row max), and the slice words are quantised straight from registers.
+constexpr int kLnRegVec = 8;
+__device__ __forceinline__ bool ln_i8_fits(int B, int K) { return K / 4 <= (128 / next_pow2(B)) * kLnRegVec; }
+
+__device__ __forceinline__ void fill_x_ln_i8_regs(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows,
+                                                  int ctid, int cw, int lane) {
+  const RowMap rm(p.B, ctid);
+  const int K = p.K, K4 = K / 4;
+  const int xrw = p.x_row_words;
+  float4 v[kLnRegVec];
+  uint2 g[kLnRegVec], be[kLnRegVec];
+#pragma unroll
+  for (int u = 0; u < kLnRegVec; ++u) {
+    const int c = rm.j + u * rm.tpr;
+    if (rm.active && c < K4) {
+      v[u] = __ldcg(reinterpret_cast<const float4*>(p.res_in + static_cast<size_t>(rm.b) * K) + c);
+      g[u] = *reinterpret_cast<const uint2*>(p.ln_g + 4 * c);
+      be[u] = *reinterpret_cast<const uint2*>(p.ln_b + 4 * c);
+    }
+  }
+  float mean = 0.f, rstd = 0.f;
+  if (rm.active) ln_from_sums(p.ln_stats_in, rm.b, K, p.ln_eps, mean, rstd);
+  uint2 hv[kLnRegVec];
+  float mx = 0.f;
+#pragma unroll
+  for (int u = 0; u < kLnRegVec; ++u) {
+    const int c = rm.j + u * rm.tpr;
+    if (rm.active && c < K4) {
+      const __half2 g01 = *reinterpret_cast<const __half2*>(&g[u].x), g23 = *reinterpret_cast<const __half2*>(&g[u].y);
+      const __half2 b01 = *reinterpret_cast<const __half2*>(&be[u].x), b23 = *reinterpret_cast<const __half2*>(&be[u].y);
+      const __half2 h01 = __floats2half2_rn((v[u].x - mean) * rstd * __low2float(g01) + __low2float(b01),
+                                            (v[u].y - mean) * rstd * __high2float(g01) + __high2float(b01));
+      const __half2 h23 = __floats2half2_rn((v[u].z - mean) * rstd * __low2float(g23) + __low2float(b23),
+                                            (v[u].w - mean) * rstd * __high2float(g23) + __high2float(b23));
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(__low2float(h01)), fabsf(__high2float(h01))),
+                           fmaxf(fabsf(__low2float(h23)), fabsf(__high2float(h23)))));
+      hv[u].x = *reinterpret_cast<const uint32_t*>(&h01);
+      hv[u].y = *reinterpret_cast<const uint32_t*>(&h23);
+    }
+  }
+  mx = row_reduce<true>(mx, rm.tpr, hd.red, cw, lane);
+  const float scale = act_scale(mx);
+  if (rm.active && rm.j == 0) hd.xscale[rm.b] = scale;
+#pragma unroll
+  for (int u = 0; u < kLnRegVec; ++u) {
+    const int c = rm.j + u * rm.tpr;
+    if (rm.active && c < K4 && c >= row0 && c < row0 + nrows) {
+      const __half2 h01 = *reinterpret_cast<const __half2*>(&hv[u].x), h23 = *reinterpret_cast<const __half2*>(&hv[u].y);
+      sx[rm.b * xrw + (c - row0)] = quant_byte(__low2float(h01), scale) | (quant_byte(__high2float(h01), scale) << 8) |
+                                    (quant_byte(__low2float(h23), scale) << 16) |
+                                    (quant_byte(__high2float(h23), scale) << 24);
+    }
+  }
+  for (int w = max(0, K4 - row0) + ctid; w < nrows; w += 128)  // zero words past K (last split)
+    for (int b = 0; b < p.B; ++b) sx[b * xrw + w] = 0u;
+}
+
+// PRO_QUANT with the row max from the producer (p.amax_in): the first x-slice loads are issued
+// before the scale is read, so the two L2 round trips overlap.
+__device__ __forceinline__ void fill_x_quant_pre(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows,
+                                                 int ctid) {
+  constexpr int kPre = 8;
+  const int K = p.K;
+  const int xrw = p.x_row_words;
+  const int total = p.B * nrows;
+  const __half* x = static_cast<const __half*>(p.x);
+  uint2 r[kPre];
+#pragma unroll
+  for (int j = 0; j < kPre; ++j) {
+    const int i = ctid + 128 * j;
+    r[j] = make_uint2(0u, 0u);
+    if (i < total) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 4;
+      if (k < K) r[j] = __ldcg(reinterpret_cast<const uint2*>(x + static_cast<size_t>(b) * p.x_ld + k));
+    }
+  }
+  if (ctid < p.B) hd.xscale[ctid] = act_scale(amax_from_stripes(p.amax_in, ctid));
+  consumer_bar();
+  auto qword = [](uint2 u, float scale) {
+    const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x), h23 = *reinterpret_cast<const __half2*>(&u.y);
+    return quant_byte(__low2float(h01), scale) | (quant_byte(__high2float(h01), scale) << 8) |
+           (quant_byte(__low2float(h23), scale) << 16) | (quant_byte(__high2float(h23), scale) << 24);
+  };
+#pragma unroll
+  for (int j = 0; j < kPre; ++j) {
+    const int i = ctid + 128 * j;
+    if (i < total) {
+      const int b = i / nrows, w = i - b * nrows;
+      sx[b * xrw + w] = (row0 + w) * 4 < K ? qword(r[j], hd.xscale[b]) : 0u;
+    }
+  }
+  if (total > 128 * kPre)
+    chunked(ctid + 128 * kPre, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 4;
+      return k < K ? __ldcg(reinterpret_cast<const uint2*>(x + static_cast<size_t>(b) * p.x_ld + k)) : make_uint2(0u, 0u);
+    }, [&](int i, uint2 u) {
+      const int b = i / nrows, w = i - b * nrows;
+      sx[b * xrw + w] = (row0 + w) * 4 < K ? qword(u, hd.xscale[b]) : 0u;
+    });
+}
+
+template <bool kInt8, int kChunk = 8>
 __device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, int row0, int nrows, int ctid) {
   const int K = p.K;
-  const int M = kInt8 ? 4 : 2;
   const int xrw = p.x_row_words;
+  const int total = p.B * nrows;
+  auto put = [&](int i, uint32_t word) {
+    const int b = i / nrows;
+    sx[b * xrw + (i - b * nrows)] = word;
+  };
   if (p.pro == PRO_LN) {
     const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
-    for (int b = 0; b < p.B; ++b) {
-      const float mean = hd.mean[b], rstd = hd.rstd[b];
-#pragma unroll 4
-      for (int w = ctid; w < nrows; w += 128) {
-        const int k = (row0 + w) * M;
-        uint32_t word = 0;
-        if (k < K) {  // K % 8 == 0 on this path
-          const float4 v = rv.load4(b, k & ~3);
-          if (!kInt8) {
-            const float va = (k & 2) ? v.z : v.x, vb = (k & 2) ? v.w : v.y;
-            word = pack_h2(ln_apply(va, mean, rstd, p.ln_g, p.ln_b, k), ln_apply(vb, mean, rstd, p.ln_g, p.ln_b, k + 1));
-          } else {
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-            const float scale = hd.xscale[b];
+    // item i -> (b, packed row): fp16 takes 2 consecutive k (half of a float4), int8 all 4
+    chunked<kChunk>(ctid, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * (kInt8 ? 4 : 2);
+      return k < K ? rv.load4(b, k & ~3) : make_float4(0.f, 0.f, 0.f, 0.f);  // K % 8 == 0 on this path
+    }, [&](int i, float4 v) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * (kInt8 ? 4 : 2);
+      uint32_t word = 0;
+      if (k < K) {
+        const float mean = hd.mean[b], rstd = hd.rstd[b];
+        if (!kInt8) {
+          const float va = (k & 2) ? v.z : v.x, vb = (k & 2) ? v.w : v.y;
+          word = pack_h2(ln_apply(va, mean, rstd, p.ln_g, p.ln_b, k), ln_apply(vb, mean, rstd, p.ln_g, p.ln_b, k + 1));
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          const float scale = hd.xscale[b];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float y = __half2float(__float2half_rn(ln_apply(vv[i], mean, rstd, p.ln_g, p.ln_b, k + i)));
-              word |= quant_byte(y, scale) << (8 * i);
-            }
+          for (int e = 0; e < 4; ++e) {
+            const float y = __half2float(__float2half_rn(ln_apply(vv[e], mean, rstd, p.ln_g, p.ln_b, k + e)));
+            word |= quant_byte(y, scale) << (8 * e);
           }
         }
-        sx[b * xrw + w] = word;
       }
-    }
+      put(i, word);
+    });
   } else if (p.pro == PRO_F16) {
     const __half* x = static_cast<const __half*>(p.x);
     const bool vec = (p.x_ld % 2) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
-    for (int b = 0; b < p.B; ++b)
-      for (int w = ctid; w < nrows; w += 128) {
-        const int k = (row0 + w) * 2;
-        uint32_t word = 0;
-        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
-        if (k + 1 < K && vec) {
-          word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
-        } else if (k < K) {
-          const __half lo = __ldcg(x + base);
-          const __half hi = (k + 1 < K) ? __ldcg(x + base + 1) : __float2half(0.f);
-          word = static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
-        }
-        sx[b * xrw + w] = word;
+    chunked<kChunk>(ctid, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 2;
+      const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+      uint32_t word = 0;
+      if (k + 1 < K && vec) {
+        word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
+      } else if (k < K) {
+        const __half lo = __ldcg(x + base);
+        const __half hi = (k + 1 < K) ? __ldcg(x + base + 1) : __float2half(0.f);
+        word = static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
       }
+      return word;
+    }, put);
   } else if (p.pro == PRO_I8) {
     const int8_t* x = static_cast<const int8_t*>(p.x);
     const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
-    for (int b = 0; b < p.B; ++b)
-      for (int w = ctid; w < nrows; w += 128) {
-        const int k = (row0 + w) * 4;
-        uint32_t word = 0;
-        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
-        if (k + 3 < K && vec) {
-          word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
-        } else {
-          for (int i = 0; i < 4; ++i)
-            if (k + i < K) word |= (static_cast<uint32_t>(static_cast<uint8_t>(__ldcg(reinterpret_cast<const signed char*>(x) + base + i)))) << (8 * i);
-        }
-        sx[b * xrw + w] = word;
+    chunked<kChunk>(ctid, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 4;
+      const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+      uint32_t word = 0;
+      if (k + 3 < K && vec) {
+        word = __ldcg(reinterpret_cast<const unsigned int*>(x + base));
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (k + e < K)
+            word |= static_cast<uint32_t>(static_cast<uint8_t>(__ldcg(reinterpret_cast<const signed char*>(x) + base + e)))
+                    << (8 * e);
       }
-  } else {  // PRO_QUANT
+      return word;
+    }, put);
+  } else {  // PRO_QUANT: fp16 x, per-token scale in hd.xscale
     const __half* x = static_cast<const __half*>(p.x);
     const bool vec = (p.x_ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 7) == 0;
-    for (int b = 0; b < p.B; ++b) {
-      const float scale = hd.xscale[b];
-#pragma unroll 4
-      for (int w = ctid; w < nrows; w += 128) {
-        const int k = (row0 + w) * 4;
-        const size_t base = static_cast<size_t>(b) * p.x_ld + k;
-        uint32_t word = 0;
-        if (vec && k + 3 < K) {
-          const uint2 u = __ldcg(reinterpret_cast<const uint2*>(x + base));
-          const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x);
-          const __half2 h23 = *reinterpret_cast<const __half2*>(&u.y);
-          word = quant_byte(__low2float(h01), scale) | (quant_byte(__high2float(h01), scale) << 8) |
-                 (quant_byte(__low2float(h23), scale) << 16) | (quant_byte(__high2float(h23), scale) << 24);
-        } else {
-          for (int i = 0; i < 4; ++i)
-            if (k + i < K) word |= quant_byte(__half2float(__ldcg(x + base + i)), scale) << (8 * i);
-        }
-        sx[b * xrw + w] = word;
+    chunked<kChunk>(ctid, total, [&](int i) {
+      const int b = i / nrows;
+      const int k = (row0 + i - b * nrows) * 4;
+      const size_t base = static_cast<size_t>(b) * p.x_ld + k;
+      uint2 u = make_uint2(0u, 0u);
+      if (vec && k + 3 < K) {
+        u = __ldcg(reinterpret_cast<const uint2*>(x + base));
+      } else {
+        unsigned short hs[4] = {0, 0, 0, 0};
+        for (int e = 0; e < 4; ++e)
+          if (k + e < K) hs[e] = __half_as_ushort(__ldcg(x + base + e));
+        u = make_uint2(hs[0] | (static_cast<uint32_t>(hs[1]) << 16), hs[2] | (static_cast<uint32_t>(hs[3]) << 16));
       }
-    }
+      return u;
+    }, [&](int i, uint2 u) {
+      const int b = i / nrows;
+      const float scale = hd.xscale[b];
+      const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x);
+      const __half2 h23 = *reinterpret_cast<const __half2*>(&u.y);
+      put(i, quant_byte(__low2float(h01), scale) | (quant_byte(__high2float(h01), scale) << 8) |
+                 (quant_byte(__low2float(h23), scale) << 16) | (quant_byte(__high2float(h23), scale) << 24));
+    });
   }
-  (void)M;
 }
 
 // ------------------------------------------------------------------ consumer loop
@@ -478,6 +611,59 @@ struct Consumer {
       }
     }
   }
+  // x-streaming variant: stage s holds the 4 weight boxes then the x box (B rows x 128 B,
+  // 128B-swizzled: 16-byte chunk c of row r sits at chunk c ^ (r & 7)).
+  __device__ __forceinline__ void run_xs(const uint8_t* ring, Header& hd, int stages, int& s, uint32_t& phase,
+                                         int n_iters, int B, int cw, int lane) {
+    bool xvalid[kNB8];
+    uint32_t xoff[kNB8][kRowsPerStage / 8];
+#pragma unroll
+    for (int bt = 0; bt < kNB8; ++bt) {
+      const int r = bt * 8 + g;
+      xvalid[bt] = r < B;
+#pragma unroll
+      for (int ks = 0; ks < kRowsPerStage / 8; ++ks)
+        xoff[bt][ks] = kStageBytes + r * 128 + (((2 * ks + (t >> 1)) ^ (r & 7)) << 4) + ((t & 1) << 3);
+    }
+    const uint8_t* wbox = ring + cw * kBoxBytes;
+    for (int it = 0; it < n_iters; ++it) {
+      ptx::mbar_wait(&hd.full[s], phase);
+      const uint8_t* stage = ring + s * kStageBytesXS;
+      const uint8_t* sw = wbox + s * kStageBytesXS;
+#pragma unroll
+      for (int ks = 0; ks < kRowsPerStage / 8; ++ks) {
+        uint32_t b0[kNB8], b1[kNB8];
+#pragma unroll
+        for (int bt = 0; bt < kNB8; ++bt) {
+          uint2 v = make_uint2(0u, 0u);
+          if (xvalid[bt]) v = *reinterpret_cast<const uint2*>(stage + xoff[bt][ks]);
+          b0[bt] = v.x;
+          b1[bt] = v.y;
+        }
+        const uint8_t* a = sw + ks * 8 * 128;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][0]);
+          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][0]);
+          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][1]);
+          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
+#pragma unroll
+          for (int bt = 0; bt < kNB8; ++bt) {
+            if constexpr (kInt8)
+              ptx::mma_s8(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
+            else
+              ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
+  }
   // part[b * ld + n] for this warp's 32 columns (n relative to the CTA tile).
   __device__ __forceinline__ void store(Acc* part, int ld, int B, int cw) const {
 #pragma unroll
@@ -509,6 +695,13 @@ __device__ __forceinline__ void dequant_pair(const Params& p, const Header& hd, 
   const float xs = hd.xscale[b];
   y0 = __fmul_rn(__fmul_rn(static_cast<float>(s0), xs), p.w_scale[n]);
   y1 = (n + 1 < p.N) ? __fmul_rn(__fmul_rn(static_cast<float>(s1), xs), p.w_scale[n + 1]) : 0.f;
+}
+// Same with the two weight scales already loaded.
+__device__ __forceinline__ void dequant_pair_ws(const Header& hd, int b, int s0, int s1, float2 ws, bool has1,
+                                                float& y0, float& y1) {
+  const float xs = hd.xscale[b];
+  y0 = __fmul_rn(__fmul_rn(static_cast<float>(s0), xs), ws.x);
+  y1 = has1 ? __fmul_rn(__fmul_rn(static_cast<float>(s1), xs), ws.y) : 0.f;
 }
 
 // Epilogue row statistics of one thread's outputs (registers), reduced per warp by row_stat_commit.

@@ -447,7 +447,7 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
   consumer_bar();
   if (I8 && ctid < B) ex.xs[p & 1][ctid] = hd.xscale[ctid];
   if (f.full_x) {
-    gemm::dev::fill_x_slice<I8>(gp, sx, hd, 0, f.spt * kRowsPerStage, ctid);
+    gemm::dev::fill_x_slice<I8, 1>(gp, sx, hd, 0, f.spt * kRowsPerStage, ctid);
     consumer_bar();
   }
   using C = gemm::dev::Consumer<I8, kNB8>;
@@ -458,7 +458,7 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
     const int tile = unit_tile(f, u), chunk = unit_chunk(f, u);
     const int st0 = chunk * f.cs, nst = min(f.spt, st0 + f.cs) - st0;
     if (!f.full_x) {
-      gemm::dev::fill_x_slice<I8>(gp, sx, hd, st0 * kRowsPerStage, nst * kRowsPerStage, ctid);
+      gemm::dev::fill_x_slice<I8, 1>(gp, sx, hd, st0 * kRowsPerStage, nst * kRowsPerStage, ctid);
       consumer_bar();
     }
     c.zero();

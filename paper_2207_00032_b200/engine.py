@@ -131,8 +131,8 @@ class DecoderModel:
         return nxt, hist
 
     def launch_trace(self, steps: int = 8, stream=None):
-        """Per-launch device timeline of `steps` more decode steps: array [steps][launches][2] of
-        globaltimer ns (first CTA start, last CTA end), launch order = the step's enqueue order."""
+        """Per-launch device timeline of `steps` more decode steps: array [steps][launches][3] of
+        (first CTA start ns, last CTA end ns, kind DSINF_LK_*) in the step's enqueue order."""
         capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 1))
         out = []
         try:
@@ -140,10 +140,10 @@ class DecoderModel:
                 self.step(1, stream=stream)
                 n = C.c_int64()
                 capi.check(capi.lib.dsinf_model_launch_trace(self._h, None, 0, C.byref(n)))
-                buf = np.zeros(2 * n.value, dtype=np.uint64)
+                buf = np.zeros(3 * n.value, dtype=np.uint64)
                 capi.check(capi.lib.dsinf_model_launch_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                              buf.size, None))
-                out.append(buf.reshape(-1, 2))
+                out.append(buf.reshape(-1, 3))
         finally:
             capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 0))
         return np.stack(out)

@@ -142,3 +142,24 @@ def test_context_capacity_is_enforced():
     with pytest.raises(capi.InfeasibleError):
         m.step(1)
     m.close()
+
+
+# Both GEMM plans on both sides of the default batch threshold (gemm::kXsMinBatch = 4):
+#   xs:    x streamed by TMA per stage (row_prep launches for LayerNorm / int8 quantisation)
+#   slice: x normalised / quantised into a per-CTA smem slice by the GEMM prologue
+PLANS = {"xs": {"DSINF_XS": "1", "DSINF_XS_OD": "1"}, "slice": {"DSINF_XS": "0", "DSINF_XS_OD": "0"}}
+
+
+@pytest.mark.parametrize("plan", list(PLANS))
+@pytest.mark.parametrize("dtype_bytes,batch", [(2, 1), (2, 16), (1, 1), (1, 8)], ids=["f16b1", "f16b16", "i8b1", "i8b8"])
+def test_gemm_plans(monkeypatch, plan, dtype_bytes, batch):
+    for k, v in PLANS[plan].items():
+        monkeypatch.setenv(k, v)
+    run_parity(512, 2, 8, 2000, batch=batch, dtype_bytes=dtype_bytes, step_kernel=False)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1], ids=["f16", "i8"])
+def test_tp_local_x_stream(monkeypatch, dtype_bytes):
+    """TP without producer statistics: row_prep sums the residual itself and writes it back."""
+    monkeypatch.setenv("DSINF_XS", "1")
+    run_parity(512, 2, 8, 1000, tp=2, batch=4, dtype_bytes=dtype_bytes, step_kernel=False)
