@@ -14,8 +14,10 @@ ORACLE_LIB := oracle/liboracle.so
 REF_LIB := oracle/_ref/libinfersim_ref.so
 
 ARCH := -gencode arch=compute_100a,code=sm_100a
+# DIAG=1: per-CTA / per-phase diagnostics in the SBI-GeMM kernel (tools/phase_trace.py, tools/cta_log.py)
+DIAGFLAGS := $(if $(DIAG),-DDSINF_DIAG,)
 NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xcompiler -ffp-contract=off \
-             --expt-relaxed-constexpr -Iinclude -I$(CSRC) -Xptxas -warn-spills
+             --expt-relaxed-constexpr -Iinclude -I$(CSRC) -Xptxas -warn-spills $(DIAGFLAGS)
 CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC) -I/usr/local/cuda/include
 
 CU_SRCS := $(CSRC)/sbi_gemm.cu $(CSRC)/step_kernel.cu $(CSRC)/attention.cu $(CSRC)/ops.cu $(CSRC)/model.cu $(CSRC)/capi.cu

@@ -249,6 +249,15 @@ int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* 
 #define DSINF_LK_ARGMAX 7
 #define DSINF_LK_PREP 8 /* row preparation (LayerNorm / quantisation) of the x-streaming plan */
 int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* launches);
+/* Phase stamps of the same launches (SBI-GeMM only; other kernels leave ~0 / 0): out[8*i + 0] =
+ * earliest dependency release, [8*i + 1] = latest prologue end, [8*i + 2] = latest main-loop end
+ * (globaltimer ns), [8*i + 3] = longest per-CTA prologue (ns), [8*i + 4] = latest release,
+ * [8*i + 5..7] = sub-phase probes (longest per-CTA time since release, ns).
+ * Diagnostics, not on the reference path. */
+int dsinf_model_launch_phases(dsinf_model* m, uint64_t* out, int64_t len);
+/* Diagnostics (DSINF_CTA_LOG=<n> at creation): per-CTA [smid, start, release, prologue end, loop
+ * end, end] globaltimer stamps of the n-th SBI-GeMM launch of the last step, 6 words per CTA. */
+int dsinf_model_cta_log(dsinf_model* m, uint64_t* out, int64_t len);
 /* Turn the per-launch timeline on (1) or off (0) after creation; re-captures the step graph. */
 int dsinf_model_set_launch_trace(dsinf_model* m, int on);
 /* Bytes per step for an arbitrary position (ctx = pos + 1). */

@@ -170,6 +170,8 @@ SIGNATURES = {
     "dsinf_model_bytes_per_step": (i64, [vp, i64]),
     "dsinf_model_step_trace": (C.c_int, [vp, P(u64), i64, P(i64), P(i32), P(i32)]),
     "dsinf_model_launch_trace": (C.c_int, [vp, P(u64), i64, P(i64)]),
+    "dsinf_model_launch_phases": (C.c_int, [vp, P(u64), i64]),
+    "dsinf_model_cta_log": (C.c_int, [vp, P(u64), i64]),
     "dsinf_model_set_launch_trace": (C.c_int, [vp, i32]),
     "dsinf_synthetic_tensor": (C.c_int, [u64, i32, i32, i64, i64, P(C.c_float)]),
     "dsinf_shard_tensor": (C.c_int, [P(ModelConfig), i32, i32, i32, i32, u64, P(C.c_float), i64, P(i64), P(i64)]),

@@ -42,23 +42,43 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     ptx::cluster_sync();
   else
     __syncthreads();
+  // every rank's (max, sum) in one DSMEM round trip, then this CTA's output dims (all ranks'
+  // partials requested before the first is used)
+  constexpr int kMaxC = 16;
+  float mr[kMaxC], lr[kMaxC];
+#pragma unroll
+  for (int r = 0; r < kMaxC; ++r)
+    if (r < C) {
+      const uint32_t a = ptx::map_shared_rank(&cst[0], r);
+      const float2 v = ptx::ld_dsmem_f2_nc(a);
+      mr[r] = v.x;
+      lr[r] = v.y;
+    }
   float MM = -INFINITY;
-  for (int r = 0; r < C; ++r) MM = fmaxf(MM, ptx::ld_dsmem_f(ptx::map_shared_rank(&cst[0], r)));
-  float wts[16];
+#pragma unroll
+  for (int r = 0; r < kMaxC; ++r)
+    if (r < C) MM = fmaxf(MM, mr[r]);
+  float wts[kMaxC];
   float LL = 0.f;
-  for (int r = 0; r < C; ++r) {
-    const float mr = ptx::ld_dsmem_f(ptx::map_shared_rank(&cst[0], r));
-    const float lr = ptx::ld_dsmem_f(ptx::map_shared_rank(&cst[1], r));
-    const float w = mr == -INFINITY ? 0.f : expf(mr - MM);
-    wts[r] = w;
-    LL += w * lr;
-  }
+#pragma unroll
+  for (int r = 0; r < kMaxC; ++r)
+    if (r < C) {
+      const float w = mr[r] == -INFINITY ? 0.f : expf(mr[r] - MM);
+      wts[r] = w;
+      LL += w * lr[r];
+    }
   const float inv = 1.0f / LL;
   const int hd = p.H * d;
   float amax = 0.f;
   for (int i = c + C * tid; i < d; i += C * kAttnThreads) {
+    float part[kMaxC];
+#pragma unroll
+    for (int r = 0; r < kMaxC; ++r)
+      if (r < C) part[r] = ptx::ld_dsmem_f_nc(ptx::map_shared_rank(&co[i], r));
     float acc = 0.f;
-    for (int r = 0; r < C; ++r) acc = fmaf(wts[r], ptx::ld_dsmem_f(ptx::map_shared_rank(&co[i], r)), acc);
+#pragma unroll
+    for (int r = 0; r < kMaxC; ++r)
+      if (r < C) acc = fmaf(wts[r], part[r], acc);
     const __half o = __float2half_rn(acc * inv);
     p.out[static_cast<size_t>(b) * hd + head * d + i] = o;
     amax = fmaxf(amax, fabsf(__half2float(o)));
@@ -68,7 +88,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     if ((tid & 31) == 0 && m != 0)
       atomicMax(p.amax_out + ((head + c) % gemm::kStatStripes) * 32 + b, m);
   }
-  if (C > 1) ptx::cluster_sync();
+  if (C > 1) ptx::cluster_sync_relaxed();  // peers' DSMEM reads of our partials are consumed
   ptx::trace_end(p.trace);
 }
 

@@ -119,6 +119,8 @@ struct dsinf_model {
   unsigned long long* ltrace = nullptr;
   std::vector<int> ltrace_kinds;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
   int64_t ltrace_n = 0;
+  unsigned long long* cta_log = nullptr;  // DSINF_CTA_LOG=<n>: per-CTA stamps of the n-th SBI-GeMM launch of a step
+  int cta_log_launch = -1;
 
   void* alloc(size_t bytes) {
     void* p = nullptr;
@@ -135,6 +137,7 @@ struct dsinf_model {
     if (graph) cudaGraphDestroy(graph);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& a : allocs) cudaFree(a.p);
+    if (cta_log) cudaFree(cta_log);
   }
 };
 
@@ -434,6 +437,7 @@ struct Enqueuer {
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
   int64_t pdl_launches = 0;
+  int gemm_index = 0;
 
   // DSINF_LAUNCH_TRACE: per-launch [first CTA start, last CTA end] stamps, in launch order
   int slot = 0;
@@ -488,6 +492,7 @@ struct Enqueuer {
     gemm::Params p = p_in;
     p.trace = tslot(bit == 0 ? DSINF_LK_QKV : bit == 2 ? DSINF_LK_O : bit == 3 ? DSINF_LK_UP : bit == 4 ? DSINF_LK_DOWN
                                                                                                   : DSINF_LK_LM);
+    if (m.cta_log && gemm_index++ == m.cta_log_launch) p.cta_log = m.cta_log;
     pdl_launches += P(bit);
     gemm::launch(p, plan, int8_w, s, P(bit));
     ++launches;
@@ -689,6 +694,8 @@ struct Enqueuer {
     if (m.ltrace) {
       DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace, 0xff, ptx::kTraceEnd * sizeof(unsigned long long), s));
       DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + ptx::kTraceEnd, 0, ptx::kTraceEnd * sizeof(unsigned long long), s));
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + 2 * ptx::kTraceEnd, 0xff, ptx::kTraceEnd * sizeof(unsigned long long), s));
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + 3 * ptx::kTraceEnd, 0, (ptx::kTracePhases - 3) * ptx::kTraceEnd * sizeof(unsigned long long), s));
     }
     for (Shard& sh : m.shards) {  // per-step statistics slots
       if (sh.lnstats)
@@ -874,8 +881,12 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     for (auto& sh : m->shards) build_shard(*m, sh, s);
     DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
     if (m->t == 1 && rt->use_step_kernel) build_step_program(*m);
+    if (const char* cl = std::getenv("DSINF_CTA_LOG")) {
+      m->cta_log_launch = std::atoi(cl);
+      DSINF_CUDA_CHECK(cudaMallocManaged(&m->cta_log, 6 * 4096 * sizeof(unsigned long long)));
+    }
     if (const char* lt = std::getenv("DSINF_LAUNCH_TRACE"); lt && std::atoi(lt) != 0)
-      m->ltrace = m->alloc_n<unsigned long long>(2 * ptx::kTraceEnd);
+      m->ltrace = m->alloc_n<unsigned long long>(ptx::kTracePhases * ptx::kTraceEnd);
     *out = m.release();
   });
 }
@@ -969,7 +980,7 @@ int dsinf_model_step_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t* 
 int dsinf_model_set_launch_trace(dsinf_model* m, int on) {
   return guarded([&] {
     require(m != nullptr, "null model");
-    if (on && !m->ltrace) m->ltrace = m->alloc_n<unsigned long long>(2 * ptx::kTraceEnd);
+    if (on && !m->ltrace) m->ltrace = m->alloc_n<unsigned long long>(ptx::kTracePhases * ptx::kTraceEnd);
     if (!on) m->ltrace = nullptr;  // the buffer stays owned by the model until destroy
     m->ltrace_n = 0;
     if (m->exec) {  // launch parameters changed: re-capture the step graph
@@ -1000,6 +1011,27 @@ int dsinf_model_launch_trace(dsinf_model* m, uint64_t* out, int64_t len, int64_t
         out[3 * i + 2] = i < static_cast<int64_t>(m->ltrace_kinds.size()) ? m->ltrace_kinds[i] : ~0ull;
       }
     }
+  });
+}
+
+int dsinf_model_launch_phases(dsinf_model* m, uint64_t* out, int64_t len) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    require(m->ltrace != nullptr, "launch trace disabled");
+    require(out != nullptr && len >= 8 * m->ltrace_n, "phase buffer too small");
+    std::vector<unsigned long long> ph(8 * ptx::kTraceEnd);
+    DSINF_CUDA_CHECK(cudaDeviceSynchronize());
+    DSINF_CUDA_CHECK(cudaMemcpy(ph.data(), m->ltrace + 2 * ptx::kTraceEnd, ph.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < m->ltrace_n; ++i)
+      for (int j = 0; j < 8; ++j) out[8 * i + j] = ph[j * ptx::kTraceEnd + i];
+  });
+}
+
+int dsinf_model_cta_log(dsinf_model* m, uint64_t* out, int64_t len) {
+  return guarded([&] {
+    require(m != nullptr && m->cta_log != nullptr, "cta log disabled (set DSINF_CTA_LOG=<launch> before model creation)");
+    DSINF_CUDA_CHECK(cudaDeviceSynchronize());
+    for (int64_t i = 0; i < std::min<int64_t>(len, 6 * 4096); ++i) out[i] = m->cta_log[i];
   });
 }
 

@@ -7,6 +7,7 @@
 #include "launch.cuh"
 #include "ops.cuh"
 #include "sbi_gemm.cuh"
+#include "sbi_gemm_dev.cuh"
 #include "ptx.cuh"
 #include "synth.h"
 
@@ -374,10 +375,8 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
       s2 += lred[1][w];
     }
   }
-  const double m = static_cast<double>(s1) / (static_cast<double>(gemm::kSumScale) * p.K);
-  const double e2 = static_cast<double>(s2) / (static_cast<double>(gemm::kSqScale) * p.K);
-  const float mean = static_cast<float>(m);
-  const float rstd = static_cast<float>(1.0 / sqrt(fmax(e2 - m * m, 0.0) + static_cast<double>(p.eps)));
+  float mean, rstd;
+  gemm::dev::ln_mean_rstd(s1, s2, p.inv_k, p.eps, mean, rstd);
   uint2 hv[kPrepVec];
   float mx = 0.f;
 #pragma unroll
@@ -441,7 +440,9 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
 
 }  // namespace
 
-void row_prep(const PrepParams& p, cudaStream_t s, bool pdl) {
+void row_prep(const PrepParams& p_in, cudaStream_t s, bool pdl) {
+  PrepParams p = p_in;
+  p.inv_k = 1.0 / static_cast<double>(p.K);
   if (p.K % 8 != 0 || p.K / 4 > kPrepThreads * kPrepVec) throw ConfigError("row_prep: K must be a multiple of 8, <= 16384");
   if (p.mode == PREP_QUANT_I8 && (p.x_ld % 4 != 0 || (reinterpret_cast<uintptr_t>(p.x) & 7) != 0))
     throw ConfigError("row_prep: x rows must be 8-byte aligned");

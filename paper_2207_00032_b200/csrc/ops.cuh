@@ -71,6 +71,7 @@ struct PrepParams {
   const __half* ln_g;
   const __half* ln_b;
   float eps;
+  double inv_k;  // 1 / K (set by row_prep)
   const __half* x;             // QUANT: fp16 [B][x_ld]
   int x_ld;
   const unsigned* amax;        // QUANT: row max stripes (gemm::kAmaxSlotWords layout)

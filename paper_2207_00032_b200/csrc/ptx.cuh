@@ -103,6 +103,10 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Arrive without release semantics (no fence over this thread's outstanding global stores).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t map_shared_rank(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
@@ -116,6 +120,22 @@ __device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
 __device__ __forceinline__ int2 ld_dsmem_i2(uint32_t addr) {
   int2 v;
   asm volatile("ld.shared::cluster.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+// No memory clobber: several of these may be in flight before the first result is used.
+__device__ __forceinline__ uint2 ld_dsmem_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 ld_dsmem_f2_nc(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float ld_dsmem_f_nc(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float ld_dsmem_f(uint32_t addr) {
@@ -141,6 +161,53 @@ __device__ __forceinline__ void trace_begin(unsigned long long* slot) {
 }
 __device__ __forceinline__ void trace_end(unsigned long long* slot) {
   if (slot != nullptr && threadIdx.x == 0) atomicMax(slot + kTraceEnd, gtimer());
+}
+// Phase stamps of SBI-GeMM launches (compiled in with -DDSINF_DIAG, `make DIAG=1`) (thread `tid` of each CTA): slot[2 * kTraceEnd] = earliest
+// dependency release (after griddepcontrol.wait), slot[3 * kTraceEnd] = latest prologue end,
+// slot[4 * kTraceEnd] = latest main-loop end, slot[5 * kTraceEnd] = longest per-CTA prologue
+// (own release -> own prologue end), slot[6 * kTraceEnd] = latest release.
+constexpr int kTracePhases = 10;  // + slots 7..9: sub-phase probes (max over CTAs of t - own release)
+__device__ __forceinline__ unsigned long long trace_release(unsigned long long* slot, int tid) {
+  if (slot == nullptr || threadIdx.x != tid) return 0;
+  const unsigned long long t = gtimer();
+  atomicMin(slot + 2 * kTraceEnd, t);
+  atomicMax(slot + 6 * kTraceEnd, t);
+  return t;
+}
+// Sub-phase probe: max over CTAs of SM clock cycles since `c0` (clock64 at release), read after
+// `dep` is available and after every earlier memory operation of the thread (memory clobber).
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)::"memory");
+  return c;
+}
+__device__ __forceinline__ void trace_sub(unsigned long long* slot, int idx, int tid, long long c0, long long dep = 0) {
+#ifndef DSINF_DIAG
+  return;
+#endif
+  if (slot == nullptr || threadIdx.x != tid) return;
+  long long c;
+  asm volatile("{ .reg .u64 d; mov.u64 d, %1; mov.u64 %0, %%clock64; }" : "=l"(c) : "l"(dep) : "memory");
+  atomicMax(slot + idx * kTraceEnd, static_cast<unsigned long long>(c - c0));
+}
+// Same, but the stamp is taken only once `v` has arrived (a branch on it stalls the warp).
+__device__ __forceinline__ void trace_sub_after(unsigned long long* slot, int idx, int tid, long long c0, unsigned v) {
+#ifndef DSINF_DIAG
+  return;
+#endif
+  if (slot == nullptr || threadIdx.x != tid) return;
+  long long c = 0;
+  if (v != 0x7f7f7f7fu) c = clock64();
+  atomicMax(slot + idx * kTraceEnd, static_cast<unsigned long long>(c - c0));
+}
+__device__ __forceinline__ void trace_prologue_end(unsigned long long* slot, int tid, unsigned long long t_rel) {
+  if (slot == nullptr || threadIdx.x != tid) return;
+  const unsigned long long t = gtimer();
+  atomicMax(slot + 3 * kTraceEnd, t);
+  atomicMax(slot + 5 * kTraceEnd, t - t_rel);
+}
+__device__ __forceinline__ void trace_phase_max(unsigned long long* slot, int idx, int tid) {
+  if (slot != nullptr && threadIdx.x == tid) atomicMax(slot + idx * kTraceEnd, gtimer());
 }
 
 // ---------------------------------------------------------------- warp MMA (legacy tensor path)

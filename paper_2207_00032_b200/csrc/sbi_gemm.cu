@@ -62,6 +62,17 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 
   __shared__ dev::EpiStats es;
   ptx::trace_begin(p.trace);
+#ifdef DSINF_DIAG
+  unsigned long long* clog = p.cta_log ? p.cta_log + 6 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+#else
+  constexpr unsigned long long* clog = nullptr;
+#endif
+  if (clog && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    clog[0] = smid;
+    clog[1] = ptx::gtimer();
+  }
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.tmap);
     if (kXS) ptx::prefetch_tensormap(&p.xmap);
@@ -138,15 +149,23 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
     ptx::pdl_wait();
+#ifdef DSINF_DIAG
+    const unsigned long long t_rel = ptx::trace_release(p.trace, 32);
+    const long long c_rel = ptx::clk();
+#else
+    constexpr unsigned long long t_rel = 0;
+    constexpr long long c_rel = 0;
+#endif
+    if (clog && threadIdx.x == 32) clog[2] = ptx::gtimer();
     if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
       if (kInt8 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
     } else if (!kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr) {
-      dev::fill_x_ln_f16_pre(p, sx, hd, row_begin, p.rows_per_split, ctid);
+      dev::fill_x_ln_f16_pre(p, sx, hd, row_begin, p.rows_per_split, ctid, c_rel);
     } else if (kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr && dev::ln_i8_fits(p.B, p.K)) {
       dev::fill_x_ln_i8_regs(p, sx, hd, row_begin, p.rows_per_split, ctid, cw, lane);
     } else if (kInt8 && p.pro == PRO_QUANT && p.amax_in != nullptr && (p.x_ld % 4) == 0 && (p.K % 4) == 0 &&
                (reinterpret_cast<uintptr_t>(p.x) & 7) == 0) {
-      dev::fill_x_quant_pre(p, sx, hd, row_begin, p.rows_per_split, ctid);
+      dev::fill_x_quant_pre(p, sx, hd, row_begin, p.rows_per_split, ctid, c_rel);
     } else {
       if (p.pro == PRO_LN)
         dev::ln_row_stats<kInt8>(p, hd, ctid, cw, lane, p.res_out != nullptr && tile == 0 && split == 0);
@@ -158,6 +177,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       dev::fill_x_slice<kInt8>(p, sx, hd, row_begin, p.rows_per_split, ctid);
     }
     dev::consumer_bar();
+#ifdef DSINF_DIAG
+    ptx::trace_prologue_end(p.trace, 32, t_rel);
+#endif
+    if (clog && threadIdx.x == 32) clog[3] = ptx::gtimer();
 
     dev::Consumer<kInt8, kNB8> c;
     c.init(lane);
@@ -168,6 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane);
     else
       c.run(ring, hd, stages, s, phase, n_iters, sx, p.x_row_words, p.B, cw, lane);
+#ifdef DSINF_DIAG
+    ptx::trace_phase_max(p.trace, 4, 32);
+#endif
+    if (clog && threadIdx.x == 32) clog[4] = ptx::gtimer();
     ptx::pdl_trigger();
     dev::consumer_bar();  // every consumer is done reading the ring
     c.store(reinterpret_cast<typename dev::Consumer<kInt8, kNB8>::Acc*>(ring), kPartLd, p.B, cw);
@@ -231,8 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     __syncthreads();
     dev::stats_flush(p, es, (tile + split) % kStatStripes);
   }
-  if (nsplit > 1) ptx::cluster_sync();  // keep our smem alive for remote readers
+  // keep our smem alive until the peers' DSMEM reads are done (their values are consumed before
+  // they arrive, so no release ordering -- and no GPU-scope fence over our epilogue stores -- needed)
+  if (nsplit > 1) ptx::cluster_sync_relaxed();
   ptx::trace_end(p.trace);
+  if (clog && threadIdx.x == 0) clog[5] = ptx::gtimer();
 }
 
 template <bool kInt8, int kNB8, bool kXS>
@@ -453,6 +483,7 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
   p.x_row_words = plan.rows_per_split + 8;
+  p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
   const bool xs = plan.x_stream != 0;

@@ -20,6 +20,7 @@ constexpr int kBoxBytes = kWarpCols * 4 * kRowsPerStage;   // 4 KB: one 128B-swi
 constexpr int kStageBytes = kBoxBytes * kConsumerWarps;    // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kMaxB = 16;                                  // batch rows per launch
+constexpr int kMaxSplit = 16;                              // K splits per column tile (cluster size)
 constexpr int kPartLd = kColTile + 4;                      // split-K partial row stride (floats)
 constexpr int kHeaderBytes = 1024;                         // barriers + per-row scalars
 // x-streaming mode (large batch): each stage also carries the B x 32-word x tile by TMA
@@ -76,6 +77,7 @@ struct Params {
   const __half* ln_g;
   const __half* ln_b;
   float ln_eps;
+  double ln_inv_k;               // 1 / K (set by launch)
   const long long* ln_stats_in;  // PRO_LN: row sums from the producer (else a full-row pass)
   const unsigned* amax_in;       // PRO_QUANT: row max |x| from the producer (else a full-row pass)
   // epilogue
@@ -92,6 +94,7 @@ struct Params {
   long long* ln_stats_out;  // EPI_RESID: accumulate the new residual's row sums (slot, zeroed per step)
   unsigned* amax_out;       // EPI_F16 / EPI_GELU_F16: accumulate row max |out|
   unsigned long long* trace;  // launch timeline slot (ptx::trace_begin / trace_end) or null
+  unsigned long long* cta_log;  // diagnostics: per-CTA [smid, start, release, prologue end, loop end, end] or null
 };
 
 struct Plan {

@@ -129,19 +129,27 @@ __device__ __forceinline__ float ln_apply(float v, float mean, float rstd, const
 // LayerNorm statistics of the full row (single shifted pass) -> hd.mean / hd.rstd; with int8
 // weights also the per-token scale of the fp16-rounded normalised row -> hd.xscale.
 // `write_res` stores the residual (r + delta + bias) once (one CTA per launch / phase).
+// Mean / rstd from the fixed-point row sums (int64, exact and order-independent).  Only
+// multiplications in fp64 (inv_k = 1/K from the host) and one fp32 rsqrt: no fp64 divide / sqrt
+// subroutines on the prologue's critical path.
+__device__ __forceinline__ void ln_mean_rstd(long long s1, long long s2, double inv_k, float eps, float& mean,
+                                             float& rstd) {
+  const double m = static_cast<double>(s1) * (inv_k * (1.0 / static_cast<double>(kSumScale)));
+  const double e2 = static_cast<double>(s2) * (inv_k * (1.0 / static_cast<double>(kSqScale)));
+  const double var = fmax(fma(-m, m, e2), 0.0);
+  mean = static_cast<float>(m);
+  rstd = rsqrtf(static_cast<float>(var) + eps);
+}
 // Mean / rstd of row b from the producer's fixed-point sums (kStatStripes stripes).
-__device__ __forceinline__ void ln_from_sums(const long long* st, int b, int K, float eps, float& mean, float& rstd) {
+__device__ __forceinline__ void ln_from_sums(const long long* st, int b, double inv_k, float eps, float& mean,
+                                             float& rstd) {
   long long s1 = 0, s2 = 0;
 #pragma unroll
   for (int s = 0; s < kStatStripes; ++s) {
     s1 += __ldcg(st + (s * kMaxB + b) * 2);
     s2 += __ldcg(st + (s * kMaxB + b) * 2 + 1);
   }
-  const double m = static_cast<double>(s1) / (static_cast<double>(kSumScale) * K);
-  const double e2 = static_cast<double>(s2) / (static_cast<double>(kSqScale) * K);
-  const double var = fmax(e2 - m * m, 0.0);
-  mean = static_cast<float>(m);
-  rstd = static_cast<float>(1.0 / sqrt(var + static_cast<double>(eps)));
+  ln_mean_rstd(s1, s2, inv_k, eps, mean, rstd);
 }
 
 // Row max |x| from the producer's stripes.
@@ -158,7 +166,7 @@ __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int 
   const int K = p.K;
   const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
   if (p.ln_stats_in != nullptr) {  // statistics from the producing epilogue: no full-row pass
-    if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, K, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+    if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, p.ln_inv_k, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
     if (!kInt8) return;
     consumer_bar();
     const float mean = rm.active ? hd.mean[rm.b] : 0.f, rstd = rm.active ? hd.rstd[rm.b] : 0.f;
@@ -273,7 +281,8 @@ __device__ __forceinline__ void chunked(int ctid, int total, Load load, Store st
 // PRO_LN, fp16, statistics from the producer (p.ln_stats_in): the first residual / gamma / beta
 // loads are issued BEFORE the statistics are read, so the two L2 round trips overlap.  Replaces
 // ln_row_stats + consumer_bar + fill_x_slice for this case (all 128 consumer threads call it).
-__device__ __forceinline__ void fill_x_ln_f16_pre(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows, int ctid) {
+__device__ __forceinline__ void fill_x_ln_f16_pre(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows, int ctid,
+                                                  long long c_rel = 0) {
   constexpr int kPre = 8;
   const int K = p.K;
   const int xrw = p.x_row_words;
@@ -296,7 +305,7 @@ __device__ __forceinline__ void fill_x_ln_f16_pre(const Params& p, uint32_t* sx,
       }
     }
   }
-  if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, K, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+  if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, p.ln_inv_k, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
   consumer_bar();
 #pragma unroll
   for (int j = 0; j < kPre; ++j) {
@@ -346,8 +355,11 @@ __device__ __forceinline__ void fill_x_ln_i8_regs(const Params& p, uint32_t* sx,
       be[u] = *reinterpret_cast<const uint2*>(p.ln_b + 4 * c);
     }
   }
-  float mean = 0.f, rstd = 0.f;
-  if (rm.active) ln_from_sums(p.ln_stats_in, rm.b, K, p.ln_eps, mean, rstd);
+  // one thread per row reads the producer's sums (every thread reading them would put ~all CTAs'
+  // requests on the same few L2 lines)
+  if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, p.ln_inv_k, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+  consumer_bar();
+  const float mean = rm.active ? hd.mean[rm.b] : 0.f, rstd = rm.active ? hd.rstd[rm.b] : 0.f;
   uint2 hv[kLnRegVec];
   float mx = 0.f;
 #pragma unroll
@@ -386,7 +398,7 @@ __device__ __forceinline__ void fill_x_ln_i8_regs(const Params& p, uint32_t* sx,
 // PRO_QUANT with the row max from the producer (p.amax_in): the first x-slice loads are issued
 // before the scale is read, so the two L2 round trips overlap.
 __device__ __forceinline__ void fill_x_quant_pre(const Params& p, uint32_t* sx, Header& hd, int row0, int nrows,
-                                                 int ctid) {
+                                                 int ctid, long long c_rel = 0) {
   constexpr int kPre = 8;
   const int K = p.K;
   const int xrw = p.x_row_words;

@@ -132,7 +132,9 @@ class DecoderModel:
 
     def launch_trace(self, steps: int = 8, stream=None):
         """Per-launch device timeline of `steps` more decode steps: array [steps][launches][3] of
-        (first CTA start ns, last CTA end ns, kind DSINF_LK_*) in the step's enqueue order."""
+        (first CTA start ns, last CTA end ns, kind DSINF_LK_*) in the step's enqueue order, then for SBI-GeMM
+        launches (first release, last prologue end, last main-loop end, longest CTA prologue, last release, 3 sub-phase probes) ns —
+        [steps][launches][11]."""
         capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 1))
         out = []
         try:
@@ -143,7 +145,9 @@ class DecoderModel:
                 buf = np.zeros(3 * n.value, dtype=np.uint64)
                 capi.check(capi.lib.dsinf_model_launch_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                              buf.size, None))
-                out.append(buf.reshape(-1, 3))
+                ph = np.zeros(8 * n.value, dtype=np.uint64)
+                capi.check(capi.lib.dsinf_model_launch_phases(self._h, ph.ctypes.data_as(C.POINTER(C.c_uint64)), ph.size))
+                out.append(np.concatenate([buf.reshape(-1, 3), ph.reshape(-1, 8)], axis=1))
         finally:
             capi.check(capi.lib.dsinf_model_set_launch_trace(self._h, 0))
         return np.stack(out)
