@@ -141,6 +141,26 @@ typedef struct dsinf_gemm_args {
 
 int dsinf_gemm(const dsinf_gemm_args* args, void* stream);
 
+/* ---- large-batch regime (fusion.hpp:145-154: GEMMs isolated when the batch is large; the paper's
+ * prompt / large-batch path): tcgen05 tensor-core GEMM with TMEM accumulators.
+ * Weights are the row-major N x K matrix pack_weights takes as input (gemm.hpp:113), K-major like
+ * x.  F16: fp16 operands, fp32 accumulate.  I8: W8A8, exact int32 accumulate, per-row W scales
+ * and per-row x scales (the decode recipe; quantise both with dsinf_quantize_activations_int8). */
+#define DSINF_EPI_RESID 2 /* out (F32) += x.W^T + bias: residual-stream update */
+typedef struct dsinf_gemm_lb_args {
+  const void* w;          /* [N][K] row-major, F16 or I8 */
+  int32_t w_dtype;        /* DSINF_DT_F16 or DSINF_DT_I8 (x has the same type) */
+  const float* w_scales;  /* I8: [N] */
+  int64_t N, K, M;
+  const void* x;          /* [M][K] row-major */
+  const float* x_scales;  /* I8: [M] */
+  const void* bias;       /* optional F16 [N] */
+  void* out;              /* [M][N] row-major */
+  int32_t out_dtype;      /* F32 or F16 (DSINF_EPI_GELU needs F16, DSINF_EPI_RESID F32) */
+  int32_t epilogue;       /* DSINF_EPI_NONE / DSINF_EPI_GELU / DSINF_EPI_RESID */
+} dsinf_gemm_lb_args;
+int dsinf_gemm_large_batch(const dsinf_gemm_lb_args* args, void* stream);
+
 /* The B200 launch plan the device GEMM uses for a shape (extension of derive_schedule):
  * column tile width, split-K cluster size and packed rows per split. */
 typedef struct dsinf_launch_plan {

@@ -25,6 +25,7 @@ DT_F64 = 4
 
 EPI_NONE = 0
 EPI_GELU = 1
+EPI_RESID = 2
 
 TP_NONE = 0
 TP_NCCL = 1
@@ -87,6 +88,12 @@ class GemmArgs(C.Structure):
                 ("N", C.c_int64), ("K", C.c_int64), ("B", C.c_int64), ("x", C.c_void_p),
                 ("x_dtype", C.c_int32), ("x_scales", C.c_void_p), ("bias", C.c_void_p), ("out", C.c_void_p),
                 ("out_dtype", C.c_int32), ("epilogue", C.c_int32), ("ksplit", C.c_int32)]
+
+
+class LbArgs(C.Structure):
+    _fields_ = [("w", C.c_void_p), ("w_dtype", C.c_int32), ("w_scales", C.c_void_p), ("N", C.c_int64),
+                ("K", C.c_int64), ("M", C.c_int64), ("x", C.c_void_p), ("x_scales", C.c_void_p),
+                ("bias", C.c_void_p), ("out", C.c_void_p), ("out_dtype", C.c_int32), ("epilogue", C.c_int32)]
 
 
 class LaunchPlan(C.Structure):
@@ -154,6 +161,7 @@ SIGNATURES = {
     "dsinf_quantize_weights_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
     "dsinf_quantize_activations_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
     "dsinf_gemm": (C.c_int, [P(GemmArgs), vp]),
+    "dsinf_gemm_large_batch": (C.c_int, [P(LbArgs), vp]),
     "dsinf_gemm_launch_plan": (C.c_int, [i64, i64, i64, i32, P(LaunchPlan)]),
     "dsinf_attention_decode": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, vp, vp]),
     "dsinf_model_create": (C.c_int, [P(ModelConfig), P(RuntimeConfig), vp, P(vp)]),

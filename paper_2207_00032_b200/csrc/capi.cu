@@ -8,6 +8,7 @@
 #include "common.h"
 #include "ops.cuh"
 #include "sbi_gemm.cuh"
+#include "tc_gemm.cuh"
 #include "synth.h"
 
 using namespace dsinf;
@@ -81,6 +82,42 @@ int dsinf_gemm(const dsinf_gemm_args* args, void* stream) {
     require(args != nullptr, "null args");
     gemm::configure();
     run_gemm(*args, as_stream(stream));
+  });
+}
+
+int dsinf_gemm_large_batch(const dsinf_gemm_lb_args* a, void* stream) {
+  return guarded([&] {
+    require(a != nullptr, "null args");
+    require(a->w && a->x && a->out, "null pointer argument");
+    require(a->N >= 1 && a->K >= 1 && a->M >= 1, "gemm shape dims must be positive");
+    require(a->N < (1 << 30) && a->K < (1 << 28) && a->M < (1 << 30), "gemm shape too large");
+    require(a->w_dtype == DSINF_DT_F16 || a->w_dtype == DSINF_DT_I8, "w_dtype must be F16 or I8");
+    const bool i8 = a->w_dtype == DSINF_DT_I8;
+    require(!i8 || (a->w_scales && a->x_scales), "I8 needs w_scales and x_scales");
+    require(a->out_dtype == DSINF_DT_F32 || a->out_dtype == DSINF_DT_F16, "out_dtype must be F32 or F16");
+    tc::Params p{};
+    p.M = static_cast<int>(a->M);
+    p.N = static_cast<int>(a->N);
+    p.K = static_cast<int>(a->K);
+    const int eb = i8 ? 1 : 2;
+    tc::make_maps(p, a->x, p.K * eb, a->w, p.K * eb, eb);
+    p.x_scale = a->x_scales;
+    p.w_scale = a->w_scales;
+    p.bias = static_cast<const __half*>(a->bias);
+    p.out = a->out;
+    p.out_ld = p.N;
+    if (a->epilogue == DSINF_EPI_GELU) {
+      require(a->out_dtype == DSINF_DT_F16, "GeLU epilogue writes F16");
+      p.epi = tc::EPI_GELU_F16;
+    } else if (a->epilogue == DSINF_EPI_RESID) {
+      require(a->out_dtype == DSINF_DT_F32, "residual epilogue accumulates into F32");
+      p.epi = tc::EPI_RESID;
+    } else {
+      require(a->epilogue == DSINF_EPI_NONE, "unknown epilogue");
+      p.epi = a->out_dtype == DSINF_DT_F32 ? tc::EPI_F32 : tc::EPI_F16;
+    }
+    tc::configure();
+    tc::launch(p, i8, as_stream(stream));
   });
 }
 

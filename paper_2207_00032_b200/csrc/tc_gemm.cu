@@ -1,0 +1,328 @@
+// tcgen05 / TMEM large-batch GEMM for sm_100a (see tc_gemm.cuh).
+//
+// One CTA = one 128 x 256 output tile, warp-specialised:
+//   warp 0      one elected thread streams x and W K-blocks (128 B wide) with 2-D TMA into a
+//               4-stage mbarrier ring (128B swizzle, the canonical K-major UMMA layout);
+//   warp 1      allocates 256 TMEM columns (the fp32 / int32 accumulator: lane = row, column = n);
+//               one elected thread issues tcgen05.mma (M=128, N=256, K=16 fp16 / 32 int8) four
+//               times per stage and frees the stage with tcgen05.commit;
+//   warps 2..5  epilogue: wait for the final commit, tcgen05.ld 32 columns at a time (each warp
+//               owns the 32 TMEM lanes of its quarter), dequantise / bias / GeLU / RoPE / residual,
+//               store straight to global.
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+#include <cudaTypedefs.h>
+
+#include "common.h"
+#include "ptx.cuh"
+#include "sbi_gemm_dev.cuh"
+#include "tc_gemm.cuh"
+
+namespace dsinf {
+namespace tc {
+
+namespace {
+
+// ---------------------------------------------------------------- tcgen05 wrappers
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(slot)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, K-major operand in the 128B-swizzle canonical layout:
+// rows of 128 B, 8-row core groups 1024 B apart (SBO), descriptor version 1, layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3fff);       // start address
+  d |= static_cast<uint64_t>(1) << 16;                      // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;              // SBO
+  d |= static_cast<uint64_t>(1) << 46;                      // version
+  d |= static_cast<uint64_t>(2) << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: K-major A and B, M = 128, N = 256.
+//   kind::f16: D f32 (1), A/B f16 (0);  kind::i8: D s32 (2), A/B s8 (1).
+template <bool kInt8>
+__host__ __device__ constexpr uint32_t instr_desc() {
+  return (kInt8 ? 2u : 1u) << 4 | (kInt8 ? 1u : 0u) << 7 | (kInt8 ? 1u : 0u) << 10 |
+         static_cast<uint32_t>(kBN >> 3) << 17 | static_cast<uint32_t>(kBM >> 4) << 24;
+}
+
+template <bool kInt8>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kInt8)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   ptx::smem_u32(bar))
+               : "memory");
+}
+// 32 lanes x 32 columns of 32-bit: thread t of the warp gets lane (base + t), columns [col, col + 32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- epilogue of one row's 32 columns
+template <bool kInt8>
+__device__ __forceinline__ void epilogue32(const Params& p, int row, int n0, const uint32_t (&v)[32]) {
+  float y[32];
+  if constexpr (kInt8) {
+    const float xs = p.x_scale[row];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = n0 + j;
+      const float ws = n < p.N ? __ldg(p.w_scale + n) : 0.f;
+      y[j] = __fmul_rn(__fmul_rn(static_cast<float>(static_cast<int>(v[j])), xs), ws);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) y[j] = __uint_as_float(v[j]);
+  }
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < p.N) y[j] = __fadd_rn(y[j], __half2float(p.bias[n0 + j]));
+  }
+  const bool full = n0 + 32 <= p.N;
+  switch (p.epi) {
+    case EPI_F32: {
+      float* o = static_cast<float*>(p.out) + static_cast<size_t>(row) * p.out_ld + n0;
+      if (full && (p.out_ld % 4) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < p.N) o[j] = y[j];
+      }
+      break;
+    }
+    case EPI_RESID: {
+      float* o = static_cast<float*>(p.out) + static_cast<size_t>(row) * p.out_ld + n0;
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < p.N) o[j] = __fadd_rn(o[j], y[j]);
+      break;
+    }
+    case EPI_F16:
+    case EPI_GELU_F16: {
+      if (p.epi == EPI_GELU_F16) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = gemm::dev::gelu_tanh(y[j]);
+      }
+      __half* o = static_cast<__half*>(p.out) + static_cast<size_t>(row) * p.out_ld + n0;
+      if (full && (p.out_ld % 8) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 u;
+          u.x = gemm::dev::pack_h2(y[j], y[j + 1]);
+          u.y = gemm::dev::pack_h2(y[j + 2], y[j + 3]);
+          u.z = gemm::dev::pack_h2(y[j + 4], y[j + 5]);
+          u.w = gemm::dev::pack_h2(y[j + 6], y[j + 7]);
+          *reinterpret_cast<uint4*>(o + j) = u;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < p.N) o[j] = __float2half_rn(y[j]);
+      }
+      break;
+    }
+    case EPI_QKV: {
+      const int hd = p.heads * p.head_dim;
+      const int b = row / p.seq_len;
+      const int pos = p.pos0 + (row - b * p.seq_len);
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const int n = n0 + j;
+        if (n >= p.N) break;
+        const int sec = n / hd;
+        const int rem = n - sec * hd;
+        const int head = rem / p.head_dim;
+        const int i = rem - head * p.head_dim;
+        float y0 = y[j], y1 = y[j + 1];
+        if (sec < 2) {  // GPT-J interleaved rotary embedding (same arithmetic as the decode epilogue)
+          const float2 cs = p.rope[static_cast<size_t>(pos) * (p.head_dim / 2) + i / 2];
+          const float r0 = __fsub_rn(__fmul_rn(y0, cs.x), __fmul_rn(y1, cs.y));
+          const float r1 = __fadd_rn(__fmul_rn(y0, cs.y), __fmul_rn(y1, cs.x));
+          y0 = r0;
+          y1 = r1;
+        }
+        const __half2 h = __floats2half2_rn(y0, y1);
+        if (sec == 0) {
+          *reinterpret_cast<__half2*>(p.q_out + static_cast<size_t>(row) * hd + rem) = h;
+        } else {
+          __half* cache = sec == 1 ? p.k_cache : p.v_cache;
+          const size_t off = ((static_cast<size_t>(b) * p.heads + head) * p.max_seq + pos) * p.head_dim + i;
+          *reinterpret_cast<__half2*>(cache + off) = h;
+        }
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <bool kInt8>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_ready = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // m fastest: the row tiles that share a weight tile run together (W streams from HBM once,
+  // x stays in L2)
+  const int m0 = blockIdx.x * kBM;
+  const int n0 = blockIdx.y * kBN;
+  const int nk = p.k_blocks;
+
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tensormap(&p.amap);
+    ptx::prefetch_tensormap(&p.bmap);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(acc_ready, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ================= TMA producer
+      ptx::pdl_wait();
+      const uint64_t pol_a = ptx::policy_evict_last();   // x tiles are re-read by every column tile
+      const uint64_t pol_b = ptx::policy_evict_normal();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) ptx::mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+        uint8_t* sa = smem + s * kStageBytes;
+        ptx::tma_load_2d(sa, &p.amap, kb * kBK, m0, &full[s], pol_a);
+        ptx::tma_load_2d(sa + kABytes, &p.bmap, kb * kBK, n0, &full[s], pol_b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ================= MMA issuer
+      constexpr uint32_t idesc = instr_desc<kInt8>();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        ptx::mbar_wait(&full[s], (kb / kStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + s * kStageBytes);
+        const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 32; ++k)  // 32 bytes of K per MMA (16 fp16 / 32 int8)
+          mma<kInt8>(tmem, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
+                     (kb | k) != 0 ? 1u : 0u);
+        mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+      }
+      mma_commit(acc_ready);
+    }
+  } else {
+    // ================= epilogue: warp w owns TMEM lanes [32 (w % 4), +32)
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    ptx::mbar_wait(acc_ready, 0);
+    tc_fence_after();
+    ptx::pdl_trigger();
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+      if (row < p.M && n0 + c * 32 < p.N) epilogue32<kInt8>(p, row, n0 + c * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kBN);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
+void byte_map(CUtensorMap* map, const void* base, int rows, int row_bytes, int ld_bytes, int box_rows) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld_bytes % 16) != 0)
+    throw ConfigError("tc_gemm: operands need 16-byte aligned bases and row strides");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_bytes), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_bytes)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (tc_gemm) failed: " + std::to_string(static_cast<int>(r)));
+}
+
+}  // namespace
+
+void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld_bytes, int elem_bytes) {
+  if (p.M < 1 || p.N < 1 || p.K < 1) throw ConfigError("tc_gemm: gemm shape dims must be positive");
+  const int kbytes = p.K * elem_bytes;
+  byte_map(&p.amap, x, p.M, kbytes, x_ld_bytes, kBM);
+  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, kBN);
+  p.k_blocks = (kbytes + kBK - 1) / kBK;
+}
+
+void configure() {
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+}
+
+void launch(const Params& p, bool int8, cudaStream_t s) {
+  const dim3 grid((p.M + kBM - 1) / kBM, (p.N + kBN - 1) / kBN);
+  if (int8)
+    tc_gemm_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(p);
+  else
+    tc_gemm_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(p);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace tc
+}  // namespace dsinf

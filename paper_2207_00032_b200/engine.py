@@ -193,6 +193,33 @@ def gemm(w_packed, x, N: int, K: int, *, w_scales=None, x_scales=None, bias=None
     return out
 
 
+def gemm_large_batch(w, x, *, w_scales=None, x_scales=None, bias=None, out=None, out_dtype=None, gelu=False,
+                     resid=False, stream=None):
+    """tcgen05 tensor-core GEMM of the large-batch regime: out[M][N] = x[M][K] . W[N][K]^T.
+
+    w: row-major [N][K] fp16, or int8 with w_scales [N]; x: [M][K] of the same type (int8 with
+    x_scales [M]).  gelu -> fp16 out; resid -> out (fp32) += result."""
+    N, K = w.shape
+    M = x.shape[0]
+    i8 = w.dtype == torch.int8
+    if out is None:
+        od = out_dtype or (torch.float16 if gelu else torch.float32)
+        out = torch.empty((M, N), dtype=od, device=x.device)
+    a = capi.LbArgs()
+    a.w = _dptr(w)
+    a.w_dtype = capi.DT_I8 if i8 else capi.DT_F16
+    a.w_scales = _dptr(w_scales)
+    a.N, a.K, a.M = N, K, M
+    a.x = _dptr(x)
+    a.x_scales = _dptr(x_scales)
+    a.bias = _dptr(bias)
+    a.out = _dptr(out)
+    a.out_dtype = capi.DT_F32 if out.dtype == torch.float32 else capi.DT_F16
+    a.epilogue = capi.EPI_GELU if gelu else (capi.EPI_RESID if resid else capi.EPI_NONE)
+    capi.check(capi.lib.dsinf_gemm_large_batch(C.byref(a), _stream_ptr(stream)))
+    return out
+
+
 def pack_weights_device(w, pack_M: int = 2, stream=None):
     """Row-major [N][K] (fp16/fp32) -> packed fp16 [ceil(K/M)*M*N] (gemm.hpp:113-130 layout)."""
     N, K = w.shape
