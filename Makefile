@@ -20,7 +20,7 @@ NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall 
              --expt-relaxed-constexpr -Iinclude -I$(CSRC) -Xptxas -warn-spills $(DIAGFLAGS)
 CXXFLAGS := -O2 -std=c++17 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC) -I/usr/local/cuda/include
 
-CU_SRCS := $(CSRC)/sbi_gemm.cu $(CSRC)/tc_gemm.cu $(CSRC)/step_kernel.cu $(CSRC)/attention.cu $(CSRC)/ops.cu $(CSRC)/model.cu $(CSRC)/capi.cu
+CU_SRCS := $(CSRC)/sbi_gemm.cu $(CSRC)/tc_gemm.cu $(CSRC)/step_kernel.cu $(CSRC)/attention.cu $(CSRC)/ops.cu $(CSRC)/prefill.cu $(CSRC)/model.cu $(CSRC)/capi.cu
 CPP_SRCS := $(CSRC)/host_api.cpp $(CSRC)/nccl_dl.cpp
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS))

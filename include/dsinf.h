@@ -225,6 +225,11 @@ int dsinf_model_set_prompt_device(dsinf_model* m, const int32_t* prompt_dev, int
 /* Enqueue one decode step: embed the token at the current position (prompt token while
  * pos < prompt_len, else the previous greedy token), run every layer, the LM head and the
  * greedy argmax, then advance the position.  Replays a CUDA graph when enabled. */
+/* Prompt prefill in the large-batch regime (fusion.hpp:145-154): all B x P
+ * prompt tokens through every layer at once on the tcgen05 tensor cores, leaving the model in the
+ * state dsinf_decode_steps(m, P) would (KV cache rows 0..P-1, history, next token, position P).
+ * Needs a prompt set at position 0, tp_size 1.  First call generates row-major weight copies. */
+int dsinf_model_prefill(dsinf_model* m, void* stream);
 int dsinf_decode_step(dsinf_model* m, void* stream);
 /* Enqueue `steps` decode steps back to back. */
 int dsinf_decode_steps(dsinf_model* m, int64_t steps, void* stream);

@@ -169,6 +169,7 @@ SIGNATURES = {
     "dsinf_model_set_prompt": (C.c_int, [vp, P(i32), i64, vp]),
     "dsinf_model_set_prompt_device": (C.c_int, [vp, vp, i64, vp]),
     "dsinf_decode_step": (C.c_int, [vp, vp]),
+    "dsinf_model_prefill": (C.c_int, [vp, vp]),
     "dsinf_decode_steps": (C.c_int, [vp, i64, vp]),
     "dsinf_decode_step_host": (C.c_int, [vp, P(i32), P(i32), vp]),
     "dsinf_model_outputs": (C.c_int, [vp, P(vp), P(i64), P(vp), P(vp), P(vp)]),

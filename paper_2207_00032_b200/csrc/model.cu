@@ -29,6 +29,7 @@
 #include "ptx.cuh"
 #include "sbi_gemm.cuh"
 #include "step_kernel.cuh"
+#include "tc_gemm.cuh"
 #include "synth.h"
 
 namespace dsinf {
@@ -55,6 +56,21 @@ struct LayerW {
   uint32_t* wdown = nullptr;
   float* sdown = nullptr;
   __half* bdown = nullptr;
+  // row-major [N][K] copies for the tensor-core prefill (fp16, or int8 with the scales above);
+  // generated on the first dsinf_model_prefill
+  void *rqkv = nullptr, *ro = nullptr, *rup = nullptr, *rdown = nullptr;
+};
+
+// Prefill activations for M = B x P rows (grown on demand).
+struct PrefillBufs {
+  int64_t cap = 0;
+  float* res = nullptr;    // [M][h]
+  __half* xn = nullptr;    // [M][h] LayerNorm output (fp16 path)
+  int8_t* xq = nullptr;    // [M][max(h, F/t)] int8 GEMM input
+  float* xs = nullptr;     // [M] its per-row scales
+  __half* q = nullptr;     // [M][Hl*d]
+  __half* a = nullptr;     // [M][Hl*d] attention output
+  __half* u = nullptr;     // [M][F/t] GeLU output
 };
 
 struct Shard {
@@ -78,6 +94,8 @@ struct Shard {
   long long* lnstats = nullptr;  // [2L+1][kLnSlotWords]: LayerNorm row sums from the producing epilogue
   unsigned* amax = nullptr;      // [2L][kAmaxSlotWords]: int8 activation row max from the producer
   gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
+  PrefillBufs pf;
+  bool rm_ready = false;
 };
 
 }  // namespace
@@ -297,6 +315,49 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln);
   sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od);
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm);
+}
+
+// Row-major copies of the layer GEMM weights for the tensor-core prefill (same synthetic values;
+// int8 quantised with the packed layout's row scales).
+void build_rowmajor(Model& m, Shard& sh, cudaStream_t s) {
+  const int r = sh.rank;
+  const int64_t h = m.h;
+  for (int l = 0; l < m.L; ++l) {
+    LayerW& w = sh.layers[l];
+    auto make = [&](int tensor, const float* scales) -> void* {
+      const ops::ShardMap map = tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, l, tensor);
+      const int64_t n = map.N_local * map.K_local;
+      if (m.int8) {
+        int8_t* out = m.alloc_n<int8_t>(n);
+        ops::init_rowmajor_map_i8(map, scales, out, s);
+        return out;
+      }
+      __half* out = m.alloc_n<__half>(n);
+      ops::init_rowmajor_map_f16(map, out, s);
+      return out;
+    };
+    w.rqkv = make(DSINF_T_QKV, w.sqkv);
+    w.ro = make(DSINF_T_O, w.so);
+    w.rup = make(DSINF_T_UP, w.sup);
+    w.rdown = make(DSINF_T_DOWN, w.sdown);
+  }
+  sh.rm_ready = true;
+}
+
+void ensure_prefill_bufs(Model& m, Shard& sh, int64_t M) {
+  PrefillBufs& pf = sh.pf;
+  if (pf.cap >= M) return;
+  const int64_t h = m.h, Hd = m.Hl * m.d, Fl = m.Fl;
+  pf.res = m.alloc_n<float>(M * h);
+  pf.xn = m.alloc_n<__half>(M * h);
+  if (m.int8) {
+    pf.xq = m.alloc_n<int8_t>(M * std::max(h, Fl));
+    pf.xs = m.alloc_n<float>(M);
+  }
+  pf.q = m.alloc_n<__half>(M * Hd);
+  pf.a = m.alloc_n<__half>(M * Hd);
+  pf.u = m.alloc_n<__half>(M * Fl);
+  pf.cap = M;
 }
 
 gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w) {
@@ -685,6 +746,143 @@ struct Enqueuer {
     }
   }
 
+  // Prompt prefill (large-batch regime, TP = 1): every layer over all B x P prompt tokens with
+  // the tcgen05 GEMMs, then the decode path's LM head / argmax / select on the last token.
+  void prefill(int P) {
+    Shard& sh = m.shards[0];
+    PrefillBufs& pf = sh.pf;
+    const int M = m.B * P;
+    const int h = static_cast<int>(m.h), Hd = static_cast<int>(m.Hl * m.d), Fl = static_cast<int>(m.Fl);
+    const bool i8 = m.int8;
+    const int eb = i8 ? 1 : 2;
+    ops::PrefillEmbedParams pe{};
+    pe.wte = sh.wte;
+    pe.prompt = m.prompt;
+    pe.prompt_ld = m.prompt_cap;
+    pe.P = P;
+    pe.hist = m.hist;
+    pe.max_ctx = m.max_ctx;
+    pe.res = pf.res;
+    pe.B = m.B;
+    pe.h = h;
+    pe.V = static_cast<int>(m.V);
+    ops::prefill_embed(pe, s);
+    ++launches;
+    auto ln = [&](const __half* g, const __half* b) {  // LayerNorm rows -> GEMM-ready x
+      ops::PrepParams pp{};
+      pp.mode = i8 ? ops::PREP_LN_I8 : ops::PREP_LN_F16;
+      pp.res = pf.res;
+      pp.ln_g = g;
+      pp.ln_b = b;
+      pp.eps = m.rt.ln_eps;
+      pp.out = i8 ? static_cast<void*>(pf.xq) : static_cast<void*>(pf.xn);
+      pp.out_scale = pf.xs;
+      pp.B = M;
+      pp.K = h;
+      ops::row_prep(pp, s, false);
+      ++launches;
+    };
+    auto quant = [&](const __half* x, int K) {  // int8: per-row quantisation of an fp16 activation
+      ops::PrepParams pp{};
+      pp.mode = ops::PREP_QUANT_I8;
+      pp.x = x;
+      pp.x_ld = K;
+      pp.out = pf.xq;
+      pp.out_scale = pf.xs;
+      pp.B = M;
+      pp.K = K;
+      ops::row_prep(pp, s, false);
+      ++launches;
+    };
+    auto gemm = [&](tc::Params& p, const void* x, const void* w, const float* ws, int N, int K) {
+      p.M = M;
+      p.N = N;
+      p.K = K;
+      tc::make_maps(p, x, K * eb, w, K * eb, eb);
+      p.x_scale = pf.xs;
+      p.w_scale = ws;
+      tc::launch(p, i8, s);
+      ++launches;
+    };
+    const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+    for (int l = 0; l < m.L; ++l) {
+      const LayerW& w = sh.layers[l];
+      ln(w.ln1g, w.ln1b);
+      tc::Params q{};
+      q.epi = tc::EPI_QKV;
+      q.bias = w.bqkv;
+      q.q_out = pf.q;
+      q.k_cache = sh.kc + l * layer_kv;
+      q.v_cache = sh.vc + l * layer_kv;
+      q.rope = m.rope;
+      q.seq_len = P;
+      q.pos0 = 0;
+      q.heads = static_cast<int>(m.Hl);
+      q.head_dim = static_cast<int>(m.d);
+      q.max_seq = m.max_ctx;
+      gemm(q, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rqkv, w.sqkv, 3 * Hd, h);
+      ops::PrefillAttnParams a{};
+      a.q = pf.q;
+      a.kc = q.k_cache;
+      a.vc = q.v_cache;
+      a.out = pf.a;
+      a.B = m.B;
+      a.P = P;
+      a.H = static_cast<int>(m.Hl);
+      a.d = static_cast<int>(m.d);
+      a.max_seq = m.max_ctx;
+      a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+      ops::prefill_attention(a, s);
+      ++launches;
+      if (i8) quant(pf.a, Hd);
+      tc::Params o{};
+      o.epi = tc::EPI_RESID;
+      o.bias = w.bo;
+      o.out = pf.res;
+      o.out_ld = h;
+      gemm(o, i8 ? static_cast<const void*>(pf.xq) : pf.a, w.ro, w.so, h, Hd);
+      ln(w.ln2g, w.ln2b);
+      tc::Params u{};
+      u.epi = tc::EPI_GELU_F16;
+      u.bias = w.bup;
+      u.out = pf.u;
+      u.out_ld = Fl;
+      gemm(u, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rup, w.sup, Fl, h);
+      if (i8) quant(pf.u, Fl);
+      tc::Params dn{};
+      dn.epi = tc::EPI_RESID;
+      dn.bias = w.bdown;
+      dn.out = pf.res;
+      dn.out_ld = h;
+      gemm(dn, i8 ? static_cast<const void*>(pf.xq) : pf.u, w.rdown, w.sdown, h, Fl);
+    }
+    // last prompt token of every sequence -> the decode state, then LM head / argmax / select
+    long long* lslot = lnslot(sh, 2 * static_cast<int>(m.L));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(lslot, 0, gemm::kLnSlotWords * sizeof(long long), s));
+    ops::PrefillGatherParams g{};
+    g.res_rows = pf.res;
+    g.P = P;
+    g.res = sh.res[0];
+    g.ln_stats = lslot;
+    g.pos = m.pos;
+    g.B = m.B;
+    g.h = h;
+    ops::prefill_gather(g, s);
+    ++launches;
+    lm_head(sh);
+    ops::SelectParams sp{};
+    sp.vals = m.am_val;
+    sp.idxs = m.am_idx;
+    sp.shards = 1;
+    sp.B = m.B;
+    sp.next_tok = m.next_tok;
+    sp.pos = m.pos;
+    sp.hist = m.hist;
+    sp.max_ctx = m.max_ctx;
+    ops::select_token(sp, s, false);
+    ++launches;
+  }
+
   void step() {
     if (m.step_prog.ready()) {  // TP = 1: the whole step is one persistent kernel
       m.step_prog.launch(s);
@@ -928,6 +1126,26 @@ int dsinf_model_set_prompt(dsinf_model* m, const int32_t* prompt_host, int64_t p
 
 int dsinf_model_set_prompt_device(dsinf_model* m, const int32_t* prompt_dev, int64_t prompt_len, void* stream) {
   return guarded([&] { set_prompt_common(m, prompt_dev, prompt_len, false, static_cast<cudaStream_t>(stream)); });
+}
+
+int dsinf_model_prefill(dsinf_model* m, void* stream) {
+  return guarded([&] {
+    require(m != nullptr, "null model");
+    require(m->prompt_len >= 1, "prefill needs a prompt (dsinf_model_set_prompt)");
+    require(m->host_pos == 0, "prefill must start at position 0 (call dsinf_model_set_prompt first)");
+    require(m->t == 1 && m->fuse_ln, "prefill runs at tp_size 1 with fused LayerNorm statistics");
+    require(m->d % 32 == 0 && m->d <= 256, "prefill attention needs head_dim % 32 == 0 and <= 256");
+    require(m->h % 16 == 0 && (4 * m->h) % 16 == 0, "prefill needs hidden_dim % 16 == 0 (16-byte TMA rows)");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Shard& sh = m->shards[0];
+    tc::configure();
+    ops::configure_prefill();
+    if (!sh.rm_ready) build_rowmajor(*m, sh, s);
+    ensure_prefill_bufs(*m, sh, static_cast<int64_t>(m->B) * m->prompt_len);
+    Enqueuer e{*m, s, m->rt.use_pdl != 0};
+    e.prefill(m->prompt_len);
+    m->host_pos = m->prompt_len;
+  });
 }
 
 int dsinf_decode_step(dsinf_model* m, void* stream) { return dsinf_decode_steps(m, 1, stream); }

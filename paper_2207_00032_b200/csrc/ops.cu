@@ -84,6 +84,27 @@ __global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t*
   }
 }
 
+// Row-major [N_local][K_local] copies of the same synthetic tensor for the tensor-core
+// (large-batch) path: fp16 values, or int8 quantised with the packed layout's row scales (so both
+// layouts hold identical int8 weights).
+__global__ void init_rowmajor_map_f16_kernel(ShardMap m, __half* out) {
+  const int64_t total = m.N_local * m.K_local;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / m.K_local, k = i - n * m.K_local;
+    out[i] = __float2half_rn(synth_value(m, global_row(m, n), m.col_off + k));
+  }
+}
+
+__global__ void init_rowmajor_map_i8_kernel(ShardMap m, const float* scales, int8_t* out) {
+  const int64_t total = m.N_local * m.K_local;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t n = i / m.K_local, k = i - n * m.K_local;
+    out[i] = static_cast<int8_t>(q8(synth_value(m, global_row(m, n), m.col_off + k), scales[n]));
+  }
+}
+
 __global__ void init_vector_kernel(ShardMap m, float offset, __half* out) {
   for (int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; n < m.N_local;
        n += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -301,7 +322,22 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
   __shared__ float red[kPrepThreads / 32];
   if (p.mode == PREP_QUANT_I8) {
     float mx = 0.f;
-    for (int s = 0; s < gemm::kStatStripes; ++s) mx = fmaxf(mx, __uint_as_float(__ldcg(p.amax + s * 32 + b)));
+    if (p.amax != nullptr) {
+      for (int s = 0; s < gemm::kStatStripes; ++s) mx = fmaxf(mx, __uint_as_float(__ldcg(p.amax + s * 32 + b)));
+    } else {  // row max computed here (large-batch path: rows beyond the producer's stripes)
+      const uint2* row2 = reinterpret_cast<const uint2*>(p.x + static_cast<size_t>(b) * p.x_ld);
+      for (int c = threadIdx.x; c < K4; c += kPrepThreads) {
+        const uint2 u = __ldcg(row2 + c);
+        const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x), h23 = *reinterpret_cast<const __half2*>(&u.y);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(__low2float(h01)), fabsf(__high2float(h01))),
+                             fmaxf(fabsf(__low2float(h23)), fabsf(__high2float(h23)))));
+      }
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      mx = red[0];
+      for (int w = 1; w < kPrepThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+    }
     const float scale = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
     if (threadIdx.x == 0) p.out_scale[b] = scale;
     const __half* row = p.x + static_cast<size_t>(b) * p.x_ld;
@@ -460,6 +496,16 @@ void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStre
   DSINF_CUDA_CHECK(cudaGetLastError());
   const int64_t total = (m.K_local + 3) / 4 * m.N_local;
   init_packed_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, scales, packed);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_rowmajor_map_f16(const ShardMap& m, __half* out, cudaStream_t s) {
+  init_rowmajor_map_f16_kernel<<<blocks_for(m.N_local * m.K_local, 256), 256, 0, s>>>(m, out);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_rowmajor_map_i8(const ShardMap& m, const float* scales, int8_t* out, cudaStream_t s) {
+  init_rowmajor_map_i8_kernel<<<blocks_for(m.N_local * m.K_local, 256), 256, 0, s>>>(m, scales, out);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -24,6 +24,10 @@ struct ShardMap {
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s);
 // Same tensor quantised per global output row to int8 (pack_M = 4) + fp32 row scales.
 void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s);
+// Row-major [N_local][K_local] copy of the same tensor for the tensor-core path: fp16, or int8
+// quantised with the given (packed-layout) row scales.
+void init_rowmajor_map_f16(const ShardMap& m, __half* out, cudaStream_t s);
+void init_rowmajor_map_i8(const ShardMap& m, const float* scales, int8_t* out, cudaStream_t s);
 // 1-D tensor (bias / LN) of length n_local: value = offset + unit(flat = row(n)) * amp.
 void init_vector_f16(const ShardMap& m, float offset, __half* out, cudaStream_t s);
 // Row-major fp16 [rows][cols] (replicated embedding table).
@@ -58,7 +62,8 @@ void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl);
 enum PrepMode : int {
   PREP_LN_F16 = 0,    // out fp16 = LayerNorm(res) with the producer's row sums
   PREP_LN_I8 = 1,     // out int8 = quantise(fp16 LayerNorm(res)), scale = row max / 127
-  PREP_QUANT_I8 = 2,  // out int8 = quantise(x fp16), scale from the producer's row max
+  PREP_QUANT_I8 = 2,  // out int8 = quantise(x fp16), scale from the producer's row max (amax), or
+                      // from the row itself when amax is null
 };
 struct PrepParams {
   int mode;
@@ -118,6 +123,42 @@ struct SelectParams {
   int max_ctx;
 };
 void select_token(const SelectParams& p, cudaStream_t s, bool pdl);
+
+// ---- prompt prefill (large-batch regime): M = B * P rows, row m = token (m % P) of sequence m / P
+struct PrefillEmbedParams {
+  const __half* wte;       // [V][h]
+  const int32_t* prompt;   // [B][prompt_ld]
+  int prompt_ld, P;
+  int32_t* hist;           // [B][max_ctx]
+  int max_ctx;
+  float* res;              // [M][h]
+  int B, h, V;
+};
+void prefill_embed(const PrefillEmbedParams& p, cudaStream_t s);
+
+// Causal attention of every prompt token over the prompt's KV cache (positions 0..t).
+struct PrefillAttnParams {
+  const __half* q;   // [M][H*d] (RoPE applied)
+  const __half* kc;  // [B][H][max_seq][d] (this layer)
+  const __half* vc;
+  __half* out;       // [M][H*d]
+  int B, P, H, d, max_seq;
+  float scale;
+};
+void configure_prefill();
+void prefill_attention(const PrefillAttnParams& p, cudaStream_t s);
+
+// Hands the last prompt token's residual row of every sequence to the decode state: res [B][h],
+// the final LayerNorm's fixed-point row sums (stripe 0 of `ln_stats`), *pos = P - 1.
+struct PrefillGatherParams {
+  const float* res_rows;  // [M][h]
+  int P;
+  float* res;             // [B][h]
+  long long* ln_stats;    // kLnSlotWords slot (zeroed by the caller)
+  int* pos;
+  int B, h;
+};
+void prefill_gather(const PrefillGatherParams& p, cudaStream_t s);
 
 // Sum of `n` shard buffers (in shard order), written back to every shard buffer.
 struct LocalReduceParams {

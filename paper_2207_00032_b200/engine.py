@@ -103,6 +103,10 @@ class DecoderModel:
     def step(self, n: int = 1, stream=None) -> None:
         capi.check(capi.lib.dsinf_decode_steps(self._h, n, _stream_ptr(stream)))
 
+    def prefill(self, stream=None) -> None:
+        """The whole prompt at once on the tensor cores (same resulting state as step(prompt_len))."""
+        capi.check(capi.lib.dsinf_model_prefill(self._h, _stream_ptr(stream)))
+
     def outputs(self):
         logits, ld, nxt, hist, pos = C.c_void_p(), C.c_int64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         capi.check(capi.lib.dsinf_model_outputs(self._h, C.byref(logits), C.byref(ld), C.byref(nxt), C.byref(hist),

@@ -163,3 +163,92 @@ def test_tp_local_x_stream(monkeypatch, dtype_bytes):
     """TP without producer statistics: row_prep sums the residual itself and writes it back."""
     monkeypatch.setenv("DSINF_XS", "1")
     run_parity(512, 2, 8, 1000, tp=2, batch=4, dtype_bytes=dtype_bytes, step_kernel=False)
+
+
+def run_prefill_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, prompt_len=40, gen=3, max_ctx=64):
+    """Prefill (tcgen05 large-batch path) vs the oracle stepping through the prompt token by token;
+    then `gen` decode steps from the prefilled KV cache.  Same tolerances as run_parity."""
+    tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
+    rng = np.random.default_rng(hidden * 3 + layers + batch + prompt_len)
+    prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
+    gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED)
+    ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED)
+    gpu.set_prompt(prompt)
+    gpu.prefill()
+    torch.cuda.synchronize()
+    for pos in range(prompt_len):
+        ol, onext = ora.step(prompt[:, pos], pos)
+    worst = 0.0
+    for g in range(gen + 1):
+        pos = prompt_len - 1 + g
+        if g > 0:
+            gpu.step(1)
+            torch.cuda.synchronize()
+        lg = gpu.full_logits()
+        nxt, hist = gpu.read_tokens()
+        if g > 0:
+            ol, onext = ora.step(hist[:, pos], pos)
+        else:
+            assert np.array_equal(hist[:, :prompt_len], prompt)
+        tol = tol_rel * float(ol.std()) + tol_abs
+        err = float(np.abs(lg - ol).max())
+        worst = max(worst, err / tol)
+        assert err <= tol, f"pos {pos}: max|dlogit| {err:.4g} > tol {tol:.4g}"
+        srt = np.sort(ol, axis=1)
+        for b in range(batch):
+            if srt[b, -1] - srt[b, -2] > tol:
+                assert nxt[b] == onext[b], f"pos {pos} b {b}: token {nxt[b]} != oracle {onext[b]}"
+    assert int(gpu.read_tokens()[1][0, prompt_len]) == int(hist[0, prompt_len])
+    gpu.close()
+    ora.close()
+    return worst
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+@pytest.mark.parametrize("batch,prompt_len", [(1, 40), (3, 50), (2, 130)])
+def test_prefill_matches_oracle_small(dtype_bytes, batch, prompt_len):
+    run_prefill_parity(256, 2, 4, 1000, batch=batch, dtype_bytes=dtype_bytes, prompt_len=prompt_len,
+                       max_ctx=prompt_len + 8)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+def test_prefill_matches_oracle_head_dim_128(dtype_bytes):
+    run_prefill_parity(1024, 2, 8, 2000, batch=2, dtype_bytes=dtype_bytes, prompt_len=96, max_ctx=104)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+def test_prefill_equals_token_by_token_decode(dtype_bytes):
+    """The large-batch prefill and P decode steps over the prompt leave the same state: same
+    history and greedy continuation, logits within the fp16 / int8 tolerance."""
+    hidden, layers, heads, vocab, B, P = 512, 3, 8, 3000, 4, 64
+    rng = np.random.default_rng(77)
+    prompt = rng.integers(0, vocab, (B, P)).astype(np.int32)
+    a = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=B, max_ctx=80, seed=SEED)
+    b = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=B, max_ctx=80, seed=SEED)
+    a.set_prompt(prompt)
+    b.set_prompt(prompt)
+    a.prefill()
+    b.step(P)
+    torch.cuda.synchronize()
+    la, lb = a.full_logits(), b.full_logits()
+    tol = (0.03 if dtype_bytes == 2 else 0.06) * float(lb.std()) + (0.01 if dtype_bytes == 2 else 0.02)
+    assert float(np.abs(la - lb).max()) <= tol
+    ha, hb = a.read_tokens()[1], b.read_tokens()[1]
+    assert np.array_equal(ha[:, :P], hb[:, :P])
+    srt = np.sort(lb, axis=1)
+    for i in range(B):  # greedy token identical unless the top-1/top-2 margin is inside the tolerance
+        if srt[i, -1] - srt[i, -2] > tol:
+            assert ha[i, P] == hb[i, P]
+    a.close()
+    b.close()
+
+
+def test_prefill_rejects_bad_state():
+    gpu = DecoderModel(256, 1, 4, 1000, batch=1, max_ctx=16, seed=SEED)
+    with pytest.raises(capi.ConfigError):
+        gpu.prefill()  # no prompt
+    gpu.set_prompt(np.array([[1, 2, 3]], dtype=np.int32))
+    gpu.step(1)
+    with pytest.raises(capi.ConfigError):
+        gpu.prefill()  # not at position 0
+    gpu.close()
