@@ -41,6 +41,60 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def measured_tensor_peak():
+    """Dense bf16 TFLOP/s for a kernel timed alone (burst), measured or the recipe's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    return 1590.0, "fallback"
+
+
+def tc_roofline(E, torch, preset, M, dtype, stream):
+    """The prefill's dominant kernel: the tcgen05 GEMM at the layer shapes with M = batch x prompt,
+    each timed alone (CUDA-graph replays, CUDA events on the launching stream).  Returns the
+    flop-weighted TFLOP/s (TOP/s for int8) and the per-shape table."""
+    i8 = dtype == "int8"
+    dev = torch.device("cuda")
+    rows = []
+    tot_f = tot_t = 0.0
+    for name, N, K in gemm_shapes(preset, 1)[0]:
+        if i8:
+            w = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
+            x = torch.randint(-127, 128, (M, K), dtype=torch.int8, device=dev)
+            ws, xs = torch.rand(N, device=dev) * 1e-3, torch.rand(M, device=dev) * 1e-2
+        else:
+            w = (torch.randn(N, K, device=dev) * 0.02).half()
+            x = torch.randn(M, K, device=dev).half()
+            ws = xs = None
+        out = torch.empty(M, N, dtype=torch.float16, device=dev)
+        reps = 10
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                E.gemm_large_batch(w, x, w_scales=ws, x_scales=xs, out=out, stream=stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(reps):
+                    E.gemm_large_batch(w, x, w_scales=ws, x_scales=xs, out=out, stream=stream)
+        torch.cuda.synchronize()
+        best = 1e9
+        with torch.cuda.stream(stream):  # replay on the stream the events are recorded on
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+                b.synchronize()
+                best = min(best, a.elapsed_time(b) / reps)
+        f = 2.0 * M * N * K
+        rows.append({"kernel": f"tc_gemm[{name}] M={M} N={N} K={K}", "us": round(best * 1e3, 2),
+                     "tflops": round(f / (best * 1e-3) / 1e12, 1)})
+        tot_f += f
+        tot_t += best * 1e-3
+        del g
+    return tot_f / tot_t / 1e12, rows
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
@@ -301,12 +355,27 @@ def run_ours(args, preset, rank, world, local_rank):
 
             dist.barrier()
 
-    # ---- device-timed decode (inputs resident in HBM)
-    model.set_prompt(prompt, stream=stream)
-    t0 = time.perf_counter()
-    model.step(args.prompt, stream=stream)  # prefill: prompt tokens through the same step graph
+    # ---- prompt prefill: the large-batch (tcgen05) path at TP = 1, else the prompt tokens through
+    # the decode step graph
+    use_tc_prefill = world == 1 and not args.token_prefill
+
+    def do_prefill():
+        model.set_prompt(prompt, stream=stream)
+        if use_tc_prefill:
+            model.prefill(stream=stream)
+        else:
+            model.step(args.prompt, stream=stream)
+
+    do_prefill()  # first call builds the row-major weight copies and buffers
     stream.synchronize()
-    prefill_s = time.perf_counter() - t0
+    pst, pen = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pst.record(stream)
+    do_prefill()
+    pen.record(stream)
+    pen.synchronize()
+    prefill_ms = pst.elapsed_time(pen)
+
+    # ---- device-timed decode (inputs resident in HBM)
     model.step(args.warmup, stream=stream)
     pos0 = args.prompt + args.warmup
     barrier()
@@ -337,8 +406,7 @@ def run_ours(args, preset, rank, world, local_rank):
     # ---- end to end through the C ABI with host buffers (H2D tokens in, D2H tokens out each step)
     import ctypes as C
 
-    model.set_prompt(prompt, stream=stream)
-    model.step(args.prompt, stream=stream)
+    do_prefill()
     stream.synchronize()
     tin = torch.empty(args.batch, dtype=torch.int32, pin_memory=True)
     tout = torch.empty(args.batch, dtype=torch.int32, pin_memory=True)
@@ -371,6 +439,8 @@ def run_ours(args, preset, rank, world, local_rank):
     insitu = insitu_roofline(model, preset, world, args.batch, args.dtype, peak_gbs, stream)
     roof = None
     cpu = None
+    prefill = {"ms": round(prefill_ms, 3), "tokens_per_s": round(args.batch * args.prompt * 1e3 / prefill_ms, 1),
+               "path": "decode step graph, token by token"}
     if rank == 0:
         per_kernel, agg_alone = kernel_roofline(E, torch, preset, world, args.batch, args.dtype, peak_gbs, stream)
         agg = insitu[0] if insitu else agg_alone
@@ -394,6 +464,22 @@ def run_ours(args, preset, rank, world, local_rank):
                 "alone": {"achieved": round(agg_alone, 1), "per_kernel": per_kernel},
                 "step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak_gbs, 4),
                          "bytes_per_step": int(step_bytes / args.steps)}}
+        if use_tc_prefill:
+            M = args.batch * args.prompt
+            tpk, tkind = measured_tensor_peak()
+            if args.dtype == "int8":
+                tpk, tkind = 2 * tpk, f"2x {tkind} bf16 (int8 tensor rate)"
+            agg_tc, rows_tc = tc_roofline(E, torch, preset, M, args.dtype, stream)
+            h, L = preset.hidden, preset.layers
+            pf_flops = 2.0 * M * 12 * h * h * L + 2.0 * M * args.prompt * h * L
+            prefill = {"ms": round(prefill_ms, 3), "tokens_per_s": round(M * 1e3 / prefill_ms, 1),
+                       "tflops": round(pf_flops / (prefill_ms * 1e-3) / 1e12, 1), "path": "tcgen05 large-batch",
+                       "roofline": {"bound": "tensor", "achieved": round(agg_tc, 1), "peak": tpk,
+                                    "unit": "TOP/s" if args.dtype == "int8" else "TFLOP/s",
+                                    "frac": round(agg_tc / tpk, 4), "peak_kind": tkind,
+                                    "kernel": "tc_gemm_kernel (tcgen05.mma + TMEM), flop-weighted over the layer "
+                                              "GEMMs at M = batch x prompt, each timed alone",
+                                    "per_kernel": rows_tc}}
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             cms, kind, sample = reference_ms_per_token(preset, 1, args.batch, dtype_bytes, args.cpu_budget, threads)
@@ -408,7 +494,7 @@ def run_ours(args, preset, rank, world, local_rank):
                 "d2h_bytes_per_step": 4 * args.batch, "ms_per_step": e2e_s * 1e3 / args.steps},
         "gpu_launches": int(info.kernels_per_step) * args.steps,
         "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-        "prefill_ms": round(prefill_s * 1e3, 2), "generated_sample": gen_sample,
+        "prefill": prefill, "generated_sample": gen_sample,
     }
     model.close()
     if comm is not None:
@@ -430,6 +516,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")
     args = ap.parse_args()
