@@ -261,6 +261,8 @@ class DecoderSession {
     check(dsinf_model_set_prompt(m_, prompts.data(), prompt_len, stream));
   }
   void step(std::int64_t n = 1, void* stream = nullptr) { check(dsinf_decode_steps(m_, n, stream)); }
+  // the whole prompt at once on the tensor cores (same resulting state as step(prompt_len))
+  void prefill(void* stream = nullptr) { check(dsinf_model_prefill(m_, stream)); }
   // one step with host buffers: tokens_in -> the model -> tokens_out (synchronous)
   void step_host(const std::int32_t* tokens_in, std::int32_t* tokens_out, void* stream = nullptr) {
     check(dsinf_decode_step_host(m_, tokens_in, tokens_out, stream));
