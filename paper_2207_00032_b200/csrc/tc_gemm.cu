@@ -190,22 +190,26 @@ __device__ __forceinline__ void epilogue32(const Params& p, int row, int n0, con
   }
 }
 
+// Persistent: one CTA per SM walks the tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... (m
+// fastest, so the CTAs in flight share a weight tile: W streams from HBM about once, x stays in
+// L2).  The accumulator is double-buffered in TMEM (2 x 256 columns): the epilogue warps drain
+// tile j while the MMA thread already accumulates tile j + 1, and the TMA ring runs across tile
+// boundaries.
 template <bool kInt8>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* acc_ready = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+  uint64_t* acc_full = empty + kStages;   // [2] MMA -> epilogue (tcgen05.commit)
+  uint64_t* acc_empty = acc_full + 2;     // [2] epilogue -> MMA (128 epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // m fastest: the row tiles that share a weight tile run together (W streams from HBM once,
-  // x stays in L2)
-  const int m0 = blockIdx.x * kBM;
-  const int n0 = blockIdx.y * kBN;
   const int nk = p.k_blocks;
+  const int m_tiles = (p.M + kBM - 1) / kBM;
+  const int tiles = m_tiles * ((p.N + kBN - 1) / kBN);
 
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.amap);
@@ -214,63 +218,84 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(acc_ready, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&acc_full[a], 1);
+      ptx::mbar_init(&acc_empty[a], kEpiThreads);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kBN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * kBN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ================= TMA producer
+    if (lane == 0) {  // ================= TMA producer (ring continuous across tiles)
       ptx::pdl_wait();
       const uint64_t pol_a = ptx::policy_evict_last();   // x tiles are re-read by every column tile
       const uint64_t pol_b = ptx::policy_evict_normal();
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) ptx::mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-        ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
-        uint8_t* sa = smem + s * kStageBytes;
-        ptx::tma_load_2d(sa, &p.amap, kb * kBK, m0, &full[s], pol_a);
-        ptx::tma_load_2d(sa + kABytes, &p.bmap, kb * kBK, n0, &full[s], pol_b);
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % m_tiles) * kBM, n0 = (t / m_tiles) * kBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+          uint8_t* sa = smem + s * kStageBytes;
+          ptx::tma_load_2d(sa, &p.amap, kb * kBK, m0, &full[s], pol_a);
+          ptx::tma_load_2d(sa + kABytes, &p.bmap, kb * kBK, n0, &full[s], pol_b);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ================= MMA issuer
       constexpr uint32_t idesc = instr_desc<kInt8>();
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        ptx::mbar_wait(&full[s], (kb / kStages) & 1);
+      int it = 0, j = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+        const int a = j & 1;
+        ptx::mbar_wait(&acc_empty[a], ((j >> 1) & 1) ^ 1);  // the epilogue has drained this buffer
         tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + s * kStageBytes);
-        const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+        const uint32_t acc = tmem + static_cast<uint32_t>(a * kBN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          ptx::mbar_wait(&full[s], (it / kStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + s * kStageBytes);
+          const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 32; ++k)  // 32 bytes of K per MMA (16 fp16 / 32 int8)
-          mma<kInt8>(tmem, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
-                     (kb | k) != 0 ? 1u : 0u);
-        mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+          for (int k = 0; k < kBK / 32; ++k)  // 32 bytes of K per MMA (16 fp16 / 32 int8)
+            mma<kInt8>(acc, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
+                       (kb | k) != 0 ? 1u : 0u);
+          mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+        }
+        mma_commit(&acc_full[a]);
       }
-      mma_commit(acc_ready);
     }
   } else {
     // ================= epilogue: warp w owns TMEM lanes [32 (w % 4), +32)
     const int quarter = warp & 3;
-    const int row = m0 + quarter * 32 + lane;
-    ptx::mbar_wait(acc_ready, 0);
-    tc_fence_after();
-    ptx::pdl_trigger();
+    int j = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      const int m0 = (t % m_tiles) * kBM, n0 = (t / m_tiles) * kBN;
+      const int row = m0 + quarter * 32 + lane;
+      ptx::mbar_wait(&acc_full[a], (j >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < kBN / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
-      if (row < p.M && n0 + c * 32 < p.N) epilogue32<kInt8>(p, row, n0 + c * 32, v);
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(a * kBN + c * 32), v);
+        if (row < p.M && n0 + c * 32 < p.N) epilogue32<kInt8>(p, row, n0 + c * 32, v);
+      }
+      tc_fence_before();
+      ptx::mbar_arrive(&acc_empty[a]);  // buffer a may be overwritten by tile j + 2
     }
+    ptx::pdl_trigger();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kBN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * kBN);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -315,8 +340,19 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
 }
 
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    DSINF_CUDA_CHECK(cudaGetDevice(&dev));
+    DSINF_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 void launch(const Params& p, bool int8, cudaStream_t s) {
-  const dim3 grid((p.M + kBM - 1) / kBM, (p.N + kBN - 1) / kBN);
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN);
+  const dim3 grid(std::min(tiles, sm_count()));
   if (int8)
     tc_gemm_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(p);
   else

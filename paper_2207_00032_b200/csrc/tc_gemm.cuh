@@ -26,6 +26,7 @@ constexpr int kABytes = kBM * kBK;   // 16 KB
 constexpr int kBBytes = kBN * kBK;   // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 192;        // warp 0 TMA, warp 1 MMA issue + TMEM owner, warps 2..5 epilogue
+constexpr int kEpiThreads = 128;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 enum Epi : int {
