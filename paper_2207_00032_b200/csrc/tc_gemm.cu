@@ -10,6 +10,7 @@
 //               owns the 32 TMEM lanes of its quarter), dequantise / bias / GeLU / RoPE / residual,
 //               store straight to global.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -77,6 +78,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    ptx::smem_u32(bar))
                : "memory");
+}
+// Commit to the same barrier in every CTA of `mask` (cluster pair: both CTAs' empty slots).
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   ptx::smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+// 2-D TMA box multicast to the same smem offset (and barrier) of every CTA in `mask`.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* map, int c0, int c1, uint64_t* bar, uint16_t mask,
+                                               uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(ptx::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(ptx::smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
 }
 // 32 lanes x 32 columns of 32-bit: thread t of the warp gets lane (base + t), columns [col, col + 32).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -195,7 +212,10 @@ __device__ __forceinline__ void epilogue32(const Params& p, int row, int n0, con
 // L2).  The accumulator is double-buffered in TMEM (2 x 256 columns): the epilogue warps drain
 // tile j while the MMA thread already accumulates tile j + 1, and the TMA ring runs across tile
 // boundaries.
-template <bool kInt8>
+// kPair: clusters of 2 CTAs on row tiles (m, m+1) of the same weight tile; each CTA TMA-loads one
+// 128-row half of the weight tile and multicasts it to both, halving the L2 -> SM weight traffic;
+// both CTAs' MMA commits free a stage in both (the halves live in both CTAs' smem).
+template <bool kInt8, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -209,14 +229,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   const int lane = threadIdx.x & 31;
   const int nk = p.k_blocks;
   const int m_tiles = (p.M + kBM - 1) / kBM;
-  const int tiles = m_tiles * ((p.N + kBN - 1) / kBN);
+  // units: single tiles, or (kPair) row-tile pairs handled by the two CTAs of a cluster
+  const int m_units = kPair ? (m_tiles + 1) / 2 : m_tiles;
+  const int units = m_units * ((p.N + kBN - 1) / kBN);
+  const int rank = kPair ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const int unit0 = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ustride = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  auto m_of = [&](int u) { return ((kPair ? 2 * (u % m_units) + rank : u % m_units)) * kBM; };
+  auto n_of = [&](int u) { return (u / m_units) * kBN; };
 
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.amap);
     ptx::prefetch_tensormap(&p.bmap);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], kPair ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&acc_full[a], 1);
@@ -226,7 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * kBN);
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();  // both CTAs' barriers initialised before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -236,15 +266,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       const uint64_t pol_a = ptx::policy_evict_last();   // x tiles are re-read by every column tile
       const uint64_t pol_b = ptx::policy_evict_normal();
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % m_tiles) * kBM, n0 = (t / m_tiles) * kBN;
+      for (int u = unit0; u < units; u += ustride) {
+        const int m0 = m_of(u), n0 = n_of(u);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           ptx::mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
           uint8_t* sa = smem + s * kStageBytes;
           ptx::tma_load_2d(sa, &p.amap, kb * kBK, m0, &full[s], pol_a);
-          ptx::tma_load_2d(sa + kABytes, &p.bmap, kb * kBK, n0, &full[s], pol_b);
+          if constexpr (kPair)  // my half of the weight tile, into both CTAs
+            tma_load_2d_mc(sa + kABytes + rank * (kBBytes / 2), &p.bmap, kb * kBK, n0 + rank * (kBN / 2), &full[s],
+                           0x3, pol_b);
+          else
+            ptx::tma_load_2d(sa + kABytes, &p.bmap, kb * kBK, n0, &full[s], pol_b);
         }
       }
     }
@@ -252,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     if (lane == 0) {  // ================= MMA issuer
       constexpr uint32_t idesc = instr_desc<kInt8>();
       int it = 0, j = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      for (int u = unit0; u < units; u += ustride, ++j) {
         const int a = j & 1;
         ptx::mbar_wait(&acc_empty[a], ((j >> 1) & 1) ^ 1);  // the epilogue has drained this buffer
         tc_fence_after();
@@ -267,7 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
           for (int k = 0; k < kBK / 32; ++k)  // 32 bytes of K per MMA (16 fp16 / 32 int8)
             mma<kInt8>(acc, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
                        (kb | k) != 0 ? 1u : 0u);
-          mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+          if constexpr (kPair)
+            mma_commit_mc(&empty[s], 0x3);  // both CTAs hold halves of this stage's weight tile
+          else
+            mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
         }
         mma_commit(&acc_full[a]);
       }
@@ -276,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     // ================= epilogue: warp w owns TMEM lanes [32 (w % 4), +32)
     const int quarter = warp & 3;
     int j = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+    for (int u = unit0; u < units; u += ustride, ++j) {
       const int a = j & 1;
-      const int m0 = (t % m_tiles) * kBM, n0 = (t / m_tiles) * kBN;
+      const int m0 = m_of(u), n0 = n_of(u);
       const int row = m0 + quarter * 32 + lane;
       ptx::mbar_wait(&acc_full[a], (j >> 1) & 1);
       tc_fence_after();
@@ -294,7 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     ptx::pdl_trigger();
   }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();  // the peer's last commits / multicasts into our smem have landed
+  else
+    __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 2 * kBN);
 }
 
@@ -331,13 +371,16 @@ void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld
   if (p.M < 1 || p.N < 1 || p.K < 1) throw ConfigError("tc_gemm: gemm shape dims must be positive");
   const int kbytes = p.K * elem_bytes;
   byte_map(&p.amap, x, p.M, kbytes, x_ld_bytes, kBM);
-  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, kBN);
+  p.pair = ((p.M + kBM - 1) / kBM) >= 2 && !std::getenv("DSINF_TC_NOPAIR");
+  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, p.pair ? kBN / 2 : kBN);
   p.k_blocks = (kbytes + kBK - 1) / kBK;
 }
 
 void configure() {
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
 }
 
 int sm_count() {
@@ -351,12 +394,33 @@ int sm_count() {
 }
 
 void launch(const Params& p, bool int8, cudaStream_t s) {
-  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN);
-  const dim3 grid(std::min(tiles, sm_count()));
+  const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.N + kBN - 1) / kBN;
+  if (p.pair) {
+    const int units = (m_tiles + 1) / 2 * n_tiles;
+    const int ctas = 2 * std::min(units, sm_count() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if (int8)
+      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<true, true>, p));
+    else
+      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<false, true>, p));
+    return;
+  }
+  const dim3 grid(std::min(m_tiles * n_tiles, sm_count()));
   if (int8)
-    tc_gemm_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(p);
+    tc_gemm_kernel<true, false><<<grid, kThreads, kSmemBytes, s>>>(p);
   else
-    tc_gemm_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(p);
+    tc_gemm_kernel<false, false><<<grid, kThreads, kSmemBytes, s>>>(p);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -42,6 +42,7 @@ struct Params {
   alignas(64) CUtensorMap bmap;  // W [N][K]: box 128 B x 256 rows, 128B swizzle
   int M, N, K;
   int k_blocks;                  // ceil(K * elem / 128)
+  int pair;                      // cluster-pair mode (set by make_maps: >= 2 row tiles)
   const float* x_scale;          // int8: [M]
   const float* w_scale;          // int8: [N]
   const __half* bias;            // optional [N]
