@@ -284,14 +284,23 @@ def gemm_algo_bytes(N, K, batch, int8):
 
 
 def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
-    """Per-launch device timeline (globaltimer: first CTA start -> last CTA end) of `steps` decode
-    steps replayed right after the timed region from the same CUDA graph (re-captured with two
-    timestamp atomics per CTA).  Returns (sbi_gemm byte-weighted GB/s, per-kind table) or None."""
+    """Per-launch device timeline of `steps` decode steps replayed right after the timed region from
+    the same CUDA graph (re-captured with timestamp atomics per CTA; globaltimer).
+
+    Launches overlap (programmatic dependent launch starts a GEMM's CTAs, and their weight prefetch,
+    while the previous kernel still runs), so each launch is charged the INTERVAL from the previous
+    launch's last-CTA end to its own last-CTA end: the intervals tile the step exactly, with no
+    double counting.  `achieved` = SBI-GeMM algorithmic bytes / SBI-GeMM intervals.  The
+    first-CTA-start -> last-CTA-end span is reported beside it.  Returns (GB/s, table) or None."""
     from paper_2207_00032_b200 import _capi as capi
 
     tr = model.launch_trace(steps, stream=stream).astype(np.float64)
     kinds = [capi.LK_NAMES[int(k)] for k in tr[0, :, 2]]
     dur = (tr[:, :, 1] - tr[:, :, 0]) / 1e3
+    ends = tr[:, :, 1]
+    first = np.minimum.accumulate(tr[:, :, 0], axis=1)[:, :1]
+    prev_end = np.concatenate([first, np.maximum.accumulate(ends, axis=1)[:, :-1]], axis=1)
+    interval = np.maximum(ends - prev_end, 0.0) / 1e3
     span = float(np.median((tr[:, -1, 1] - tr[:, 0, 0]) / 1e3))
     layer, lm = gemm_shapes(preset, tp)
     shapes = {n: (N, K) for n, N, K in layer + [lm]}
@@ -299,17 +308,17 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
     table = {}
     for k in dict.fromkeys(kinds):
         idx = [i for i, kk in enumerate(kinds) if kk == k]
-        d = dur[:, idx]
-        row = {"launches_per_step": len(idx), "us_mean": round(float(d.mean()), 2),
-               "share_of_step": round(float(d.sum() / steps / span), 4)}
+        d, iv = dur[:, idx], interval[:, idx]
+        row = {"launches_per_step": len(idx), "interval_us_mean": round(float(iv.mean()), 2),
+               "span_us_mean": round(float(d.mean()), 2), "share_of_step": round(float(iv.sum() / steps / span), 4)}
         if k in shapes:
             N, K = shapes[k]
             b = gemm_algo_bytes(N, K, batch, dtype == "int8" and k != "lm_head")
             row["bytes"] = b
-            row["gbs"] = round(b / (d.mean() * 1e-6) / 1e9, 1)
+            row["gbs"] = round(b / (iv.mean() * 1e-6) / 1e9, 1)
             row["frac"] = round(row["gbs"] / peak_gbs, 4)
-            tot_b += b * d.size
-            tot_us += float(d.sum())
+            tot_b += b * iv.size
+            tot_us += float(iv.sum())
         table[k] = row
     if tot_us == 0:
         return None
@@ -457,8 +466,9 @@ def run_ours(args, preset, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(agg, 1), "peak": peak_gbs, "unit": "GB/s",
                 "frac": round(agg / peak_gbs, 4), "traffic": traffic, "traffic_launch": traffic_note,
                 "peak_kind": peak_kind,
-                "kernel": ("sbi_gemm_kernel: byte-weighted over every SBI-GeMM launch of 8 decode steps, each "
-                           "launch timed first-CTA-start -> last-CTA-end on the device (globaltimer)"
+                "kernel": ("sbi_gemm_kernel: algorithmic bytes of every SBI-GeMM launch of 8 decode steps over the "
+                           "device-timeline intervals they own (previous launch's last-CTA end -> own last-CTA "
+                           "end, globaltimer)"
                            if insitu else "sbi_gemm_kernel (byte-weighted over one step's GEMM launches, timed alone)"),
                 "in_step": insitu[1] if insitu else None,
                 "alone": {"achieved": round(agg_alone, 1), "per_kernel": per_kernel},

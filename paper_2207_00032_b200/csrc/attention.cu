@@ -5,6 +5,7 @@
 // (attn_dev.cuh) and merge their (max, sum, output) partials through distributed shared memory.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "attn_dev.cuh"
 #include "common.h"
@@ -95,9 +96,14 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
 }  // namespace
 
 int attention_chunks(int B, int H) {
+  // enough CTAs for the KV stream's memory parallelism: (batch, head) pairs x chunks >= target
+  static const int target = [] {
+    const char* v = std::getenv("DSINF_ATTN_CTAS");
+    return v ? std::atoi(v) : 2 * 148;
+  }();
   const int pairs = B * H;
   int c = 1;
-  while (c < 8 && pairs * c < 2 * 148) c <<= 1;
+  while (c < 8 && pairs * c < target) c <<= 1;
   return c;
 }
 

@@ -10,7 +10,7 @@
 //     K3 attn-out GEMM                     -> d_attn (partial when t > 1)         AR(d_attn)
 //     K4 LN2+MLP-up+bias+GeLU              prologue: res0 = res1 + d_attn + b_o ; LN2
 //     K5 MLP-down GEMM                     -> d_mlp                               AR(d_mlp)
-//   LM head (final LN prologue: res0 + d_mlp + b_down[L-1]) -> logits ; argmax    AG(argmax)
+//   LM head (final LN prologue: res0 + d_mlp + b_down[L-1]) -> logits + fused argmax keys  AG(keys)
 //   select: greedy token (ties -> lowest id), pos += 1
 // The residual bias+add (paper region 4) lives in the next LayerNorm's prologue, which is
 // also where the TP all-reduced partial is folded in, so t = 1 and t > 1 share one path.
@@ -118,6 +118,7 @@ struct dsinf_model {
   int* pos = nullptr;
   float* am_val = nullptr;  // [t][B]
   int32_t* am_idx = nullptr;
+  unsigned long long* am_key = nullptr;  // [t][B] fused LM-head argmax keys (zeroed per step)
   dsinf::nccl::Comm comm = nullptr;
   cudaStream_t cap_stream = nullptr;
   cudaGraph_t graph = nullptr;
@@ -714,19 +715,12 @@ struct Enqueuer {
     }
     p.epi = gemm::EPI_F32;
     p.out = sh.logits;
-    gemm_launch(p, sh.plan_lm, false, 5);
-    ops::ArgmaxParams ap{};
-    ap.logits = sh.logits;
-    ap.ld = static_cast<int>(m.Vl);
+    // greedy argmax fused into the epilogue: one key per (shard, row), ties -> lowest index
     const int64_t first = sh.rank * m.Vl;
-    ap.valid = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(m.Vl, m.V - first)));
-    ap.B = m.B;
-    ap.idx_offset = first;
-    ap.out_val = m.am_val + sh.rank * m.B;
-    ap.out_idx = m.am_idx + sh.rank * m.B;
-    ap.trace = tslot(DSINF_LK_ARGMAX);
-    ops::argmax(ap, s, P(6));
-    ++launches;
+    p.am_out = m.am_key + sh.rank * m.B;
+    p.am_valid = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(m.Vl, m.V - first)));
+    p.am_offset = first;
+    gemm_launch(p, sh.plan_lm, false, 5);
   }
 
   // Sum of the t partials of `which` (0 = d_attn, 1 = d_mlp).
@@ -869,10 +863,10 @@ struct Enqueuer {
     g.h = h;
     ops::prefill_gather(g, s);
     ++launches;
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m.am_key, 0, sizeof(unsigned long long) * m.B, s));
     lm_head(sh);
     ops::SelectParams sp{};
-    sp.vals = m.am_val;
-    sp.idxs = m.am_idx;
+    sp.keys = m.am_key;
     sp.shards = 1;
     sp.B = m.B;
     sp.next_tok = m.next_tok;
@@ -895,6 +889,7 @@ struct Enqueuer {
       DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + 2 * ptx::kTraceEnd, 0xff, ptx::kTraceEnd * sizeof(unsigned long long), s));
       DSINF_CUDA_CHECK(cudaMemsetAsync(m.ltrace + 3 * ptx::kTraceEnd, 0, (ptx::kTracePhases - 3) * ptx::kTraceEnd * sizeof(unsigned long long), s));
     }
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m.am_key, 0, sizeof(unsigned long long) * m.t * m.B, s));
     for (Shard& sh : m.shards) {  // per-step statistics slots
       if (sh.lnstats)
         DSINF_CUDA_CHECK(cudaMemsetAsync(sh.lnstats, 0, (2 * m.L + 1) * gemm::kLnSlotWords * sizeof(long long), s));
@@ -936,12 +931,10 @@ struct Enqueuer {
     for (Shard& sh : m.shards) lm_head(sh);
     if (m.t > 1 && m.rt.tp_mode == DSINF_TP_NCCL) {
       // gather every rank's (value, index) pair; slots are laid out [rank][B]
-      nccl::allgather_bytes(m.am_val + m.shards[0].rank * m.B, m.am_val, m.B * sizeof(float), m.comm, s);
-      nccl::allgather_bytes(m.am_idx + m.shards[0].rank * m.B, m.am_idx, m.B * sizeof(int32_t), m.comm, s);
+      nccl::allgather_bytes(m.am_key + m.shards[0].rank * m.B, m.am_key, m.B * sizeof(unsigned long long), m.comm, s);
     }
     ops::SelectParams sp{};
-    sp.vals = m.am_val;
-    sp.idxs = m.am_idx;
+    sp.keys = m.am_key;
     sp.shards = m.t;
     sp.B = m.B;
     sp.next_tok = m.next_tok;
@@ -1072,6 +1065,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     m->pos = m->alloc_n<int>(1);
     m->am_val = m->alloc_n<float>(static_cast<int64_t>(m->t) * m->B);
     m->am_idx = m->alloc_n<int32_t>(static_cast<int64_t>(m->t) * m->B);
+    m->am_key = m->alloc_n<unsigned long long>(static_cast<int64_t>(m->t) * m->B);
     DSINF_CUDA_CHECK(cudaMemsetAsync(m->prompt, 0, sizeof(int32_t) * m->B * m->prompt_cap, s));
     DSINF_CUDA_CHECK(cudaMemsetAsync(m->next_tok, 0, sizeof(int32_t) * m->B, s));
     DSINF_CUDA_CHECK(cudaMemsetAsync(m->hist, 0, sizeof(int32_t) * m->B * m->max_ctx, s));

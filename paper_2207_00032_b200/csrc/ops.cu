@@ -286,14 +286,22 @@ __global__ void select_kernel(const __grid_constant__ SelectParams p) {
   ptx::pdl_wait();
   const int pos = *p.pos;
   for (int b = threadIdx.x; b < p.B; b += blockDim.x) {
-    float bv = p.vals[b];
-    int32_t bx = p.idxs[b];
-    for (int s = 1; s < p.shards; ++s) {  // ties -> lowest vocabulary index
-      const float v = p.vals[s * p.B + b];
-      const int32_t x = p.idxs[s * p.B + b];
-      if (v > bv || (v == bv && x < bx)) {
-        bv = v;
-        bx = x;
+    float bv = 0.f;
+    int32_t bx = 0;
+    if (p.keys != nullptr) {  // fused LM-head argmax: the max key is the max logit, lowest index
+      unsigned long long k = p.keys[b];
+      for (int s = 1; s < p.shards; ++s) k = max(k, p.keys[s * p.B + b]);
+      bx = gemm::argmax_key_index(k);
+    } else {
+      bv = p.vals[b];
+      bx = p.idxs[b];
+      for (int s = 1; s < p.shards; ++s) {  // ties -> lowest vocabulary index
+        const float v = p.vals[s * p.B + b];
+        const int32_t x = p.idxs[s * p.B + b];
+        if (v > bv || (v == bv && x < bx)) {
+          bv = v;
+          bx = x;
+        }
       }
     }
     p.next_tok[b] = bx;

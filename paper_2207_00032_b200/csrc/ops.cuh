@@ -116,6 +116,7 @@ void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl);
 struct SelectParams {
   const float* vals;     // [shards][B] (row stride B)
   const int32_t* idxs;   // [shards][B]
+  const unsigned long long* keys;  // or: packed (logit, index) keys [shards][B] (gemm::argmax_key)
   int shards, B;
   int32_t* next_tok;
   int* pos;

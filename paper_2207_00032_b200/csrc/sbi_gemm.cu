@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   // one warp per batch row (lanes over column pairs) so row statistics reduce with shuffles
   for (int b = warp; b < p.B; b += kThreads / 32) {
     dev::RowStat st;
+    unsigned long long best = 0;  // fused argmax (p.am_out)
     for (int q = lane; q < pairs; q += 32) {
       const int c = c_begin + 2 * q;
       const int n = n0 + c;
@@ -231,26 +232,50 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         if (has1) ws.y = __ldg(p.w_scale + n + 1);
       }
       const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
+      // the ranks' partials in batches of 4 DSMEM loads in flight, summed in rank order
       float y0, y1;
       if constexpr (kInt8) {
         int s0 = 0, s1 = 0;
-        for (int r = 0; r < nsplit; ++r) {
-          const int2 v = ptx::ld_dsmem_i2(ptx::map_shared_rank(part_base + off, r));
-          s0 += v.x;
-          s1 += v.y;
+        for (int r0 = 0; r0 < nsplit; r0 += 4) {
+          uint2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + u < nsplit) v[u] = ptx::ld_dsmem_u2(ptx::map_shared_rank(part_base + off, r0 + u));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + u < nsplit) {
+              s0 += static_cast<int>(v[u].x);
+              s1 += static_cast<int>(v[u].y);
+            }
         }
         dev::dequant_pair_ws(hd, b, s0, s1, ws, has1, y0, y1);
       } else {
         float2 acc2 = make_float2(0.f, 0.f);
-        for (int r = 0; r < nsplit; ++r) {
-          const float2 v = ptx::ld_dsmem_f2(ptx::map_shared_rank(part_base + off, r));
-          acc2.x += v.x;
-          acc2.y += v.y;
+        for (int r0 = 0; r0 < nsplit; r0 += 4) {
+          uint2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + u < nsplit) v[u] = ptx::ld_dsmem_u2(ptx::map_shared_rank(part_base + off, r0 + u));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + u < nsplit) {
+              acc2.x += __uint_as_float(v[u].x);
+              acc2.y += __uint_as_float(v[u].y);
+            }
         }
         y0 = acc2.x;
         y1 = acc2.y;
       }
       dev::epilogue_pair(p, b, n, y0, y1, has1, &st, p.epi == EPI_RESID ? &rin : nullptr);
+      if (p.am_out != nullptr) {
+        if (n < p.am_valid) best = max(best, argmax_key(y0, p.am_offset + n));
+        if (has1 && n + 1 < p.am_valid) best = max(best, argmax_key(y1, p.am_offset + n + 1));
+      }
+    }
+    if (p.am_out != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0 && best != 0) atomicMax(p.am_out + b, best);
     }
     if (want_stats) dev::row_stat_commit(st, es, b, lane);
   }
@@ -486,6 +511,8 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
+  if (p.am_out != nullptr && (p.epi != EPI_F32 || p.bias != nullptr))
+    throw ConfigError("sbi_gemm: the fused argmax needs the plain fp32 epilogue without bias");
   const bool xs = plan.x_stream != 0;
   if (xs) {
     if (p.pro != (int8_weights ? PRO_I8 : PRO_F16))

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -37,6 +38,17 @@ constexpr int kLnSlotWords = kStatStripes * kMaxB * 2;  // int64 words per Layer
 constexpr int kAmaxSlotWords = kStatStripes * 32;       // u32 words per amax slot
 constexpr float kSumScale = 4294967296.0f;               // 2^32
 constexpr float kSqScale = 268435456.0f;                 // 2^28
+
+// Order-preserving key of (logit, vocab index): larger logit wins, then the LOWER index.
+__host__ __device__ __forceinline__ unsigned long long argmax_key(float v, long long idx) {
+  unsigned u;
+  memcpy(&u, &v, 4);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(u) << 32) | static_cast<unsigned>(~static_cast<unsigned>(idx));
+}
+__host__ __device__ __forceinline__ int argmax_key_index(unsigned long long k) {
+  return static_cast<int>(~static_cast<unsigned>(k & 0xffffffffu));
+}
 
 enum Prologue : int {
   PRO_F16 = 0,    // x fp16 [B][x_ld] from global
@@ -93,6 +105,12 @@ struct Params {
   int heads, head_dim, max_seq;
   long long* ln_stats_out;  // EPI_RESID: accumulate the new residual's row sums (slot, zeroed per step)
   unsigned* amax_out;       // EPI_F16 / EPI_GELU_F16: accumulate row max |out|
+  // EPI_F32 without bias (LM head): greedy argmax fused into the epilogue -- per row the max of
+  // pack(value, global column) over columns < am_valid, atomicMax'd into am_out[b] (zeroed per
+  // step); ties resolve to the lowest column (moe.hpp:69-74).
+  unsigned long long* am_out;
+  int am_valid;
+  long long am_offset;
   unsigned long long* trace;  // launch timeline slot (ptx::trace_begin / trace_end) or null
   unsigned long long* cta_log;  // diagnostics: per-CTA [smid, start, release, prologue end, loop end, end] or null
 };
