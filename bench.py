@@ -232,6 +232,38 @@ def workload_config(args, preset, world):
 
 # ---------------------------------------------------------------- our path
 
+def decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, skip):
+    """BASELINE.json's full decode metric on one GPU: ms/token, tokens/s and step GB/s (fraction of
+    the measured HBM peak) for fp16 / int8 at batch 1 / 8 / 16, each a fresh model (prompt prefilled
+    on the tensor cores), device-timed over args.steps decode steps with CUDA events."""
+    rows = []
+    for dtype in ("fp16", "int8"):
+        for batch in (1, 8, 16):
+            if (dtype, batch) == skip:
+                continue
+            m = E.DecoderModel(preset.hidden, preset.layers, preset.heads, preset.vocab,
+                               dtype_bytes=1 if dtype == "int8" else 2, batch=batch,
+                               max_ctx=args.prompt + args.warmup + args.steps + 8, seed=SEED)
+            prompt = np.random.default_rng(SEED + batch).integers(0, preset.vocab, (batch, args.prompt)).astype(np.int32)
+            m.set_prompt(prompt, stream=stream)
+            m.prefill(stream=stream)
+            m.step(args.warmup, stream=stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            m.step(args.steps, stream=stream)
+            b.record(stream)
+            b.synchronize()
+            ms = a.elapsed_time(b)
+            pos0 = args.prompt + args.warmup
+            gb = sum(m.bytes_per_step(q) for q in range(pos0, pos0 + args.steps)) / (ms * 1e-3) / 1e9
+            rows.append({"dtype": dtype, "batch": batch, "ms_per_token": round(ms / args.steps, 4),
+                         "tokens_per_s": round(batch * args.steps * 1e3 / ms, 1), "step_gbs": round(gb, 1),
+                         "frac": round(gb / peak_gbs, 4)})
+            m.close()
+    return rows
+
+
 def kernel_roofline(E, torch, preset, tp, batch, dtype, peak_gbs, stream):
     """Times each SBI-GeMM shape of one layer (+ LM head) alone with CUDA events on the launching
     stream; 4 rotating weight copies (> L2) per shape.  Returns the per-kernel list and the byte-weighted
@@ -507,6 +539,13 @@ def run_ours(args, preset, rank, world, local_rank):
         "prefill": prefill, "generated_sample": gen_sample,
     }
     model.close()
+    if world == 1 and rank == 0 and not args.no_sweep:
+        sweep = decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, (args.dtype, args.batch))
+        sweep.insert(0, {"dtype": args.dtype, "batch": args.batch, "ms_per_token": round(ms_step, 4),
+                         "tokens_per_s": round(value, 1), "step_gbs": round(step_gbs, 1),
+                         "frac": round(step_gbs / peak_gbs, 4)})
+        line["decode_sweep"] = {"note": "BASELINE metric matrix on this GPU, same timing rules; frac = step GB/s "
+                                        "(algorithmic bytes) / measured HBM peak", "rows": sweep}
     if comm is not None:
         capi.lib.dsinf_nccl_comm_destroy(comm)
     if rank == 0:
@@ -526,6 +565,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the fp16/int8 x batch 1/8/16 decode matrix")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")
