@@ -386,7 +386,8 @@ def run_ours(args, preset, rank, world, local_rank):
     model = E.DecoderModel(preset.hidden, preset.layers, preset.heads, preset.vocab, dtype_bytes=dtype_bytes,
                            batch=args.batch, max_ctx=max_ctx, tp_size=world, tp_rank=rank,
                            tp_mode=capi.TP_NCCL if world > 1 else capi.TP_NONE, nccl_comm=comm,
-                           use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank)
+                           use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank,
+                           int8_act=capi.INT8_W8A16 if args.int8_act == "w8a16" else capi.INT8_W8A8)
     rng = np.random.default_rng(SEED)
     prompt = rng.integers(0, preset.vocab, (args.batch, args.prompt)).astype(np.int32)
 
@@ -566,6 +567,8 @@ def main():
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the fp16/int8 x batch 1/8/16 decode matrix")
+    ap.add_argument("--int8-act", choices=["w8a8", "w8a16"], default="w8a8",
+                    help="int8 decode GEMMs: per-token int8 activations (int32 accumulate) or weight-only")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")

@@ -121,6 +121,13 @@ int dsinf_quantize_weights_int8(const void* w_rowmajor_f16, int64_t N, int64_t K
 int dsinf_quantize_activations_int8(const void* x_f16, int64_t B, int64_t K, int8_t* xq,
                                     float* scales, void* stream);
 
+/* INT8 weight modes ("INT8 weight-quantized GEMMs"):
+ *  W8A8  per-token int8 activations, exact int32 accumulation (bit-exact vs the oracle);
+ *  W8A16 weight-only: fp16 activations, int8 weights widened in registers, fp32 accumulation,
+ *        per-output-row dequant -- no activation quantisation on the decode critical path. */
+#define DSINF_INT8_W8A8 0
+#define DSINF_INT8_W8A16 1
+
 #define DSINF_EPI_NONE 0
 #define DSINF_EPI_GELU 1 /* tanh GeLU after the bias */
 
@@ -137,6 +144,7 @@ typedef struct dsinf_gemm_args {
   int32_t out_dtype;      /* F32 or F16 */
   int32_t epilogue;       /* DSINF_EPI_* */
   int32_t ksplit;         /* 0 = launch plan chooses; else cluster split count {1,2,4,8,16} */
+  int32_t int8_act;       /* I8 weights: DSINF_INT8_W8A8 (int8 x, int32 accumulate) or DSINF_INT8_W8A16 */
 } dsinf_gemm_args;
 
 int dsinf_gemm(const dsinf_gemm_args* args, void* stream);
@@ -208,6 +216,8 @@ typedef struct dsinf_runtime_config {
   float rope_base;
   int32_t device;       /* CUDA device ordinal */
   int32_t use_step_kernel; /* TP = 1: run each decode step as ONE persistent kernel */
+  int32_t int8_act;     /* dtype_bytes 1: DSINF_INT8_W8A8 (default) or DSINF_INT8_W8A16 (decode GEMMs;
+                           the tensor-core prefill stays W8A8) */
 } dsinf_runtime_config;
 
 typedef struct dsinf_model dsinf_model;

@@ -463,8 +463,25 @@ static void gemm16(const float* W, int64_t N, int64_t K, int sm, const float* x1
   free(xd);
 }
 
+/* int8 weights, fp16 activations (W8A16, weight-only): y = fp32(sum_k q w_k x_k) * s_w (the sum in
+ * fp64 here; the GPU accumulates the exact int8 x fp16 products in fp32) */
+static void gemm8_a16(const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B, float* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t b = 0; b < B; ++b) {
+      double a = 0.0;
+      for (int64_t k = 0; k < K; ++k) a += (double)W[n * K + k] * (double)x16[b * K + k];
+      y[b * N + n] = (float)a * ws[n];
+    }
+}
+
 /* int8 path GEMM on fp16 activations: per-token quantisation, exact int32, fp32 dequant */
+static int g_int8_act = 0;
 static void gemm8(const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B, float* y) {
+  if (g_int8_act == 1) {
+    gemm8_a16(W, ws, N, K, x16, B, y);
+    return;
+  }
   int8_t* xq = (int8_t*)malloc((size_t)(B * K));
   float* xs = falloc(B);
   or_quant_rows(x16, B, K, xq, xs);
@@ -475,6 +492,7 @@ static void gemm8(const int8_t* W, const float* ws, int64_t N, int64_t K, const 
 
 int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits, int32_t* next_tokens) {
   const int64_t h = m->h, d = m->d, Hl = m->Hl, B = m->B, Fl = m->Fl, mc = m->c.max_ctx;
+  g_int8_act = m->c.int8_act;
   const int i8 = m->c.dtype_bytes == 1;
   const int sm = m->c.sm_count;
   if (pos < 0 || pos >= mc) return 2;

@@ -27,7 +27,8 @@ class Schedule(C.Structure):
 class Config(C.Structure):
     _fields_ = [("hidden", C.c_int64), ("layers", C.c_int64), ("heads", C.c_int64), ("vocab", C.c_int64),
                 ("max_ctx", C.c_int64), ("dtype_bytes", C.c_int32), ("tp", C.c_int32), ("batch", C.c_int32),
-                ("sm_count", C.c_int32), ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float)]
+                ("sm_count", C.c_int32), ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float),
+                ("int8_act", C.c_int32)]
 
 
 def _load(path):
@@ -180,9 +181,9 @@ class OracleModel:
     """CPU decoder with the GPU path's storage points (fp16 / fp32) and exec_reference GEMM order."""
 
     def __init__(self, hidden, layers, heads, vocab=50257, *, dtype_bytes=2, tp=1, batch=1, max_ctx=256,
-                 seed=20220701, ln_eps=1e-5, rope_base=10000.0, sm_count=148):
+                 seed=20220701, ln_eps=1e-5, rope_base=10000.0, sm_count=148, int8_act=0):
         self.cfg = Config(hidden, layers, heads, vocab, max_ctx, dtype_bytes, tp, batch, sm_count, seed, ln_eps,
-                          rope_base)
+                          rope_base, int8_act)
         self.batch, self.vocab, self.hidden = batch, vocab, hidden
         self._h = oracle_lib().or_model_create(C.byref(self.cfg))
 

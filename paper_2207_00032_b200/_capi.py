@@ -23,6 +23,8 @@ DT_F32 = 2
 DT_I8 = 3
 DT_F64 = 4
 
+INT8_W8A8 = 0
+INT8_W8A16 = 1
 EPI_NONE = 0
 EPI_GELU = 1
 EPI_RESID = 2
@@ -87,7 +89,7 @@ class GemmArgs(C.Structure):
     _fields_ = [("w_packed", C.c_void_p), ("w_dtype", C.c_int32), ("w_scales", C.c_void_p),
                 ("N", C.c_int64), ("K", C.c_int64), ("B", C.c_int64), ("x", C.c_void_p),
                 ("x_dtype", C.c_int32), ("x_scales", C.c_void_p), ("bias", C.c_void_p), ("out", C.c_void_p),
-                ("out_dtype", C.c_int32), ("epilogue", C.c_int32), ("ksplit", C.c_int32)]
+                ("out_dtype", C.c_int32), ("epilogue", C.c_int32), ("ksplit", C.c_int32), ("int8_act", C.c_int32)]
 
 
 class LbArgs(C.Structure):
@@ -110,7 +112,7 @@ class RuntimeConfig(C.Structure):
     _fields_ = [("batch", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_mode", C.c_int32),
                 ("use_cuda_graph", C.c_int32), ("use_pdl", C.c_int32), ("max_ctx", C.c_int64),
                 ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float), ("device", C.c_int32),
-                ("use_step_kernel", C.c_int32)]
+                ("use_step_kernel", C.c_int32), ("int8_act", C.c_int32)]
 
 
 class ModelInfo(C.Structure):

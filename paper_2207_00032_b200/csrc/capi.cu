@@ -30,6 +30,8 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     require(a.w_scales != nullptr, "I8 weights need w_scales");
     require(a.x_dtype == DSINF_DT_F16 || a.x_dtype == DSINF_DT_I8, "x_dtype must be F16 or I8");
     if (a.x_dtype == DSINF_DT_I8) require(a.x_scales != nullptr, "I8 x needs x_scales");
+    require(a.int8_act == DSINF_INT8_W8A8 || a.int8_act == DSINF_INT8_W8A16, "unknown int8_act");
+    require(a.int8_act != DSINF_INT8_W8A16 || a.x_dtype == DSINF_DT_F16, "W8A16 takes F16 x");
   } else {
     require(a.x_dtype == DSINF_DT_F16, "F16 weights take F16 x");
   }
@@ -38,9 +40,10 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
     const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
     const void* xb = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;
-    const bool ready_x = !i8w || a.x_dtype == DSINF_DT_I8;  // GEMM-ready x (no on-the-fly quantisation)
-    const bool xs = ready_x && gemm::prefer_x_stream(nb) && gemm::x_streamable(xb, K, K, i8w);
-    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs);
+    const bool a16 = i8w && a.int8_act == DSINF_INT8_W8A16;
+    const bool ready_x = !i8w || a16 || a.x_dtype == DSINF_DT_I8;  // GEMM-ready x (no on-the-fly quantisation)
+    const bool xs = ready_x && gemm::prefer_x_stream(nb) && gemm::x_streamable(xb, K, K, i8w && !a16);
+    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs, a16);
     gemm::Params p{};
     p.w_scale = a.w_scales;
     p.N = N;
@@ -50,7 +53,7 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     p.B = nb;
     p.x = xb;
     p.x_ld = K;
-    if (i8w)
+    if (i8w && !a16)
       p.pro = a.x_dtype == DSINF_DT_I8 ? gemm::PRO_I8 : gemm::PRO_QUANT;
     else
       p.pro = gemm::PRO_F16;

@@ -108,6 +108,8 @@ struct dsinf_model {
   int64_t h = 0, L = 0, H = 0, d = 0, Hl = 0, V = 0, Vpad = 0, Vl = 0, F = 0, Fl = 0;
   int B = 0, t = 1, max_ctx = 0;
   bool int8 = false;
+  bool a16 = false;  // int8 weights with fp16 activations (W8A16) in the decode GEMMs
+  bool q8() const { return int8 && !a16; }  // int8 activations (W8A8)
   std::vector<dsinf::DevBuf> allocs;
   std::vector<dsinf::Shard> shards;
   float2* rope = nullptr;
@@ -305,16 +307,16 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   DSINF_CUDA_CHECK(cudaMemsetAsync(sh.d_mlp, 0, B * h * 4, s));
   if (m.fuse_ln) sh.lnstats = m.alloc_n<long long>((2 * m.L + 1) * gemm::kLnSlotWords);
   if (m.xs_ln || m.xs_lm) sh.xn = m.alloc_n<__half>(static_cast<int64_t>(B) * h);
-  if (m.int8 && (m.xs_ln || m.xs_od)) {
+  if (m.q8() && (m.xs_ln || m.xs_od)) {
     sh.xq = m.alloc_n<int8_t>(static_cast<int64_t>(B) * std::max(h, Fl));
     sh.xsc = m.alloc_n<float>(B);
   }
-  if (m.int8) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
-  const bool i8 = m.int8;
-  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln);
-  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od);
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln);
-  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od);
+  if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
+  const bool i8 = m.int8, a16 = m.a16;
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, a16);
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, a16);
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, a16);
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, a16);
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm);
 }
 
@@ -567,7 +569,7 @@ struct Enqueuer {
     if (m.xs_ln) {
       ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l), m.fuse_ln || l == 0 ? nullptr : sh.d_mlp,
            m.fuse_ln || l == 0 ? nullptr : sh.layers[l - 1].bdown, m.fuse_ln ? nullptr : sh.res[1], w.ln1g, w.ln1b,
-           m.int8);
+           m.q8());
     } else {
       p.pro = gemm::PRO_LN;
       p.res_in = sh.res[0];
@@ -617,11 +619,11 @@ struct Enqueuer {
   void k3_attn_out(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wo, w.so, static_cast<int>(m.h), static_cast<int>(m.Hl * m.d), m.int8);
-    p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.pro = m.q8() ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.a;
     p.x_ld = static_cast<int>(m.Hl * m.d);
     p.amax_in = amslot(sh, 2 * l);
-    if (m.xs_od && m.int8) {  // quantise once (row max from attention), then stream int8 x
+    if (m.xs_od && m.q8()) {  // quantise once (row max from attention), then stream int8 x
       prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.a, p.x_ld,
            amslot(sh, 2 * l), p.x_ld, true);
       p.pro = gemm::PRO_I8;
@@ -645,9 +647,9 @@ struct Enqueuer {
     gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
     if (m.xs_ln) {
       if (m.fuse_ln)
-        ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.int8);
+        ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8());
       else
-        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.int8);
+        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.q8());
     } else {
       p.pro = gemm::PRO_LN;
       if (m.fuse_ln) {
@@ -672,11 +674,11 @@ struct Enqueuer {
   void k5_down(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wdown, w.sdown, static_cast<int>(m.h), static_cast<int>(m.Fl), m.int8);
-    p.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.pro = m.q8() ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.u;
     p.x_ld = static_cast<int>(m.Fl);
     p.amax_in = amslot(sh, 2 * l + 1);
-    if (m.xs_od && m.int8) {
+    if (m.xs_od && m.q8()) {
       prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.u, p.x_ld,
            amslot(sh, 2 * l + 1), p.x_ld, true);
       p.pro = gemm::PRO_I8;
@@ -1034,17 +1036,20 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     m->B = rt->batch;
     m->max_ctx = static_cast<int>(rt->max_ctx);
     m->int8 = cfg->dtype_bytes == 1;
+    require(rt->int8_act == DSINF_INT8_W8A8 || rt->int8_act == DSINF_INT8_W8A16, "unknown int8_act");
+    m->a16 = m->int8 && rt->int8_act == DSINF_INT8_W8A16;
+    require(!(m->a16 && rt->use_step_kernel), "the persistent step kernel runs W8A8 only");
     m->attn_chunks = ops::attention_chunks(m->B, static_cast<int>(m->Hl));
     {
       const char* fs = std::getenv("DSINF_FUSE_STATS");
       m->fuse_ln = m->t == 1 && (fs == nullptr || std::atoi(fs) != 0);
       // x-streaming plans need 16-byte rows of GEMM-ready x
       const int64_t Fl = 4 * m->h / m->t, Ol = m->h / m->t;
-      const bool rows16 = m->int8 ? (m->h % 16 == 0 && Fl % 16 == 0 && Ol % 16 == 0) : (Ol % 8 == 0 && Fl % 8 == 0);
+      const bool rows16 = m->q8() ? (m->h % 16 == 0 && Fl % 16 == 0 && Ol % 16 == 0) : (Ol % 8 == 0 && Fl % 8 == 0);
       m->xs_ln = rows16 && gemm::prefer_x_stream(m->B);
       const char* od = std::getenv("DSINF_XS_OD");
       const int od_v = od ? std::atoi(od) : -1;
-      m->xs_od = rows16 && (m->int8 ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
+      m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
       const char* lm = std::getenv("DSINF_XS_LM");
       m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
     }

@@ -40,12 +40,16 @@ using dev::Header;
 //   [ring: stages x 16 KB] [header 1 KB] [x slice: B rows x x_row_words words]
 // After the main loop the ring is reused for the split-K partials part[b][n].
 // kXS (x-streaming, large batch): stages are 18 KB (weights + the x box), no x slice.
-template <bool kInt8, int kNB8, bool kXS>
+// kA16 (int8 weights only): W8A16 -- x stays fp16 (slice of fp16 pairs, or two x boxes per
+// 128-k stage when streamed), weights widened in registers, fp32 accumulate, y = acc * w_scale.
+template <bool kInt8, int kNB8, bool kXS, bool kA16>
 __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
+  static_assert(!kA16 || kInt8, "W8A16 needs int8 weights");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
-  constexpr int kSB = kXS ? kStageBytesXS : kStageBytes;
+  constexpr int kSB = kXS ? (kA16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes;
+  constexpr int kXBoxes = kA16 ? 2 : 1;  // x boxes per streamed stage
   uint8_t* ring = smem;
   Header& hd = *reinterpret_cast<Header*>(smem + stages * kSB);
   uint32_t* sx = reinterpret_cast<uint32_t*>(smem + stages * kSB + kHeaderBytes);
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       // weights of the first `stages` stages before the dependency, their x boxes after it
       const uint64_t policy = ptx::policy_evict_first();
       const uint64_t xpolicy = ptx::policy_evict_last();  // x is re-read by every column tile
-      const uint32_t tx = kStageBytes + p.B * 128;
+      const uint32_t tx = kStageBytes + kXBoxes * p.B * 128;
       const int pre = min(stages, n_iters);
       for (int it = 0; it < pre; ++it) {
         ptx::mbar_arrive_expect_tx(&hd.full[it], tx);
@@ -101,8 +105,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       }
       ptx::pdl_wait();
       for (int it = 0; it < pre; ++it)
-        ptx::tma_load_2d(ring + it * kSB + kStageBytes, &p.xmap, row_begin + it * kRowsPerStage, 0, &hd.full[it],
-                         xpolicy);
+#pragma unroll
+        for (int xb = 0; xb < kXBoxes; ++xb)
+          ptx::tma_load_2d(ring + it * kSB + kStageBytes + xb * kXBoxBytes, &p.xmap,
+                           kXBoxes * (row_begin + it * kRowsPerStage) + xb * kRowsPerStage, 0, &hd.full[it], xpolicy);
       int s = pre % stages;
       uint32_t phase = pre == stages ? 1u : 0u;
       for (int it = pre; it < n_iters; ++it) {
@@ -113,7 +119,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w)
           ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
-        ptx::tma_load_2d(dst + kStageBytes, &p.xmap, r0, 0, &hd.full[s], xpolicy);
+#pragma unroll
+        for (int xb = 0; xb < kXBoxes; ++xb)
+          ptx::tma_load_2d(dst + kStageBytes + xb * kXBoxBytes, &p.xmap, kXBoxes * r0 + xb * kRowsPerStage, 0,
+                           &hd.full[s], xpolicy);
         if (++s == stages) {
           s = 0;
           phase ^= 1;
@@ -158,7 +167,15 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 #endif
     if (clog && threadIdx.x == 32) clog[2] = ptx::gtimer();
     if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
-      if (kInt8 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
+      if (kInt8 && !kA16 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
+    } else if (kA16) {  // fp16 x slice, in units of fp16 pairs: twice the packed int8 rows
+      if (p.pro == PRO_LN && p.ln_stats_in != nullptr) {
+        dev::fill_x_ln_f16_pre(p, sx, hd, 2 * row_begin, 2 * p.rows_per_split, ctid, c_rel);
+      } else {
+        if (p.pro == PRO_LN) dev::ln_row_stats<false>(p, hd, ctid, cw, lane, p.res_out != nullptr && tile == 0 && split == 0);
+        dev::consumer_bar();
+        dev::fill_x_slice<false>(p, sx, hd, 2 * row_begin, 2 * p.rows_per_split, ctid);
+      }
     } else if (!kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr) {
       dev::fill_x_ln_f16_pre(p, sx, hd, row_begin, p.rows_per_split, ctid, c_rel);
     } else if (kInt8 && p.pro == PRO_LN && p.ln_stats_in != nullptr && dev::ln_i8_fits(p.B, p.K)) {
@@ -182,22 +199,41 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 #endif
     if (clog && threadIdx.x == 32) clog[3] = ptx::gtimer();
 
-    dev::Consumer<kInt8, kNB8> c;
+    dev::Consumer<kInt8, kNB8, kA16> c;
     c.init(lane);
     c.zero();
     int s = 0;
     uint32_t phase = 0;
-    if constexpr (kXS)
+    if constexpr (kA16) {
+      const int g = lane >> 2, t = lane & 3;
+      if constexpr (kXS) {  // x word pair 2 * (4 kk + t) of batch row r in the stage's two boxes
+        c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int st, int, int kk, int bt) {
+          const int r = bt * 8 + g;
+          if (r >= p.B) return make_uint2(0u, 0u);
+          const int w = 8 * kk + 2 * t, ww = w & 31;
+          const uint8_t* xb = ring + st * kSB + kStageBytes + (w >> 5) * kXBoxBytes;
+          return *reinterpret_cast<const uint2*>(xb + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) + (ww & 3) * 4);
+        });
+      } else {
+        const int xrw = p.x_row_words;
+        c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int, int it, int kk, int bt) {
+          const int r = bt * 8 + g;
+          if (r >= p.B) return make_uint2(0u, 0u);
+          return *reinterpret_cast<const uint2*>(sx + r * xrw + it * 2 * kRowsPerStage + 8 * kk + 2 * t);
+        });
+      }
+    } else if constexpr (kXS) {
       c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane);
-    else
+    } else {
       c.run(ring, hd, stages, s, phase, n_iters, sx, p.x_row_words, p.B, cw, lane);
+    }
 #ifdef DSINF_DIAG
     ptx::trace_phase_max(p.trace, 4, 32);
 #endif
     if (clog && threadIdx.x == 32) clog[4] = ptx::gtimer();
     ptx::pdl_trigger();
     dev::consumer_bar();  // every consumer is done reading the ring
-    c.store(reinterpret_cast<typename dev::Consumer<kInt8, kNB8>::Acc*>(ring), kPartLd, p.B, cw);
+    c.store(reinterpret_cast<typename dev::Consumer<kInt8, kNB8, kA16>::Acc*>(ring), kPartLd, p.B, cw);
   }
 
   // ================= split-K reduction across the cluster (DSMEM) + epilogue
@@ -234,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
       // the ranks' partials in batches of 4 DSMEM loads in flight, summed in rank order
       float y0, y1;
-      if constexpr (kInt8) {
+      if constexpr (kInt8 && !kA16) {
         int s0 = 0, s1 = 0;
         for (int r0 = 0; r0 < nsplit; r0 += 4) {
           uint2 v[4];
@@ -265,6 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         }
         y0 = acc2.x;
         y1 = acc2.y;
+        if constexpr (kA16) {  // weight-only dequant: per output row scale
+          y0 = __fmul_rn(y0, ws.x);
+          y1 = has1 ? __fmul_rn(y1, ws.y) : 0.f;
+        }
       }
       dev::epilogue_pair(p, b, n, y0, y1, has1, &st, p.epi == EPI_RESID ? &rin : nullptr);
       if (p.am_out != nullptr) {
@@ -290,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (clog && threadIdx.x == 0) clog[5] = ptx::gtimer();
 }
 
-template <bool kInt8, int kNB8, bool kXS>
+template <bool kInt8, int kNB8, bool kXS, bool kA16 = false>
 void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pdl) {
-  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS>;
+  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(plan.col_tiles, plan.ksplit, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -315,9 +355,9 @@ void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pd
   DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
 }
 
-template <bool kInt8, int kNB8, bool kXS>
+template <bool kInt8, int kNB8, bool kXS, bool kA16 = false>
 void configure_one() {
-  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS>;
+  auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
@@ -342,27 +382,33 @@ int env_int(const char* name, int dflt) {
 }
 
 // Co-resident clusters of `split` CTAs for this kernel / smem (cached; 0 when unknown).
-const void* kernel_ptr(bool int8_weights, int nb8, bool xs) {
-  if (int8_weights) {
-    if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, true>)
-                            : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, true>);
-    return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, false>)
-                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, false>);
+const void* kernel_ptr(bool int8_weights, int nb8, bool xs, bool a16) {
+  if (a16) {
+    if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, true, true>)
+                            : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, true, true>);
+    return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, false, true>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, false, true>);
   }
-  if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, true>)
-                          : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, true>);
-  return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, false>)
-                  : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, false>);
+  if (int8_weights) {
+    if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, true, false>)
+                            : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, true, false>);
+    return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, false, false>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, false, false>);
+  }
+  if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, true, false>)
+                          : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, true, false>);
+  return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, false, false>)
+                  : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, false, false>);
 }
 
-int resident_clusters(bool int8_weights, int nb8, bool xs, int split, size_t smem) {
+int resident_clusters(bool int8_weights, int nb8, bool xs, bool a16, int split, size_t smem) {
   static std::mutex mu;
-  static std::map<std::tuple<bool, int, bool, int, size_t>, int> cache;
-  const auto key = std::make_tuple(int8_weights, nb8, xs, split, smem);
+  static std::map<std::tuple<bool, int, bool, bool, int, size_t>, int> cache;
+  const auto key = std::make_tuple(int8_weights, nb8, xs, a16, split, smem);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const void* kern = kernel_ptr(int8_weights, nb8, xs);
+  const void* kern = kernel_ptr(int8_weights, nb8, xs, a16);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, split, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -407,6 +453,10 @@ void configure() {
   configure_one<false, 2, true>();
   configure_one<true, 1, true>();
   configure_one<true, 2, true>();
+  configure_one<true, 1, false, true>();
+  configure_one<true, 2, false, true>();
+  configure_one<true, 1, true, true>();
+  configure_one<true, 2, true, true>();
 }
 
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words) {
@@ -438,22 +488,25 @@ bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
 // splits K only when the output tiles alone cannot occupy the machine, but it sizes the split
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream) {
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
+  if (a16 && !int8_weights) throw ConfigError("sbi_gemm: W8A16 needs int8 weights");
   const int m = int8_weights ? 4 : 2;
   const int rows = (K + m - 1) / m;
+  const int xw = a16 ? 2 : 1;  // x-slice words per packed row
   Plan pl{};
   pl.x_stream = x_stream ? 1 : 0;
+  pl.a16 = a16 ? 1 : 0;
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
   const size_t x_budget = 64 * 1024;
-  const size_t stage_bytes = x_stream ? kStageBytesXS : kStageBytes;
+  const size_t stage_bytes = x_stream ? (a16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes;
   auto rps_for = [&](int s) {
     int r = (rows + s - 1) / s;
     return (r + kRowsPerStage - 1) / kRowsPerStage * kRowsPerStage;
   };
   // smem x slice of the non-streaming mode (the streaming mode keeps x in the ring stages)
-  auto x_bytes = [&](int rps) { return x_stream ? size_t{0} : static_cast<size_t>(B) * (rps + 8) * 4; };
+  auto x_bytes = [&](int rps) { return x_stream ? size_t{0} : static_cast<size_t>(B) * (xw * rps + 8) * 4; };
   auto valid = [&](int s) {
     const int rps = rps_for(s);
     if ((rows + rps - 1) / rps != s) return false;  // no empty split
@@ -484,7 +537,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
     for (int s = 1; s <= 16; s <<= 1) {
       if (!valid(s)) continue;
       const int units = pl.col_tiles * s;
-      const int clusters = resident_clusters(int8_weights, pl.nb8, x_stream, s, smem_for(s, nullptr));
+      const int clusters = resident_clusters(int8_weights, pl.nb8, x_stream, a16, s, smem_for(s, nullptr));
       int capacity = clusters > 0 ? clusters * s : 2 * 148;
       if (cap_per_sm > 0) capacity = std::min(capacity, cap_per_sm * 148);  // leave room for PDL overlap
       if (units <= capacity && units > best_units) {
@@ -507,31 +560,41 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   Params p = p_in;
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
-  p.x_row_words = plan.rows_per_split + 8;
+  p.a16 = plan.a16;
+  p.x_row_words = (plan.a16 ? 2 : 1) * plan.rows_per_split + 8;
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
   if (p.am_out != nullptr && (p.epi != EPI_F32 || p.bias != nullptr))
     throw ConfigError("sbi_gemm: the fused argmax needs the plain fp32 epilogue without bias");
   const bool xs = plan.x_stream != 0;
+  const bool i8x = int8_weights && !plan.a16;  // int8 activations
+  if (plan.a16 && p.pro != PRO_F16 && p.pro != PRO_LN) throw ConfigError("sbi_gemm: W8A16 takes fp16 x (PRO_F16 / PRO_LN)");
   if (xs) {
-    if (p.pro != (int8_weights ? PRO_I8 : PRO_F16))
-      throw ConfigError("sbi_gemm: the x-streaming plan needs GEMM-ready x (fp16 for fp16 weights, int8 for int8)");
-    if (!x_streamable(p.x, p.x_ld, p.K, int8_weights)) throw ConfigError("sbi_gemm: x cannot be streamed (alignment)");
-    make_x_map(&p.xmap, p.x, p.rows, p.B, p.x_ld / (int8_weights ? 4 : 2));
+    if (p.pro != (i8x ? PRO_I8 : PRO_F16))
+      throw ConfigError("sbi_gemm: the x-streaming plan needs GEMM-ready x (fp16, or int8 for W8A8)");
+    if (!x_streamable(p.x, p.x_ld, p.K, i8x)) throw ConfigError("sbi_gemm: x cannot be streamed (alignment)");
+    // words: W8A8 int8 quads (= packed rows); fp16 pairs otherwise (W8A16: 2 per packed row)
+    make_x_map(&p.xmap, p.x, plan.a16 ? 2 * p.rows : p.rows, p.B, p.x_ld / (i8x ? 4 : 2));
   }
-#define DSINF_LAUNCH(I8, NB, XS) launch_impl<I8, NB, XS>(p, plan, stream, pdl)
-  if (int8_weights) {
+#define DSINF_LAUNCH(I8, NB, XS, A16) launch_impl<I8, NB, XS, A16>(p, plan, stream, pdl)
+  if (plan.a16) {
     if (plan.nb8 == 1) {
-      if (xs) DSINF_LAUNCH(true, 1, true); else DSINF_LAUNCH(true, 1, false);
+      if (xs) DSINF_LAUNCH(true, 1, true, true); else DSINF_LAUNCH(true, 1, false, true);
     } else {
-      if (xs) DSINF_LAUNCH(true, 2, true); else DSINF_LAUNCH(true, 2, false);
+      if (xs) DSINF_LAUNCH(true, 2, true, true); else DSINF_LAUNCH(true, 2, false, true);
+    }
+  } else if (int8_weights) {
+    if (plan.nb8 == 1) {
+      if (xs) DSINF_LAUNCH(true, 1, true, false); else DSINF_LAUNCH(true, 1, false, false);
+    } else {
+      if (xs) DSINF_LAUNCH(true, 2, true, false); else DSINF_LAUNCH(true, 2, false, false);
     }
   } else {
     if (plan.nb8 == 1) {
-      if (xs) DSINF_LAUNCH(false, 1, true); else DSINF_LAUNCH(false, 1, false);
+      if (xs) DSINF_LAUNCH(false, 1, true, false); else DSINF_LAUNCH(false, 1, false, false);
     } else {
-      if (xs) DSINF_LAUNCH(false, 2, true); else DSINF_LAUNCH(false, 2, false);
+      if (xs) DSINF_LAUNCH(false, 2, true, false); else DSINF_LAUNCH(false, 2, false, false);
     }
   }
 #undef DSINF_LAUNCH

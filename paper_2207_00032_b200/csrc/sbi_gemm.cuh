@@ -27,6 +27,8 @@ constexpr int kHeaderBytes = 1024;                         // barriers + per-row
 // x-streaming mode (large batch): each stage also carries the B x 32-word x tile by TMA
 constexpr int kXBoxBytes = kMaxB * 128;                    // 2 KB (B rows x 128 B, 128B swizzle)
 constexpr int kStageBytesXS = kStageBytes + kXBoxBytes;    // 18 KB, multiple of 1024
+// W8A16 x-streaming: int8 weight stages cover 128 k, i.e. two 32-word boxes of fp16 x pairs
+constexpr int kStageBytesXS16 = kStageBytes + 2 * kXBoxBytes;  // 20 KB
 
 // Row statistics handed from a producing epilogue to the next kernel's prologue (TP = 1 path):
 //   LayerNorm: per row, sum(y) and sum(y*y) in fixed point (int64; y * 2^32 and y^2 * 2^28,
@@ -79,6 +81,7 @@ struct Params {
   int x_row_words;       // smem stride of one x row (== 8 mod 32)
   // prologue
   int pro;
+  int a16;               // int8 weights with fp16 x (W8A16, weight-only): fp32 accumulate, y = acc * w_scale
   const void* x;
   int x_ld;
   const float* x_scale;
@@ -117,6 +120,7 @@ struct Params {
 
 struct Plan {
   int x_stream;  // 1: x streamed per stage by TMA (PRO_F16 / PRO_I8 only), no smem x slice
+  int a16;       // W8A16 plan (int8 weights, fp16 x)
   int col_tiles;
   int ksplit;
   int rows_per_split;
@@ -130,7 +134,7 @@ struct Plan {
 void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 // Sets kernel attributes for every instantiation; call before graph capture.
 void configure();
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false);
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false, bool a16 = false);
 // TMA descriptor of x for the x-streaming mode: `words` 32-bit words per row, `B` rows, row
 // stride ld_words (ld_words * 4 must be a multiple of 16 and x 16-byte aligned).
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words);

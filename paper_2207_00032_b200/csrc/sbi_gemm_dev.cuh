@@ -541,16 +541,33 @@ __device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, in
   }
 }
 
+// int8 x4 (one packed weight word: 4 consecutive k) -> two fp16 pairs, exact:
+// bytes (s + 128) under a 0x64 exponent byte are 1024 + s + 128 in fp16; subtract 1152.
+__device__ __forceinline__ void i8x4_to_h2x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const uint32_t u = w ^ 0x80808080u;
+  const uint32_t l = __byte_perm(u, 0x64646464u, 0x4140);
+  const uint32_t h = __byte_perm(u, 0x64646464u, 0x4342);
+  const __half2 bias = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
+  const __half2 lf = __hsub2(*reinterpret_cast<const __half2*>(&l), bias);
+  const __half2 hf = __hsub2(*reinterpret_cast<const __half2*>(&h), bias);
+  lo = *reinterpret_cast<const uint32_t*>(&lf);
+  hi = *reinterpret_cast<const uint32_t*>(&hf);
+}
+
 // ------------------------------------------------------------------ consumer loop
 // Accumulates `n_iters` ring stages into acc[j][bt][*] (warp `cw` owns 32 output columns).
 // The ring position (s, phase) persists across calls.  Inside a k-step of 8 packed rows the MMA
 // k-slot t reads smem row 2t (t+4 reads 2t+1), a k permutation applied to both operands that
 // keeps every fragment read conflict-free under the 128-byte TMA swizzle.
-template <bool kInt8, int kNB8>
+// kA16 (with kInt8): W8A16 -- the int8 weight words are widened to fp16 pairs in registers and
+// multiplied by fp16 x with mma.m16n8k16 (fp32 accumulate).  Per 16-k step thread t owns packed
+// row 4*kk + t (4 consecutive k): weight word -> (a0, a2) / (a1, a3), x word pair 2*(4kk + t)
+// -> (b0, b1), the same k assignment on both operands.
+template <bool kInt8, int kNB8, bool kA16 = false>
 struct Consumer {
-  using Acc = typename std::conditional<kInt8, int, float>::type;
+  using Acc = typename std::conditional<kInt8 && !kA16, int, float>::type;
   Acc acc[2][kNB8][4];
-  uint32_t aoff[2][2][2];  // [j][h][par]
+  uint32_t aoff[2][2][2];  // [j][h][par]  (kA16: par = parity of the 16-k step)
   int g, t;
 
   __device__ __forceinline__ void init(int lane) {
@@ -562,10 +579,42 @@ struct Consumer {
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int par = 0; par < 2; ++par) {
-          const int r = 2 * t + par;
+          const int r = kA16 ? 4 * par + t : 2 * t + par;
           const int c = 16 * j + 8 * h + g;
           aoff[j][h][par] = r * 128 + (((c >> 2) ^ r) << 4) + (c & 3) * 4;
         }
+  }
+  // W8A16 main loop; xword(it, kk, bt) returns the (b0, b1) x words of batch tile bt.
+  template <class XWord>
+  __device__ __forceinline__ void run_a16(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
+                                          uint32_t& phase, int n_iters, int cw, int lane, XWord xword) {
+    const uint8_t* wbox = ring + cw * kBoxBytes;
+    for (int it = 0; it < n_iters; ++it) {
+      ptx::mbar_wait(&hd.full[s], phase);
+      const uint8_t* sw = wbox + s * stage_bytes;
+#pragma unroll
+      for (int kk = 0; kk < kRowsPerStage / 4; ++kk) {
+        uint2 bx[kNB8];
+#pragma unroll
+        for (int bt = 0; bt < kNB8; ++bt) bx[bt] = xword(s, it, kk, bt);
+        const uint8_t* a = sw + (kk >> 1) * 8 * 128;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t a0, a1, a2, a3;
+          i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][0][kk & 1]), a0, a2);
+          i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][1][kk & 1]), a1, a3);
+#pragma unroll
+          for (int bt = 0; bt < kNB8; ++bt)
+            if constexpr (kA16) ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, bx[bt].x, bx[bt].y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
+      if (++s == stages) {
+        s = 0;
+        phase ^= 1;
+      }
+    }
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -608,7 +657,7 @@ struct Consumer {
           const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt) {
-            if constexpr (kInt8)
+            if constexpr (kInt8 && !kA16)
               ptx::mma_s8(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
             else
               ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
@@ -661,7 +710,7 @@ struct Consumer {
           const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt) {
-            if constexpr (kInt8)
+            if constexpr (kInt8 && !kA16)
               ptx::mma_s8(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);
             else
               ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, b0[bt], b1[bt]);

@@ -61,10 +61,10 @@ class DecoderModel:
                  dtype_bytes: int = 2, batch: int = 1, max_ctx: int = 256, tp_size: int = 1, tp_rank: int = 0,
                  tp_mode: int = capi.TP_NONE, nccl_comm: Optional[int] = None, use_cuda_graph: bool = True,
                  use_pdl: bool = True, use_step_kernel: bool = False, seed: int = 20220701, ln_eps: float = 1e-5, rope_base: float = 10000.0,
-                 device: int = 0):
+                 device: int = 0, int8_act: int = capi.INT8_W8A8):
         self.cfg = capi.ModelConfig(hidden, layers, heads, vocab, max_seq, dtype_bytes)
         self.rt = capi.RuntimeConfig(batch, tp_size, tp_rank, tp_mode, int(use_cuda_graph), int(use_pdl), max_ctx,
-                                     seed, ln_eps, rope_base, device, int(use_step_kernel))
+                                     seed, ln_eps, rope_base, device, int(use_step_kernel), int(int8_act))
         self.batch, self.vocab, self.max_ctx = batch, vocab, max_ctx
         self.hidden, self.layers, self.heads = hidden, layers, heads
         self._h = C.c_void_p()
@@ -171,7 +171,7 @@ class DecoderModel:
 # ---------------------------------------------------------------- device operators on torch tensors
 
 def gemm(w_packed, x, N: int, K: int, *, w_scales=None, x_scales=None, bias=None, out=None, out_dtype=None,
-         gelu: bool = False, ksplit: int = 0, stream=None):
+         gelu: bool = False, ksplit: int = 0, a16: bool = False, stream=None):
     """SBI-GeMM: out[B][N] = x[B][K] . W^T over the reference packed layout.
 
     w_packed: fp16 tensor [ceil(K/2)*2*N] (pack_M = 2) or int8 [ceil(K/4)*4*N] (pack_M = 4)."""
@@ -193,6 +193,7 @@ def gemm(w_packed, x, N: int, K: int, *, w_scales=None, x_scales=None, bias=None
     a.out_dtype = capi.DT_F32 if out.dtype == torch.float32 else capi.DT_F16
     a.epilogue = capi.EPI_GELU if gelu else capi.EPI_NONE
     a.ksplit = ksplit
+    a.int8_act = capi.INT8_W8A16 if a16 else capi.INT8_W8A8
     capi.check(capi.lib.dsinf_gemm(C.byref(a), _stream_ptr(stream)))
     return out
 

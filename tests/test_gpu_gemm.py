@@ -114,3 +114,35 @@ def test_exec_device_matches_exec_reference():
     out = I.exec_device(packed, x, B, sch).reshape(B, N)
     # small integers: fp16 exact, fp32 accumulation exact -> identical to the fp64 reference
     assert np.array_equal(out, x @ W.T)
+
+
+@pytest.mark.parametrize("N,K,B", [(4096, 4096, 1), (12288, 4096, 1), (4096, 16384, 1), (1024, 2048, 3),
+                                   (4096, 4096, 8), (16384, 4096, 16), (640, 320, 5)])
+def test_int8_weight_only_w8a16(N, K, B):
+    """W8A16: int8 weights (per-row scale) x fp16 activations, fp32 accumulation -- within
+    2e-3 * sum|q x| * s + 1e-3 of the exact product (both the smem-slice and the streamed-x plans)."""
+    rng = np.random.default_rng(N + K + B)
+    W = (rng.standard_normal((N, K)) * 0.05).astype(np.float16)
+    x = rng.standard_normal((B, K)).astype(np.float16)
+    dev = torch.device("cuda")
+    wq, ws = E.quantize_weights_int8(torch.from_numpy(W).to(dev))
+    out = E.gemm(wq, torch.from_numpy(x).to(dev), N, K, w_scales=ws, a16=True).cpu().numpy()
+    q_rm, s_rm = O.quant_rows(W.astype(np.float32))
+    ref = (x.astype(np.float64) @ q_rm.astype(np.float64).T) * s_rm.astype(np.float64)
+    bound = (np.abs(x.astype(np.float64)) @ np.abs(q_rm.astype(np.float64)).T) * s_rm.astype(np.float64)
+    err = np.abs(out - ref)
+    assert np.all(err <= 2e-3 * bound + 1e-3), float((err / (bound + 1e-9)).max())
+
+
+@pytest.mark.parametrize("ksplit", [1, 2, 4, 8, 16])
+def test_int8_w8a16_every_split_agrees(ksplit):
+    rng = np.random.default_rng(21)
+    N, K, B = 512, 4096, 2
+    W = (rng.standard_normal((N, K)) * 0.05).astype(np.float16)
+    x = rng.standard_normal((B, K)).astype(np.float16)
+    dev = torch.device("cuda")
+    wq, ws = E.quantize_weights_int8(torch.from_numpy(W).to(dev))
+    out = E.gemm(wq, torch.from_numpy(x).to(dev), N, K, w_scales=ws, a16=True, ksplit=ksplit).cpu().numpy()
+    q_rm, s_rm = O.quant_rows(W.astype(np.float32))
+    ref = (x.astype(np.float64) @ q_rm.astype(np.float64).T) * s_rm.astype(np.float64)
+    assert np.allclose(out, ref, rtol=2e-3, atol=2e-2)

@@ -22,16 +22,16 @@ SEED = 20220701
 
 
 def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, prompt_len=6, gen=4,
-               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=True):
+               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=True, int8_act=0):
     tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
     rng = np.random.default_rng(hidden + layers + batch)
     prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
     mode = capi.TP_LOCAL if tp > 1 else capi.TP_NONE
     gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx,
                        tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED,
-                       use_step_kernel=step_kernel)
+                       use_step_kernel=step_kernel, int8_act=int8_act)
     ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=batch, max_ctx=max_ctx,
-                        seed=SEED)
+                        seed=SEED, int8_act=int8_act)
     gpu.set_prompt(prompt)
     worst = 0.0
     margins = []
@@ -252,3 +252,13 @@ def test_prefill_rejects_bad_state():
     with pytest.raises(capi.ConfigError):
         gpu.prefill()  # not at position 0
     gpu.close()
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8, 16])
+def test_int8_weight_only_model_matches_oracle(batch):
+    """W8A16 decode (int8 weights, fp16 activations) against the oracle's W8A16 mode."""
+    run_parity(256, 2, 4, 1000, batch=batch, dtype_bytes=1, int8_act=1, step_kernel=False)
+
+
+def test_int8_weight_only_gptj_width_layer():
+    run_parity(4096, 1, 32, 2000, batch=1, dtype_bytes=1, int8_act=1, step_kernel=False, prompt_len=4, gen=3)

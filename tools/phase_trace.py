@@ -20,7 +20,8 @@ cfg = args[0] if len(args) > 0 else "gptj-6b"
 dt = args[1] if len(args) > 1 else "fp16"
 B = int(args[2]) if len(args) > 2 else 1
 p = PRESETS[cfg]
-m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt == "int8" else 2, batch=B, max_ctx=192)
+m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt in ("int8", "w8a16") else 2, batch=B, max_ctx=192,
+                 int8_act=1 if dt == "w8a16" else 0)
 m.set_prompt(np.random.default_rng(0).integers(0, p.vocab, (B, 128)).astype(np.int32))
 m.step(128)
 tr = m.launch_trace(8).astype(np.float64)  # [steps][n][6]
