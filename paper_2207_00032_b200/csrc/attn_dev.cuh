@@ -68,19 +68,26 @@ __device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1,
   float m = -INFINITY, l = 0.f, o[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = 0.f;
-  for (int r0 = 0; r0 < rounds; r0 += kAttnUnroll) {  // warp-uniform trip count
-    uint4 kr[kAttnUnroll], vr[kAttnUnroll];
+  // software-pipelined: the K/V rows of batch r0 + kAttnUnroll are requested before batch r0 is
+  // consumed, so two batches of loads are in flight (the loop is latency-bound, not bandwidth-bound)
+  uint4 kr[kAttnUnroll], vr[kAttnUnroll];
+  auto load_batch = [&](int r0, uint4 (&kk)[kAttnUnroll], uint4 (&vv)[kAttnUnroll]) {
 #pragma unroll
     for (int u = 0; u < kAttnUnroll; ++u) {
       const int j = j0 + (r0 + u) * PPR + slot;
-      if (j < j1 && has_dims) {
-        kr[u] = __ldcg(reinterpret_cast<const uint4*>(kb + static_cast<size_t>(j) * d));
-        vr[u] = __ldcg(reinterpret_cast<const uint4*>(vb + static_cast<size_t>(j) * d));
+      if (r0 < rounds && j < j1 && has_dims) {
+        kk[u] = __ldcg(reinterpret_cast<const uint4*>(kb + static_cast<size_t>(j) * d));
+        vv[u] = __ldcg(reinterpret_cast<const uint4*>(vb + static_cast<size_t>(j) * d));
       } else {
-        kr[u] = make_uint4(0, 0, 0, 0);
-        vr[u] = make_uint4(0, 0, 0, 0);
+        kk[u] = make_uint4(0, 0, 0, 0);
+        vv[u] = make_uint4(0, 0, 0, 0);
       }
     }
+  };
+  load_batch(0, kr, vr);
+  for (int r0 = 0; r0 < rounds; r0 += kAttnUnroll) {  // warp-uniform trip count
+    uint4 kn[kAttnUnroll], vn[kAttnUnroll];
+    load_batch(r0 + kAttnUnroll, kn, vn);
 #pragma unroll
     for (int u = 0; u < kAttnUnroll; ++u) {
       float kf[8];
@@ -102,6 +109,11 @@ __device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1,
         for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i] * corr);
         m = mn;
       }
+    }
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      kr[u] = kn[u];
+      vr[u] = vn[u];
     }
   }
   if (has_dims) {

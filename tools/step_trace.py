@@ -20,7 +20,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "gptj-6b"
 dt = sys.argv[2] if len(sys.argv) > 2 else "fp16"
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 p = PRESETS[cfg]
-m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt == "int8" else 2, batch=B, max_ctx=160)
+m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt == "int8" else 2, batch=B, max_ctx=160, use_step_kernel=True)
 m.set_prompt(np.random.default_rng(0).integers(0, p.vocab, (B, 128)).astype(np.int32))
 m.step(130)
 torch.cuda.synchronize()
