@@ -71,6 +71,7 @@ struct PrefillBufs {
   __half* q = nullptr;     // [M][Hl*d]
   __half* a = nullptr;     // [M][Hl*d] attention output
   __half* u = nullptr;     // [M][F/t] GeLU output
+  float* part = nullptr;   // TP > 1: [M][h] row-parallel partial (all-reduced in place)
 };
 
 struct Shard {
@@ -360,6 +361,7 @@ void ensure_prefill_bufs(Model& m, Shard& sh, int64_t M) {
   pf.q = m.alloc_n<__half>(M * Hd);
   pf.a = m.alloc_n<__half>(M * Hd);
   pf.u = m.alloc_n<__half>(M * Fl);
+  if (m.t > 1) pf.part = m.alloc_n<float>(M * h);
   pf.cap = M;
 }
 
@@ -697,17 +699,20 @@ struct Enqueuer {
     gemm_launch(p, sh.plan_down, m.int8, 4);
   }
 
-  void lm_head(Shard& sh) {
+  // complete_res: res[0] already holds the final residual (prefill); else the decode step's last
+  // MLP-down partial and bias are folded in here when the statistics are not fused (TP > 1).
+  void lm_head(Shard& sh, bool complete_res = false) {
     gemm::Params p = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), static_cast<int>(m.h), false);
+    const bool fold = !m.fuse_ln && !complete_res && m.L > 0;
     if (m.xs_lm) {
-      ln_x(sh, p, sh.res[0], lnslot(sh, 2 * static_cast<int>(m.L)), m.fuse_ln || m.L == 0 ? nullptr : sh.d_mlp,
-           m.fuse_ln || m.L == 0 ? nullptr : sh.layers[m.L - 1].bdown, nullptr, sh.lnfg, sh.lnfb, false);
+      ln_x(sh, p, sh.res[0], m.fuse_ln ? lnslot(sh, 2 * static_cast<int>(m.L)) : nullptr, fold ? sh.d_mlp : nullptr,
+           fold ? sh.layers[m.L - 1].bdown : nullptr, nullptr, sh.lnfg, sh.lnfb, false);
     } else {
       p.pro = gemm::PRO_LN;
       p.res_in = sh.res[0];
       if (m.fuse_ln) {
         p.ln_stats_in = lnslot(sh, 2 * static_cast<int>(m.L));
-      } else {
+      } else if (fold) {
         p.res_delta = m.L > 0 ? sh.d_mlp : nullptr;
         p.delta_bias = m.L > 0 ? sh.layers[m.L - 1].bdown : nullptr;
       }
@@ -745,131 +750,170 @@ struct Enqueuer {
   // Prompt prefill (large-batch regime, TP = 1): every layer over all B x P prompt tokens with
   // the tcgen05 GEMMs, then the decode path's LM head / argmax / select on the last token.
   void prefill(int P) {
-    Shard& sh = m.shards[0];
-    PrefillBufs& pf = sh.pf;
     const int M = m.B * P;
     const int h = static_cast<int>(m.h), Hd = static_cast<int>(m.Hl * m.d), Fl = static_cast<int>(m.Fl);
     const bool i8 = m.int8;
     const int eb = i8 ? 1 : 2;
-    ops::PrefillEmbedParams pe{};
-    pe.wte = sh.wte;
-    pe.prompt = m.prompt;
-    pe.prompt_ld = m.prompt_cap;
-    pe.P = P;
-    pe.hist = m.hist;
-    pe.max_ctx = m.max_ctx;
-    pe.res = pf.res;
-    pe.B = m.B;
-    pe.h = h;
-    pe.V = static_cast<int>(m.V);
-    ops::prefill_embed(pe, s);
-    ++launches;
-    auto ln = [&](const __half* g, const __half* b) {  // LayerNorm rows -> GEMM-ready x
+    const bool tp = m.t > 1;  // row-parallel GEMMs produce partials: all-reduce, then residual add
+    for (Shard& sh : m.shards) {
+      ops::PrefillEmbedParams pe{};
+      pe.wte = sh.wte;
+      pe.prompt = m.prompt;
+      pe.prompt_ld = m.prompt_cap;
+      pe.P = P;
+      pe.hist = m.hist;
+      pe.max_ctx = m.max_ctx;
+      pe.res = sh.pf.res;
+      pe.B = m.B;
+      pe.h = h;
+      pe.V = static_cast<int>(m.V);
+      ops::prefill_embed(pe, s);
+      ++launches;
+    }
+    auto ln = [&](Shard& sh, const __half* g, const __half* b) {  // LayerNorm rows -> GEMM-ready x
       ops::PrepParams pp{};
       pp.mode = i8 ? ops::PREP_LN_I8 : ops::PREP_LN_F16;
-      pp.res = pf.res;
+      pp.res = sh.pf.res;
       pp.ln_g = g;
       pp.ln_b = b;
       pp.eps = m.rt.ln_eps;
-      pp.out = i8 ? static_cast<void*>(pf.xq) : static_cast<void*>(pf.xn);
-      pp.out_scale = pf.xs;
+      pp.out = i8 ? static_cast<void*>(sh.pf.xq) : static_cast<void*>(sh.pf.xn);
+      pp.out_scale = sh.pf.xs;
       pp.B = M;
       pp.K = h;
       ops::row_prep(pp, s, false);
       ++launches;
     };
-    auto quant = [&](const __half* x, int K) {  // int8: per-row quantisation of an fp16 activation
+    auto quant = [&](Shard& sh, const __half* x, int K) {  // int8: per-row quantisation of an fp16 activation
       ops::PrepParams pp{};
       pp.mode = ops::PREP_QUANT_I8;
       pp.x = x;
       pp.x_ld = K;
-      pp.out = pf.xq;
-      pp.out_scale = pf.xs;
+      pp.out = sh.pf.xq;
+      pp.out_scale = sh.pf.xs;
       pp.B = M;
       pp.K = K;
       ops::row_prep(pp, s, false);
       ++launches;
     };
-    auto gemm = [&](tc::Params& p, const void* x, const void* w, const float* ws, int N, int K) {
+    auto gemm = [&](Shard& sh, tc::Params& p, const void* x, const void* w, const float* ws, int N, int K) {
       p.M = M;
       p.N = N;
       p.K = K;
       tc::make_maps(p, x, K * eb, w, K * eb, eb);
-      p.x_scale = pf.xs;
+      p.x_scale = sh.pf.xs;
       p.w_scale = ws;
       tc::launch(p, i8, s);
       ++launches;
     };
+    // row-parallel output: t == 1 -> residual += y + bias in the epilogue; t > 1 -> partial, all-reduce,
+    // then residual += (sum + bias) (the decode path's order)
+    auto row_parallel = [&](Shard& sh, tc::Params& p, const __half* bias) {
+      if (tp) {
+        p.epi = tc::EPI_F32;
+        p.out = sh.pf.part;
+      } else {
+        p.epi = tc::EPI_RESID;
+        p.bias = bias;
+        p.out = sh.pf.res;
+      }
+      p.out_ld = h;
+    };
+    auto reduce_add = [&](auto bias_of) {
+      if (!tp) return;
+      const int64_t count = static_cast<int64_t>(M) * h;
+      if (m.rt.tp_mode == DSINF_TP_NCCL) {
+        nccl::allreduce_sum_f32(m.shards[0].pf.part, count, m.comm, s);
+      } else {
+        ops::LocalReduceParams lr{};
+        lr.shards = m.t;
+        lr.count = count;
+        for (int i = 0; i < m.t; ++i) lr.buf[i] = m.shards[i].pf.part;
+        ops::local_allreduce(lr, s, false);
+        ++launches;
+      }
+      for (Shard& sh : m.shards) {
+        ops::prefill_residual_add(sh.pf.res, sh.pf.part, bias_of(sh), count, h, s);
+        ++launches;
+      }
+    };
     const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
     for (int l = 0; l < m.L; ++l) {
-      const LayerW& w = sh.layers[l];
-      ln(w.ln1g, w.ln1b);
-      tc::Params q{};
-      q.epi = tc::EPI_QKV;
-      q.bias = w.bqkv;
-      q.q_out = pf.q;
-      q.k_cache = sh.kc + l * layer_kv;
-      q.v_cache = sh.vc + l * layer_kv;
-      q.rope = m.rope;
-      q.seq_len = P;
-      q.pos0 = 0;
-      q.heads = static_cast<int>(m.Hl);
-      q.head_dim = static_cast<int>(m.d);
-      q.max_seq = m.max_ctx;
-      gemm(q, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rqkv, w.sqkv, 3 * Hd, h);
-      ops::PrefillAttnParams a{};
-      a.q = pf.q;
-      a.kc = q.k_cache;
-      a.vc = q.v_cache;
-      a.out = pf.a;
-      a.B = m.B;
-      a.P = P;
-      a.H = static_cast<int>(m.Hl);
-      a.d = static_cast<int>(m.d);
-      a.max_seq = m.max_ctx;
-      a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
-      ops::prefill_attention(a, s);
-      ++launches;
-      if (i8) quant(pf.a, Hd);
-      tc::Params o{};
-      o.epi = tc::EPI_RESID;
-      o.bias = w.bo;
-      o.out = pf.res;
-      o.out_ld = h;
-      gemm(o, i8 ? static_cast<const void*>(pf.xq) : pf.a, w.ro, w.so, h, Hd);
-      ln(w.ln2g, w.ln2b);
-      tc::Params u{};
-      u.epi = tc::EPI_GELU_F16;
-      u.bias = w.bup;
-      u.out = pf.u;
-      u.out_ld = Fl;
-      gemm(u, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rup, w.sup, Fl, h);
-      if (i8) quant(pf.u, Fl);
-      tc::Params dn{};
-      dn.epi = tc::EPI_RESID;
-      dn.bias = w.bdown;
-      dn.out = pf.res;
-      dn.out_ld = h;
-      gemm(dn, i8 ? static_cast<const void*>(pf.xq) : pf.u, w.rdown, w.sdown, h, Fl);
+      for (Shard& sh : m.shards) {
+        const LayerW& w = sh.layers[l];
+        PrefillBufs& pf = sh.pf;
+        ln(sh, w.ln1g, w.ln1b);
+        tc::Params q{};
+        q.epi = tc::EPI_QKV;
+        q.bias = w.bqkv;
+        q.q_out = pf.q;
+        q.k_cache = sh.kc + l * layer_kv;
+        q.v_cache = sh.vc + l * layer_kv;
+        q.rope = m.rope;
+        q.seq_len = P;
+        q.pos0 = 0;
+        q.heads = static_cast<int>(m.Hl);
+        q.head_dim = static_cast<int>(m.d);
+        q.max_seq = m.max_ctx;
+        gemm(sh, q, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rqkv, w.sqkv, 3 * Hd, h);
+        ops::PrefillAttnParams a{};
+        a.q = pf.q;
+        a.kc = q.k_cache;
+        a.vc = q.v_cache;
+        a.out = pf.a;
+        a.B = m.B;
+        a.P = P;
+        a.H = static_cast<int>(m.Hl);
+        a.d = static_cast<int>(m.d);
+        a.max_seq = m.max_ctx;
+        a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+        ops::prefill_attention(a, s);
+        ++launches;
+        if (i8) quant(sh, pf.a, Hd);
+        tc::Params o{};
+        row_parallel(sh, o, w.bo);
+        gemm(sh, o, i8 ? static_cast<const void*>(pf.xq) : pf.a, w.ro, w.so, h, Hd);
+      }
+      reduce_add([&](Shard& sh) { return sh.layers[l].bo; });
+      for (Shard& sh : m.shards) {
+        const LayerW& w = sh.layers[l];
+        PrefillBufs& pf = sh.pf;
+        ln(sh, w.ln2g, w.ln2b);
+        tc::Params u{};
+        u.epi = tc::EPI_GELU_F16;
+        u.bias = w.bup;
+        u.out = pf.u;
+        u.out_ld = Fl;
+        gemm(sh, u, i8 ? static_cast<const void*>(pf.xq) : pf.xn, w.rup, w.sup, Fl, h);
+        if (i8) quant(sh, pf.u, Fl);
+        tc::Params dn{};
+        row_parallel(sh, dn, w.bdown);
+        gemm(sh, dn, i8 ? static_cast<const void*>(pf.xq) : pf.u, w.rdown, w.sdown, h, Fl);
+      }
+      reduce_add([&](Shard& sh) { return sh.layers[l].bdown; });
     }
-    // last prompt token of every sequence -> the decode state, then LM head / argmax / select
-    long long* lslot = lnslot(sh, 2 * static_cast<int>(m.L));
-    DSINF_CUDA_CHECK(cudaMemsetAsync(lslot, 0, gemm::kLnSlotWords * sizeof(long long), s));
-    ops::PrefillGatherParams g{};
-    g.res_rows = pf.res;
-    g.P = P;
-    g.res = sh.res[0];
-    g.ln_stats = lslot;
-    g.pos = m.pos;
-    g.B = m.B;
-    g.h = h;
-    ops::prefill_gather(g, s);
-    ++launches;
-    DSINF_CUDA_CHECK(cudaMemsetAsync(m.am_key, 0, sizeof(unsigned long long) * m.B, s));
-    lm_head(sh);
+    // last prompt token of every sequence -> the decode state, then LM head (+ fused argmax) / select
+    DSINF_CUDA_CHECK(cudaMemsetAsync(m.am_key, 0, sizeof(unsigned long long) * m.t * m.B, s));
+    for (Shard& sh : m.shards) {
+      long long* lslot = lnslot(sh, 2 * static_cast<int>(m.L));
+      if (lslot) DSINF_CUDA_CHECK(cudaMemsetAsync(lslot, 0, gemm::kLnSlotWords * sizeof(long long), s));
+      ops::PrefillGatherParams g{};
+      g.res_rows = sh.pf.res;
+      g.P = P;
+      g.res = sh.res[0];
+      g.ln_stats = lslot;
+      g.pos = m.pos;
+      g.B = m.B;
+      g.h = h;
+      ops::prefill_gather(g, s);
+      ++launches;
+      lm_head(sh, /*complete_res=*/true);
+    }
+    if (m.t > 1 && m.rt.tp_mode == DSINF_TP_NCCL)
+      nccl::allgather_bytes(m.am_key + m.shards[0].rank * m.B, m.am_key, m.B * sizeof(unsigned long long), m.comm, s);
     ops::SelectParams sp{};
     sp.keys = m.am_key;
-    sp.shards = 1;
+    sp.shards = m.t;
     sp.B = m.B;
     sp.next_tok = m.next_tok;
     sp.pos = m.pos;
@@ -1132,15 +1176,16 @@ int dsinf_model_prefill(dsinf_model* m, void* stream) {
     require(m != nullptr, "null model");
     require(m->prompt_len >= 1, "prefill needs a prompt (dsinf_model_set_prompt)");
     require(m->host_pos == 0, "prefill must start at position 0 (call dsinf_model_set_prompt first)");
-    require(m->t == 1 && m->fuse_ln, "prefill runs at tp_size 1 with fused LayerNorm statistics");
     require(m->d % 32 == 0 && m->d <= 256, "prefill attention needs head_dim % 32 == 0 and <= 256");
-    require(m->h % 16 == 0 && (4 * m->h) % 16 == 0, "prefill needs hidden_dim % 16 == 0 (16-byte TMA rows)");
+    require(m->h % 16 == 0 && (m->Hl * m->d) % 16 == 0 && m->Fl % 16 == 0,
+            "prefill needs 16-byte TMA rows (hidden, per-rank head and MLP widths % 16 == 0)");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Shard& sh = m->shards[0];
     tc::configure();
     ops::configure_prefill();
-    if (!sh.rm_ready) build_rowmajor(*m, sh, s);
-    ensure_prefill_bufs(*m, sh, static_cast<int64_t>(m->B) * m->prompt_len);
+    for (Shard& sh : m->shards) {
+      if (!sh.rm_ready) build_rowmajor(*m, sh, s);
+      ensure_prefill_bufs(*m, sh, static_cast<int64_t>(m->B) * m->prompt_len);
+    }
     Enqueuer e{*m, s, m->rt.use_pdl != 0};
     e.prefill(m->prompt_len);
     m->host_pos = m->prompt_len;

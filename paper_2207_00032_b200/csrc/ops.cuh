@@ -160,6 +160,8 @@ struct PrefillGatherParams {
   int B, h;
 };
 void prefill_gather(const PrefillGatherParams& p, cudaStream_t s);
+// TP > 1: res[i] += part[i] + bias[i % h] (the all-reduced row-parallel output, bias added once).
+void prefill_residual_add(float* res, const float* part, const __half* bias, int64_t count, int h, cudaStream_t s);
 
 // Sum of `n` shard buffers (in shard order), written back to every shard buffer.
 struct LocalReduceParams {

@@ -4,6 +4,7 @@
 // prompt would (KV cache rows 0..P-1, history, next token, pos = P).
 #include <cfloat>
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.h"
@@ -334,13 +335,27 @@ __global__ void prefill_gather_kernel(const __grid_constant__ PrefillGatherParam
       a += red[0][w];
       c += red[1][w];
     }
-    p.ln_stats[b * 2] = a;  // stripe 0 of the slot
-    p.ln_stats[b * 2 + 1] = c;
+    if (p.ln_stats != nullptr) {  // stripe 0 of the slot (fused-statistics mode)
+      p.ln_stats[b * 2] = a;
+      p.ln_stats[b * 2 + 1] = c;
+    }
     if (b == 0) *p.pos = p.P - 1;
   }
 }
 
+__global__ void prefill_residual_add_kernel(float* res, const float* part, const __half* bias, int64_t count, int h) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    res[i] = __fadd_rn(res[i], __fadd_rn(part[i], __half2float(bias[i % h])));
+}
+
 }  // namespace
+
+void prefill_residual_add(float* res, const float* part, const __half* bias, int64_t count, int h, cudaStream_t s) {
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 16);
+  prefill_residual_add_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(res, part, bias, count, h);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
 
 void prefill_embed(const PrefillEmbedParams& p, cudaStream_t s) {
   if (p.h % 8 != 0) throw ConfigError("prefill: hidden_dim must be a multiple of 8");

@@ -165,14 +165,17 @@ def test_tp_local_x_stream(monkeypatch, dtype_bytes):
     run_parity(512, 2, 8, 1000, tp=2, batch=4, dtype_bytes=dtype_bytes, step_kernel=False)
 
 
-def run_prefill_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, prompt_len=40, gen=3, max_ctx=64):
+def run_prefill_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, prompt_len=40, gen=3, max_ctx=64,
+                       tp=1):
     """Prefill (tcgen05 large-batch path) vs the oracle stepping through the prompt token by token;
     then `gen` decode steps from the prefilled KV cache.  Same tolerances as run_parity."""
     tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
     rng = np.random.default_rng(hidden * 3 + layers + batch + prompt_len)
     prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
-    gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED)
-    ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED)
+    gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED,
+                       tp_size=tp, tp_mode=capi.TP_LOCAL if tp > 1 else capi.TP_NONE)
+    ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx, seed=SEED,
+                        tp=tp)
     gpu.set_prompt(prompt)
     gpu.prefill()
     torch.cuda.synchronize()
@@ -262,3 +265,11 @@ def test_int8_weight_only_model_matches_oracle(batch):
 
 def test_int8_weight_only_gptj_width_layer():
     run_parity(4096, 1, 32, 2000, batch=1, dtype_bytes=1, int8_act=1, step_kernel=False, prompt_len=4, gen=3)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+@pytest.mark.parametrize("tp", [2, 4])
+def test_prefill_tensor_parallel_matches_oracle(dtype_bytes, tp):
+    """Prefill with Megatron TP (column-parallel QKV / up, row-parallel attn-out / down with an
+    all-reduce of the [M][h] partials, vocab-parallel LM head) on one device, vs the TP-aware oracle."""
+    run_prefill_parity(512, 2, 8, 1000, batch=2, dtype_bytes=dtype_bytes, prompt_len=48, max_ctx=56, tp=tp)
