@@ -247,11 +247,17 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   const int pairs = cols_per_rank / 2;
   const uint8_t* part_base = ring;
   const bool want_stats = p.ln_stats_out != nullptr || p.amax_out != nullptr;
-  // one warp per batch row (lanes over column pairs) so row statistics reduce with shuffles
-  for (int b = warp; b < p.B; b += kThreads / 32) {
+  // lane groups of gp = min(32, pow2 >= pairs) lanes per batch row (lanes over column pairs), so
+  // a warp covers 32 / gp rows at once and the row statistics reduce with in-group shuffles
+  const int gp = pairs >= 32 ? 32 : dev::next_pow2(pairs);
+  const int rpw = 32 / gp;                      // rows per warp per pass
+  const int rows_per_pass = rpw * (kThreads / 32);
+  for (int b0 = 0; b0 < p.B; b0 += rows_per_pass) {
+    const int b = b0 + warp * rpw + lane / gp;  // this lane's row (may be >= B: shuffles only)
+    const bool brow = b < p.B;
     dev::RowStat st;
     unsigned long long best = 0;  // fused argmax (p.am_out)
-    for (int q = lane; q < pairs; q += 32) {
+    for (int q = lane & (gp - 1); brow && q < pairs; q += gp) {
       const int c = c_begin + 2 * q;
       const int n = n0 + c;
       if (n >= p.N) continue;
@@ -313,11 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       }
     }
     if (p.am_out != nullptr) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if (lane == 0 && best != 0) atomicMax(p.am_out + b, best);
+      for (int o = gp >> 1; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (brow && (lane & (gp - 1)) == 0 && best != 0) atomicMax(p.am_out + b, best);
     }
-    if (want_stats) dev::row_stat_commit(st, es, b, lane);
+    if (want_stats) dev::row_stat_commit_group(st, es, brow ? b : 0, lane, gp, brow);
   }
   if (want_stats) {
     __syncthreads();

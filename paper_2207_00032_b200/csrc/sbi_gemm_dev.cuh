@@ -790,6 +790,21 @@ __device__ __forceinline__ void row_stat_commit(RowStat st, EpiStats& es, int b,
   }
 }
 
+// Same for a group of `gp` lanes (power of two, aligned) holding row b: the group leader stores.
+__device__ __forceinline__ void row_stat_commit_group(RowStat st, EpiStats& es, int b, int lane, int gp, bool valid) {
+  unsigned m = __float_as_uint(st.amax);
+  for (int o = gp >> 1; o > 0; o >>= 1) {
+    st.s1 += __shfl_xor_sync(0xffffffffu, st.s1, o);
+    st.s2 += __shfl_xor_sync(0xffffffffu, st.s2, o);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if (valid && (lane & (gp - 1)) == 0) {
+    es.esum[b][0] = static_cast<unsigned long long>(st.s1);
+    es.esum[b][1] = static_cast<unsigned long long>(st.s2);
+    es.emax[b] = m;
+  }
+}
+
 // One CTA's epilogue statistics -> the global stripes (after a block-wide barrier).
 __device__ __forceinline__ void stats_flush(const Params& p, const EpiStats& es, int stripe) {
   if (p.ln_stats_out != nullptr && threadIdx.x < 2 * p.B) {
