@@ -95,6 +95,11 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* map, int c
       "l"(map), "r"(c0), "r"(c1), "r"(ptx::smem_u32(bar)), "h"(mask), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ uint4 ld_dsmem_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
 // 32 lanes x 32 columns of 32-bit: thread t of the warp gets lane (base + t), columns [col, col + 32).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -338,6 +343,146 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 1) tmem_dealloc(tmem, 2 * kBN);
 }
 
+// Split-K mode for one row tile (M <= 128, the B = 1 prompt): the weights must stream at HBM rate,
+// so a 128-column tile is split over a cluster of `split` CTAs along K; each accumulates its K range
+// in TMEM, stages the partial tile in its (drained) ring smem, and after a cluster barrier rank r
+// sums the ranks' partials for column chunks r, r + split, ... through DSMEM (rank order) and runs
+// the fused epilogue on them.
+template <bool kInt8>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSStages * kSStageBytes);
+  uint64_t* empty = full + kSStages;
+  uint64_t* acc_ready = empty + kSStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.split;
+  const int rank = static_cast<int>(ptx::cluster_ctarank());
+  const int n0 = static_cast<int>(blockIdx.x / S) * kSBN;
+  const int kps = (p.k_blocks + S - 1) / S;
+  const int kb0 = rank * kps, kb1 = min(p.k_blocks, kb0 + kps);
+  const int nk = max(0, kb1 - kb0);
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tensormap(&p.amap);
+    ptx::prefetch_tensormap(&p.bmap);
+    for (int st = 0; st < kSStages; ++st) {
+      ptx::mbar_init(&full[st], 1);
+      ptx::mbar_init(&empty[st], 1);
+    }
+    ptx::mbar_init(acc_ready, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kSBN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::pdl_wait();
+      const uint64_t pol_a = ptx::policy_evict_last();
+      const uint64_t pol_b = ptx::policy_evict_first();  // each weight byte is read once
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % kSStages;
+        ptx::mbar_wait(&empty[st], ((i / kSStages) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[st], kSStageBytes);
+        uint8_t* sa = smem + st * kSStageBytes;
+        ptx::tma_load_2d(sa, &p.amap, (kb0 + i) * kBK, 0, &full[st], pol_a);
+        ptx::tma_load_2d(sa + kABytes, &p.bmap, (kb0 + i) * kBK, n0, &full[st], pol_b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // instruction descriptor with N = 128
+      constexpr uint32_t idesc = (instr_desc<kInt8>() & ~(0x3fu << 17)) | (static_cast<uint32_t>(kSBN >> 3) << 17);
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % kSStages;
+        ptx::mbar_wait(&full[st], (i / kSStages) & 1);
+        tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(smem + st * kSStageBytes);
+        const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 32; ++k)
+          mma<kInt8>(tmem, da + static_cast<uint64_t>(k * 2), db + static_cast<uint64_t>(k * 2), idesc,
+                     (i | k) != 0 ? 1u : 0u);
+        mma_commit(&empty[st]);
+      }
+      mma_commit(acc_ready);
+    }
+  }
+  // partial tile -> own smem (the ring is drained once every MMA has completed)
+  uint32_t* part = reinterpret_cast<uint32_t*>(smem);
+  const int quarter = warp & 3;
+  const int row = quarter * 32 + lane;  // epilogue warps 2..5: TMEM lane quarter = warp % 4
+  if (warp >= 2) {
+    if (nk > 0) {
+      ptx::mbar_wait(acc_ready, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < kSBN / 32; ++c) {
+      uint32_t v[32];
+      if (nk > 0) {
+        tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c * 32, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<uint4*>(part + row * kSPartLd + c * 32 + j) = make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  }
+  tc_fence_before();
+  ptx::cluster_sync();  // every rank's partial tile is in its smem
+  if (warp >= 2 && row < p.M) {
+    for (int c = rank; c < kSBN / 32; c += S) {
+      if (n0 + c * 32 >= p.N) break;
+      uint32_t v[32];
+      if constexpr (kInt8) {
+        int acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0;
+        for (int r = 0; r < S; ++r) {
+          const uint32_t base = ptx::map_shared_rank(part + row * kSPartLd + c * 32, r);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const uint4 u = ld_dsmem_u4(base + j * 4);
+            acc[j] += static_cast<int>(u.x);
+            acc[j + 1] += static_cast<int>(u.y);
+            acc[j + 2] += static_cast<int>(u.z);
+            acc[j + 3] += static_cast<int>(u.w);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = static_cast<uint32_t>(acc[j]);
+      } else {
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int r = 0; r < S; ++r) {  // rank order: deterministic
+          const uint32_t base = ptx::map_shared_rank(part + row * kSPartLd + c * 32, r);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const uint4 u = ld_dsmem_u4(base + j * 4);
+            acc[j] += __uint_as_float(u.x);
+            acc[j + 1] += __uint_as_float(u.y);
+            acc[j + 2] += __uint_as_float(u.z);
+            acc[j + 3] += __uint_as_float(u.w);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc[j]);
+      }
+      epilogue32<kInt8>(p, row, n0 + c * 32, v);
+    }
+  }
+  if (warp >= 2) ptx::pdl_trigger();
+  ptx::cluster_sync_relaxed();  // peers are done reading our partials
+  if (warp == 1) tmem_dealloc(tmem, kSBN);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -367,13 +512,25 @@ void byte_map(CUtensorMap* map, const void* base, int rows, int row_bytes, int l
 
 }  // namespace
 
+int sm_count();
+
 void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld_bytes, int elem_bytes) {
   if (p.M < 1 || p.N < 1 || p.K < 1) throw ConfigError("tc_gemm: gemm shape dims must be positive");
   const int kbytes = p.K * elem_bytes;
-  byte_map(&p.amap, x, p.M, kbytes, x_ld_bytes, kBM);
-  p.pair = ((p.M + kBM - 1) / kBM) >= 2 && !std::getenv("DSINF_TC_NOPAIR");
-  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, p.pair ? kBN / 2 : kBN);
   p.k_blocks = (kbytes + kBK - 1) / kBK;
+  byte_map(&p.amap, x, p.M, kbytes, x_ld_bytes, kBM);
+  const int m_tiles = (p.M + kBM - 1) / kBM;
+  p.pair = m_tiles >= 2 && !std::getenv("DSINF_TC_NOPAIR");
+  // one row tile: split K over a cluster so that ~2 CTAs per SM stream the weights
+  p.split = 1;
+  if (m_tiles == 1 && !std::getenv("DSINF_TC_NOSPLIT")) {
+    const int n128 = (p.N + kSBN - 1) / kSBN;
+    // measured: clusters of up to 4 keep two CTAs per SM co-resident; 8-CTA clusters and second
+    // waves are slower
+    while (p.split < 4 && n128 * (2 * p.split) <= 2 * sm_count() && p.k_blocks >= 4 * (2 * p.split)) p.split *= 2;
+    if (const char* v = std::getenv("DSINF_TC_SPLIT")) p.split = std::max(1, std::min(8, std::atoi(v)));
+  }
+  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, (p.pair || p.split > 1) ? 128 : kBN);
 }
 
 void configure() {
@@ -381,6 +538,10 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmemBytes));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 int sm_count() {
@@ -395,6 +556,26 @@ int sm_count() {
 
 void launch(const Params& p, bool int8, cudaStream_t s) {
   const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.N + kBN - 1) / kBN;
+  if (p.split > 1) {
+    const int n128 = (p.N + kSBN - 1) / kSBN;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n128 * p.split);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = p.split;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if (int8)
+      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<true>, p));
+    else
+      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<false>, p));
+    return;
+  }
   if (p.pair) {
     const int units = (m_tiles + 1) / 2 * n_tiles;
     const int ctas = 2 * std::min(units, sm_count() / 2);

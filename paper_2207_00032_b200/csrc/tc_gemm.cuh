@@ -28,6 +28,11 @@ constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 192;        // warp 0 TMA, warp 1 MMA issue + TMEM owner, warps 2..5 epilogue
 constexpr int kEpiThreads = 128;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+// split-K mode (small M): 128 x 128 tiles, 3 stages of 32 KB, two CTAs per SM
+constexpr int kSBN = 128, kSStages = 3;
+constexpr int kSStageBytes = kABytes + kSBN * kBK;
+constexpr int kSPartLd = kSBN + 4;  // fp32 / int32 partial row stride (floats)
+constexpr int kSSmemBytes = kSStages * kSStageBytes + 1024 + 256;
 
 enum Epi : int {
   EPI_F32 = 0,       // out fp32 = y (+ bias)
@@ -43,6 +48,8 @@ struct Params {
   int M, N, K;
   int k_blocks;                  // ceil(K * elem / 128)
   int pair;                      // cluster-pair mode (set by make_maps: >= 2 row tiles)
+  int split;                     // > 1: split-K mode for one row tile (M <= 128): 128-column tiles, a cluster of
+                                 // `split` CTAs per tile reduces its partials through DSMEM
   const float* x_scale;          // int8: [M]
   const float* w_scale;          // int8: [N]
   const __half* bias;            // optional [N]
