@@ -88,27 +88,39 @@ __device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1,
   for (int r0 = 0; r0 < rounds; r0 += kAttnUnroll) {  // warp-uniform trip count
     uint4 kn[kAttnUnroll], vn[kAttnUnroll];
     load_batch(r0 + kAttnUnroll, kn, vn);
+    // scores of the batch's kAttnUnroll positions, then ONE online-softmax rescale per batch
+    float sc[kAttnUnroll];
+    float mt = -INFINITY;
 #pragma unroll
     for (int u = 0; u < kAttnUnroll; ++u) {
       float kf[8];
       h8_to_f(kr[u], kf);
-      float s = 0.f;
+      float sdot = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s = fmaf(q[i], kf[i], s);
+      for (int i = 0; i < 8; ++i) sdot = fmaf(q[i], kf[i], sdot);
 #pragma unroll
-      for (int off = TPP / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      for (int off = TPP / 2; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
       const int j = j0 + (r0 + u) * PPR + slot;
-      if (j < j1) {
-        const float mn = fmaxf(m, s);
-        const float corr = expf(m - mn);
-        const float pj = expf(s - mn);
+      sc[u] = j < j1 ? sdot : -INFINITY;
+      mt = fmaxf(mt, sc[u]);
+    }
+    if (mt != -INFINITY) {
+      const float mn = fmaxf(m, mt);
+      const float corr = expf(m - mn);
+      l *= corr;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] *= corr;
+#pragma unroll
+      for (int u = 0; u < kAttnUnroll; ++u) {
+        if (sc[u] == -INFINITY) continue;
+        const float pj = expf(sc[u] - mn);
         float vf[8];
         h8_to_f(vr[u], vf);
-        l = l * corr + pj;
+        l += pj;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i] * corr);
-        m = mn;
+        for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i]);
       }
+      m = mn;
     }
 #pragma unroll
     for (int u = 0; u < kAttnUnroll; ++u) {
