@@ -308,7 +308,10 @@ __global__ void select_kernel(const __grid_constant__ SelectParams p) {
     if (pos + 1 < p.max_ctx) p.hist[static_cast<size_t>(b) * p.max_ctx + pos + 1] = bx;
   }
   __syncthreads();
-  if (threadIdx.x == 0) *p.pos = pos + 1;
+  if (threadIdx.x == 0) {
+    *p.pos = pos + 1;
+    if (p.step_ctr) *p.step_ctr += 1;
+  }
 }
 
 // ---------------------------------------------------------------- row preparation (x streaming)
@@ -363,6 +366,10 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
   // LayerNorm of the residual row (same expression as the fused GEMM prologue, so both plans
   // produce identical x); statistics from the producer or summed here in the same fixed point
   const size_t rb = static_cast<size_t>(b) * p.K;
+  if (p.red_flag != nullptr) {  // fused all-reduce: every rank's partial has landed
+    if (threadIdx.x == 0) ptx::wait_flag(p.red_flag, p.step_ctr, p.red_per_step);
+    __syncthreads();
+  }
   float4 v[kPrepVec];
   long long s1 = 0, s2 = 0;
 #pragma unroll
@@ -373,6 +380,13 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
       v[u] = __ldcg(reinterpret_cast<const float4*>(p.res + rb) + c);
       if (p.res_delta) {
         float4 t = __ldcg(reinterpret_cast<const float4*>(p.res_delta + rb) + c);
+        for (int q = 1; q < p.delta_slots; ++q) {
+          const float4 u = __ldcg(reinterpret_cast<const float4*>(p.res_delta + q * p.delta_stride + rb) + c);
+          t.x = __fadd_rn(t.x, u.x);
+          t.y = __fadd_rn(t.y, u.y);
+          t.z = __fadd_rn(t.z, u.z);
+          t.w = __fadd_rn(t.w, u.w);
+        }
         if (p.delta_bias) {
           const __half2 d01 = *reinterpret_cast<const __half2*>(p.delta_bias + 4 * c);
           const __half2 d23 = *reinterpret_cast<const __half2*>(p.delta_bias + 4 * c + 2);

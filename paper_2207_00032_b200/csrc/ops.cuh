@@ -70,6 +70,11 @@ struct PrepParams {
   const float* res;            // LN: residual [B][K] fp32
   const float* res_delta;      // LN, optional: residual = res + (res_delta + delta_bias) ...
   const __half* delta_bias;
+  int delta_slots;             // fused all-reduce: res_delta = rank-order sum of this many partials
+  long long delta_stride;      //   `delta_stride` floats apart, readable once red_flag reaches
+  const unsigned long long* red_flag;  //   (*step_ctr + 1) * red_per_step
+  const long long* step_ctr;
+  unsigned long long red_per_step;
   float* res_out;              // ... stored here (this kernel is the row's only writer)
   const long long* ln_stats;   // LN: fixed-point row sums (gemm::kLnSlotWords layout), or null:
                                // computed here with the same fixed-point scheme
@@ -114,6 +119,7 @@ struct ArgmaxParams {
 void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl);
 
 struct SelectParams {
+  long long* step_ctr;   // optional: decode-step counter (+1 per step; fused all-reduce flags)
   const float* vals;     // [shards][B] (row stride B)
   const int32_t* idxs;   // [shards][B]
   const unsigned long long* keys;  // or: packed (logit, index) keys [shards][B] (gemm::argmax_key)

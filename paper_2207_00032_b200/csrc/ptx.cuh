@@ -149,6 +149,19 @@ __device__ __forceinline__ float ld_dsmem_f(uint32_t addr) {
   return v;
 }
 
+// ---------------------------------------------------------------- cross-GPU flags (fused all-reduce)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin (one thread) until *flag >= (*step + 1) * per_step.
+__device__ __forceinline__ void wait_flag(const unsigned long long* flag, const long long* step,
+                                          unsigned long long per_step) {
+  const unsigned long long target = (static_cast<unsigned long long>(*reinterpret_cast<const volatile long long*>(step)) + 1ull) * per_step;
+  while (ld_acquire_sys(flag) < target) __nanosleep(32);
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

@@ -166,6 +166,10 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     constexpr long long c_rel = 0;
 #endif
     if (clog && threadIdx.x == 32) clog[2] = ptx::gtimer();
+    if (p.red_flag != nullptr) {  // fused all-reduce: every rank's partial has landed
+      if (ctid == 0) ptx::wait_flag(p.red_flag, p.step_ctr, p.red_per_step);
+      dev::consumer_bar();
+    }
     if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
       if (kInt8 && !kA16 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
     } else if (kA16) {  // fp16 x slice, in units of fp16 pairs: twice the packed int8 rows
@@ -312,6 +316,16 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           y1 = has1 ? __fmul_rn(y1, ws.y) : 0.f;
         }
       }
+      if (p.push_n > 0) {  // fused all-reduce: this rank's partial into every rank's slot
+        const size_t o = static_cast<size_t>(b) * p.out_ld + n;
+        for (int q = 0; q < p.push_n; ++q) {
+          if (has1)
+            *reinterpret_cast<float2*>(p.push_dst[q] + o) = make_float2(y0, y1);
+          else
+            p.push_dst[q][o] = y0;
+        }
+        continue;
+      }
       dev::epilogue_pair(p, b, n, y0, y1, has1, &st, p.epi == EPI_RESID ? &rin : nullptr);
       if (p.am_out != nullptr) {
         if (n < p.am_valid) best = max(best, argmax_key(y0, p.am_offset + n));
@@ -327,6 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (want_stats) {
     __syncthreads();
     dev::stats_flush(p, es, (tile + split) % kStatStripes);
+  }
+  if (p.push_n > 0) {  // publish the pushed partials: one system-scope release per destination rank
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < p.push_n; ++q) atomicAdd_system(p.push_flag[q], 1ull);
+    }
   }
   // keep our smem alive until the peers' DSMEM reads are done (their values are consumed before
   // they arrive, so no release ordering -- and no GPU-scope fence over our epilogue stores -- needed)
@@ -570,6 +591,8 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
   if (p.pro == PRO_LN && (p.K % 8) != 0) throw ConfigError("LayerNorm prologue needs K % 8 == 0");
+  if (p.push_n > 0 && (p.epi != EPI_F32 || p.bias != nullptr || p.push_n > 8 || (p.out_ld % 2) != 0))
+    throw ConfigError("sbi_gemm: the fused all-reduce pushes the plain fp32 partial (no bias)");
   if (p.am_out != nullptr && (p.epi != EPI_F32 || p.bias != nullptr))
     throw ConfigError("sbi_gemm: the fused argmax needs the plain fp32 epilogue without bias");
   const bool xs = plan.x_stream != 0;

@@ -88,6 +88,14 @@ struct Params {
   const float* res_in;
   const float* res_delta;
   const __half* delta_bias;
+  // fused tensor-parallel all-reduce (consumer side): res_delta holds `delta_slots` partials
+  // `delta_stride` floats apart (one per rank, summed in rank order); red_flag must reach
+  // (*step_ctr + 1) * red_per_step before they are read (0 slots = plain res_delta)
+  int delta_slots;
+  long long delta_stride;
+  const unsigned long long* red_flag;
+  const long long* step_ctr;
+  unsigned long long red_per_step;
   float* res_out;
   const __half* ln_g;
   const __half* ln_b;
@@ -108,6 +116,11 @@ struct Params {
   int heads, head_dim, max_seq;
   long long* ln_stats_out;  // EPI_RESID: accumulate the new residual's row sums (slot, zeroed per step)
   unsigned* amax_out;       // EPI_F16 / EPI_GELU_F16: accumulate row max |out|
+  // fused all-reduce (producer side, EPI_F32): the partial [B][N] goes to push_dst[q] (rank q's slot
+  // for this rank) for q < push_n, then each CTA adds 1 to every push_flag[q] (system scope)
+  int push_n;
+  float* push_dst[8];
+  unsigned long long* push_flag[8];
   // EPI_F32 without bias (LM head): greedy argmax fused into the epilogue -- per row the max of
   // pack(value, global column) over columns < am_valid, atomicMax'd into am_out[b] (zeroed per
   // step); ties resolve to the lowest column (moe.hpp:69-74).

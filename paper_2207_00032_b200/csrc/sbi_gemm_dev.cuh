@@ -93,16 +93,26 @@ __device__ __forceinline__ float act_scale(float maxabs) {
   return maxabs > 0.0f ? __fdiv_rn(maxabs, 127.0f) : 1.0f;
 }
 
-// Residual-stream element: r + (delta + delta_bias)  (delta optional).
+// Residual-stream element: r + (delta + delta_bias)  (delta optional; with `nd` > 1 slots the
+// delta is the rank-order sum of the fused all-reduce's partials).
 struct ResidualView {
   const float* r;
   const float* d;
   const __half* db;
   int K;
+  int nd = 1;
+  long long ds = 0;
   __device__ __forceinline__ float4 load4(int b, int k) const {
     float4 v = __ldcg(reinterpret_cast<const float4*>(r + static_cast<size_t>(b) * K + k));
     if (d) {
       float4 t = __ldcg(reinterpret_cast<const float4*>(d + static_cast<size_t>(b) * K + k));
+      for (int q = 1; q < nd; ++q) {
+        const float4 u = __ldcg(reinterpret_cast<const float4*>(d + q * ds + static_cast<size_t>(b) * K + k));
+        t.x = __fadd_rn(t.x, u.x);
+        t.y = __fadd_rn(t.y, u.y);
+        t.z = __fadd_rn(t.z, u.z);
+        t.w = __fadd_rn(t.w, u.w);
+      }
       if (db) {
         const __half2 b01 = *reinterpret_cast<const __half2*>(db + k);
         const __half2 b23 = *reinterpret_cast<const __half2*>(db + k + 2);
@@ -119,6 +129,12 @@ struct ResidualView {
     return v;
   }
 };
+__device__ __forceinline__ ResidualView residual_view(const Params& p) {
+  ResidualView rv{p.res_in, p.res_delta, p.delta_bias, p.K};
+  rv.nd = p.delta_slots > 0 ? p.delta_slots : 1;
+  rv.ds = p.delta_stride;
+  return rv;
+}
 
 __device__ __forceinline__ float ln_apply(float v, float mean, float rstd, const __half* g, const __half* bta,
                                           int k) {
@@ -164,7 +180,7 @@ template <bool kInt8>
 __device__ void ln_row_stats(const Params& p, Header& hd, int ctid, int cw, int lane, bool write_res) {
   const RowMap rm(p.B, ctid);
   const int K = p.K;
-  const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
+  const ResidualView rv = residual_view(p);
   if (p.ln_stats_in != nullptr) {  // statistics from the producing epilogue: no full-row pass
     if (ctid < p.B) ln_from_sums(p.ln_stats_in, ctid, p.ln_inv_k, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
     if (!kInt8) return;
@@ -451,7 +467,7 @@ __device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, in
     sx[b * xrw + (i - b * nrows)] = word;
   };
   if (p.pro == PRO_LN) {
-    const ResidualView rv{p.res_in, p.res_delta, p.delta_bias, K};
+    const ResidualView rv = residual_view(p);
     // item i -> (b, packed row): fp16 takes 2 consecutive k (half of a float4), int8 all 4
     chunked<kChunk>(ctid, total, [&](int i) {
       const int b = i / nrows;

@@ -273,3 +273,32 @@ def test_prefill_tensor_parallel_matches_oracle(dtype_bytes, tp):
     """Prefill with Megatron TP (column-parallel QKV / up, row-parallel attn-out / down with an
     all-reduce of the [M][h] partials, vocab-parallel LM head) on one device, vs the TP-aware oracle."""
     run_prefill_parity(512, 2, 8, 1000, batch=2, dtype_bytes=dtype_bytes, prompt_len=48, max_ctx=56, tp=tp)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+@pytest.mark.parametrize("tp,batch", [(2, 1), (4, 3), (8, 2)])
+def test_fused_allreduce_tp_matches_oracle(dtype_bytes, tp, batch, monkeypatch):
+    """Tensor parallelism with the fused all-reduce (row-parallel epilogues push their partials into
+    every rank's slots and bump a counter; the next LayerNorm prologue waits and sums the slots in
+    rank order) against the TP-aware oracle, graph-replayed over several steps."""
+    monkeypatch.setenv("DSINF_FUSED_AR", "1")
+    run_parity(512, 3, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, tp=tp, step_kernel=False, prompt_len=5, gen=4)
+
+
+def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
+    """Same TP=4 model with the fused all-reduce and with explicit on-device all-reduce launches:
+    identical greedy tokens, logits within fp32 summation-order noise."""
+    rng = np.random.default_rng(5)
+    prompt = rng.integers(0, 1000, (2, 6)).astype(np.int32)
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("DSINF_FUSED_AR", fused)
+        m = DecoderModel(512, 2, 8, 1000, batch=2, max_ctx=24, tp_size=4, tp_mode=capi.TP_LOCAL, seed=SEED)
+        m.set_prompt(prompt)
+        m.step(10)
+        torch.cuda.synchronize()
+        outs.append((m.full_logits(), m.read_tokens()[1]))
+        m.close()
+    (la, ha), (lb, hb) = outs
+    assert np.array_equal(ha, hb)
+    assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(lb).max()) + 1e-4
