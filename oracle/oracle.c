@@ -475,10 +475,11 @@ static void gemm8_a16(const int8_t* W, const float* ws, int64_t N, int64_t K, co
     }
 }
 
-/* int8 path GEMM on fp16 activations: per-token quantisation, exact int32, fp32 dequant */
-static int g_int8_act = 0;
-static void gemm8(const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B, float* y) {
-  if (g_int8_act == 1) {
+/* int8 path GEMM on fp16 activations: per-token quantisation, exact int32, fp32 dequant
+ * (int8_act 1: weight-only, fp16 activations) */
+static void gemm8(int int8_act, const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B,
+                  float* y) {
+  if (int8_act == 1) {
     gemm8_a16(W, ws, N, K, x16, B, y);
     return;
   }
@@ -492,7 +493,6 @@ static void gemm8(const int8_t* W, const float* ws, int64_t N, int64_t K, const 
 
 int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits, int32_t* next_tokens) {
   const int64_t h = m->h, d = m->d, Hl = m->Hl, B = m->B, Fl = m->Fl, mc = m->c.max_ctx;
-  g_int8_act = m->c.int8_act;
   const int i8 = m->c.dtype_bytes == 1;
   const int sm = m->c.sm_count;
   if (pos < 0 || pos >= mc) return 2;
@@ -529,7 +529,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
       const int64_t Nq = 3 * Hl * d;
       /* K1: QKV + bias + RoPE + KV append */
       if (!i8) gemm16(w->wqkv, Nq, h, sm, xln, B, yd);
-      else gemm8(w->qqkv, w->sqkv, Nq, h, xln, B, yf);
+      else gemm8(m->c.int8_act, w->qqkv, w->sqkv, Nq, h, xln, B, yf);
       for (int64_t b = 0; b < B; ++b)
         for (int64_t n = 0; n < Nq; n += 2) {
           const int64_t sec = n / (Hl * d), rem = n % (Hl * d), hh = rem / d, i = rem % d;
@@ -607,7 +607,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wo, h, Hl * d, sm, xa, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(w->qo, w->so, h, Hl * d, xa, B, yf);
+        gemm8(m->c.int8_act, w->qo, w->so, h, Hl * d, xa, B, yf);
       }
       for (int64_t i = 0; i < B * h; ++i) dsum[i] = rk == 0 ? yf[i] : dsum[i] + yf[i];
       free(xa);
@@ -629,7 +629,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
           for (int64_t n = 0; n < Fl; ++n)
             u16[b * Fl + n] = f16r((float)gelu_tanh(yd[b * Fl + n] + ly->bup[rk * Fl + n]));
       } else {
-        gemm8(w->qup, w->sup, Fl, h, xln, B, yf);
+        gemm8(m->c.int8_act, w->qup, w->sup, Fl, h, xln, B, yf);
         for (int64_t b = 0; b < B; ++b)
           for (int64_t n = 0; n < Fl; ++n) {
             const float y = yf[b * Fl + n] + ly->bup[rk * Fl + n];
@@ -641,7 +641,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wdown, h, Fl, sm, u16, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(w->qdown, w->sdown, h, Fl, u16, B, yf);
+        gemm8(m->c.int8_act, w->qdown, w->sdown, h, Fl, u16, B, yf);
       }
       for (int64_t i = 0; i < B * h; ++i) dm[i] = rk == 0 ? yf[i] : dm[i] + yf[i];
     }
