@@ -501,7 +501,10 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
 void row_prep(const PrepParams& p_in, cudaStream_t s, bool pdl) {
   PrepParams p = p_in;
   p.inv_k = 1.0 / static_cast<double>(p.K);
-  if (p.K % 8 != 0 || p.K / 4 > kPrepThreads * kPrepVec) throw ConfigError("row_prep: K must be a multiple of 8, <= 16384");
+  if (p.K % 8 != 0) throw ConfigError("row_prep: K must be a multiple of 8");
+  // the LayerNorm modes hold the row in registers; quantisation loops over any K
+  if (p.mode != PREP_QUANT_I8 && p.K / 4 > kPrepThreads * kPrepVec)
+    throw ConfigError("row_prep: LayerNorm rows must be <= 16384 wide");
   if (p.mode == PREP_QUANT_I8 && (p.x_ld % 4 != 0 || (reinterpret_cast<uintptr_t>(p.x) & 7) != 0))
     throw ConfigError("row_prep: x rows must be 8-byte aligned");
   launch_pdl(row_prep_kernel, dim3(p.B), dim3(kPrepThreads), 0, s, pdl, p);
