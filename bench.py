@@ -158,10 +158,11 @@ def gemm_shapes(preset, tp):
     return layer, ("lm_head", vpad // tp, h)
 
 
-def reference_ms_per_token(preset, tp, batch, dtype_bytes, budget_s, threads):
+def reference_ms_per_token(preset, tp, batch, dtype_bytes, budget_s, threads, rows_cache=None):
     """exec_reference (gemm.hpp:147-202, compiled from the reference headers) on a row sample of every
     per-rank GEMM of one decode step; per-token time = L * sum(layer GEMMs) + LM head, each scaled
-    from its row sample (every output row costs the same).  Returns (ms_per_token, kind, sample)."""
+    from its row sample (every output row costs the same).  Returns (ms_per_token, kind, sample).
+    `rows_cache` (dict) keeps the calibrated sample sizes across calls."""
     from oracle import oracle as O
 
     layer, lm = gemm_shapes(preset, tp)
@@ -172,11 +173,16 @@ def reference_ms_per_token(preset, tp, batch, dtype_bytes, budget_s, threads):
     total_ms = 0.0
     rows_used = {}
     for name, N, K in shapes:
-        # calibrate: time a small sample, then size the real sample to the per-shape budget
-        rows = max(threads, 64)
-        t = _time_rows(O, ref, N, K, batch, dtype_bytes, rows, threads)
-        rate = t / rows
-        rows = int(min(N, max(threads, per_shape / max(rate, 1e-9))))
+        if rows_cache is not None and name in rows_cache:
+            rows = rows_cache[name]
+        else:
+            # calibrate: time a small sample, then size the real sample to the per-shape budget
+            rows = max(threads, 64)
+            t = _time_rows(O, ref, N, K, batch, dtype_bytes, rows, threads)
+            rate = t / rows
+            rows = int(min(N, max(threads, per_shape / max(rate, 1e-9))))
+            if rows_cache is not None:
+                rows_cache[name] = rows
         t = _time_rows(O, ref, N, K, batch, dtype_bytes, rows, threads)
         ms_full = t * (N / rows) * 1e3
         rows_used[name] = rows
@@ -207,8 +213,11 @@ def run_reference(args, preset, rank, world):
     threads = os.cpu_count() or 1
     dtype_bytes = 1 if args.dtype == "int8" else 2
     vals = []
+    # the whole --warmup + --steps run stays within ~2 minutes of host time (timed exec + setup)
+    budget = max(1.0, min(args.ref_step_budget, 50.0 / max(1, args.warmup + args.steps)))
+    rows_cache = {}
     for i in range(args.warmup + args.steps):
-        ms, kind, sample = reference_ms_per_token(preset, world, args.batch, dtype_bytes, args.ref_step_budget, threads)
+        ms, kind, sample = reference_ms_per_token(preset, world, args.batch, dtype_bytes, budget, threads, rows_cache)
         if i >= args.warmup:
             vals.append(ms)
     ms = statistics.median(vals)
