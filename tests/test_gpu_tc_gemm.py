@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 from paper_2207_00032_b200 import engine as E  # noqa: E402
 
 SHAPES = [(256, 64, 128), (512, 128, 256), (1024, 4096, 128), (4800, 1600, 300), (12288, 4096, 256),
-          (300, 200, 77), (256, 64, 1), (4096, 16384, 128)]
+          (300, 200, 77), (256, 64, 1), (4096, 16384, 128), (4800, 1600, 3), (16384, 4096, 100)]
 
 
 def _rand_f16(rng, shape, scale=1.0):
@@ -35,8 +35,10 @@ def test_tc_fp16_matches_reference(N, K, M):
     assert np.all(err <= 2e-3 * bound + 1e-3), float((err / (bound + 1e-9)).max())
 
 
-@pytest.mark.parametrize("N,K,M", [(256, 128, 128), (1024, 4096, 256), (4800, 1600, 300), (300, 208, 77)])
+@pytest.mark.parametrize("N,K,M", [(256, 128, 128), (1024, 4096, 256), (4800, 1600, 300), (300, 208, 77),
+                                   (1024, 4096, 64), (4096, 16384, 16), (12288, 4096, 128)])
 def test_tc_int8_bit_exact(N, K, M):
+    """(M <= 128 with long K runs the split-K cluster mode: int32 partials summed through DSMEM.)"""
     rng = np.random.default_rng(N * 5 + K + M)
     W = rng.standard_normal((N, K)).astype(np.float32) * 0.05
     x = rng.standard_normal((M, K)).astype(np.float32)
