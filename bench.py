@@ -234,9 +234,12 @@ def run_reference(args, preset, rank, world):
 
 
 def workload_config(args, preset, world):
-    return {"workload": f"{preset.name} {args.dtype} greedy decode, batch {args.batch}, {args.prompt}-token prompt, "
-                        f"TP={world}", "model": args.config, "global_batch": args.batch, "seq_len": args.prompt,
-            "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
+    cfg = {"workload": f"{preset.name} {args.dtype} greedy decode, batch {args.batch}, {args.prompt}-token prompt, "
+                       f"TP={world}", "model": args.config, "global_batch": args.batch, "seq_len": args.prompt,
+           "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
+    if args.dtype == "int8":
+        cfg["int8_act"] = (("w8a16" if args.batch <= 8 else "w8a8") if args.int8_act == "auto" else args.int8_act)
+    return cfg
 
 
 # ---------------------------------------------------------------- our path
@@ -252,7 +255,9 @@ def decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, skip):
                 continue
             m = E.DecoderModel(preset.hidden, preset.layers, preset.heads, preset.vocab,
                                dtype_bytes=1 if dtype == "int8" else 2, batch=batch,
-                               max_ctx=args.prompt + args.warmup + args.steps + 8, seed=SEED)
+                               max_ctx=args.prompt + args.warmup + args.steps + 8, seed=SEED,
+                               int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16,
+                                         "auto": capi.INT8_AUTO}[args.int8_act])
             prompt = np.random.default_rng(SEED + batch).integers(0, preset.vocab, (batch, args.prompt)).astype(np.int32)
             m.set_prompt(prompt, stream=stream)
             m.prefill(stream=stream)
@@ -266,7 +271,9 @@ def decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, skip):
             ms = a.elapsed_time(b)
             pos0 = args.prompt + args.warmup
             gb = sum(m.bytes_per_step(q) for q in range(pos0, pos0 + args.steps)) / (ms * 1e-3) / 1e9
-            rows.append({"dtype": dtype, "batch": batch, "ms_per_token": round(ms / args.steps, 4),
+            mode = (("w8a16" if batch <= 8 else "w8a8") if args.int8_act == "auto" else args.int8_act) \
+                if dtype == "int8" else None
+            rows.append({"dtype": dtype, "batch": batch, "int8_act": mode, "ms_per_token": round(ms / args.steps, 4),
                          "tokens_per_s": round(batch * args.steps * 1e3 / ms, 1), "step_gbs": round(gb, 1),
                          "frac": round(gb / peak_gbs, 4)})
             m.close()
@@ -396,7 +403,7 @@ def run_ours(args, preset, rank, world, local_rank):
                            batch=args.batch, max_ctx=max_ctx, tp_size=world, tp_rank=rank,
                            tp_mode=capi.TP_NCCL if world > 1 else capi.TP_NONE, nccl_comm=comm,
                            use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank,
-                           int8_act=capi.INT8_W8A16 if args.int8_act == "w8a16" else capi.INT8_W8A8)
+                           int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16, "auto": capi.INT8_AUTO}[args.int8_act])
     rng = np.random.default_rng(SEED)
     prompt = rng.integers(0, preset.vocab, (args.batch, args.prompt)).astype(np.int32)
 
@@ -590,8 +597,9 @@ def main():
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the fp16/int8 x batch 1/8/16 decode matrix")
-    ap.add_argument("--int8-act", choices=["w8a8", "w8a16"], default="w8a8",
-                    help="int8 decode GEMMs: per-token int8 activations (int32 accumulate) or weight-only")
+    ap.add_argument("--int8-act", choices=["w8a8", "w8a16", "auto"], default="auto",
+                    help="int8 decode GEMMs: per-token int8 activations (int32 accumulate), weight-only, or the "
+                         "measured per-batch choice (W8A16 for batch <= 8, W8A8 above)")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")

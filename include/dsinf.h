@@ -127,6 +127,7 @@ int dsinf_quantize_activations_int8(const void* x_f16, int64_t B, int64_t K, int
  *        per-output-row dequant -- no activation quantisation on the decode critical path. */
 #define DSINF_INT8_W8A8 0
 #define DSINF_INT8_W8A16 1
+#define DSINF_INT8_AUTO 2 /* runtime config only: W8A16 for batch <= 8, W8A8 above (measured) */
 
 #define DSINF_EPI_NONE 0
 #define DSINF_EPI_GELU 1 /* tanh GeLU after the bias */
@@ -216,8 +217,8 @@ typedef struct dsinf_runtime_config {
   float rope_base;
   int32_t device;       /* CUDA device ordinal */
   int32_t use_step_kernel; /* TP = 1: run each decode step as ONE persistent kernel */
-  int32_t int8_act;     /* dtype_bytes 1: DSINF_INT8_W8A8 (default) or DSINF_INT8_W8A16 (decode GEMMs;
-                           the tensor-core prefill stays W8A8) */
+  int32_t int8_act;     /* dtype_bytes 1: DSINF_INT8_W8A8 (default), DSINF_INT8_W8A16 or DSINF_INT8_AUTO
+                           (decode GEMMs; the tensor-core prefill stays W8A8) */
 } dsinf_runtime_config;
 
 typedef struct dsinf_model dsinf_model;

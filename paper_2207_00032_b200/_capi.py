@@ -25,6 +25,7 @@ DT_F64 = 4
 
 INT8_W8A8 = 0
 INT8_W8A16 = 1
+INT8_AUTO = 2
 EPI_NONE = 0
 EPI_GELU = 1
 EPI_RESID = 2

@@ -117,8 +117,11 @@ struct dsinf_model {
   int64_t h = 0, L = 0, H = 0, d = 0, Hl = 0, V = 0, Vpad = 0, Vl = 0, F = 0, Fl = 0;
   int B = 0, t = 1, max_ctx = 0;
   bool int8 = false;
-  bool a16 = false;  // int8 weights with fp16 activations (W8A16) in the decode GEMMs
-  bool q8() const { return int8 && !a16; }  // int8 activations (W8A8)
+  bool a16 = false;  // int8 weights with fp16 activations (W8A16) in some decode GEMM
+  int a16_mask = 0;  // which: bit 0 QKV, 1 attn-out, 2 MLP-up, 3 MLP-down
+  bool a16g(int g) const { return int8 && ((a16_mask >> g) & 1); }
+  bool q8g(int g) const { return int8 && !a16g(g); }  // GEMM g takes int8 activations (W8A8)
+  bool q8() const { return q8g(0) || q8g(1) || q8g(2) || q8g(3); }  // any W8A8 GEMM
   std::vector<dsinf::DevBuf> allocs;
   std::vector<dsinf::Shard> shards;
   float2* rope = nullptr;
@@ -332,11 +335,11 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
     sh.xsc = m.alloc_n<float>(B);
   }
   if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
-  const bool i8 = m.int8, a16 = m.a16;
-  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, a16);
-  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, a16);
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, a16);
-  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, a16);
+  const bool i8 = m.int8;
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0));
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1));
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2));
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3));
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm);
 }
 
@@ -639,7 +642,7 @@ struct Enqueuer {
     if (m.xs_ln) {
       ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l), m.fuse_ln || l == 0 ? nullptr : sh.d_mlp,
            m.fuse_ln || l == 0 ? nullptr : sh.layers[l - 1].bdown, m.fuse_ln ? nullptr : sh.res[1], w.ln1g, w.ln1b,
-           m.q8());
+           m.q8g(0));
     } else {
       p.pro = gemm::PRO_LN;
       p.res_in = sh.res[0];
@@ -690,11 +693,11 @@ struct Enqueuer {
   void k3_attn_out(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wo, w.so, static_cast<int>(m.h), static_cast<int>(m.Hl * m.d), m.int8);
-    p.pro = m.q8() ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.pro = m.q8g(1) ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.a;
     p.x_ld = static_cast<int>(m.Hl * m.d);
     p.amax_in = amslot(sh, 2 * l);
-    if (m.xs_od && m.q8()) {  // quantise once (row max from attention), then stream int8 x
+    if (m.xs_od && m.q8g(1)) {  // quantise once (row max from attention), then stream int8 x
       prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.a, p.x_ld,
            amslot(sh, 2 * l), p.x_ld, true);
       p.pro = gemm::PRO_I8;
@@ -719,9 +722,9 @@ struct Enqueuer {
     gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
     if (m.xs_ln) {
       if (m.fuse_ln)
-        ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8());
+        ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8g(2));
       else
-        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.q8());
+        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.q8g(2));
     } else {
       p.pro = gemm::PRO_LN;
       if (m.fuse_ln) {
@@ -747,11 +750,11 @@ struct Enqueuer {
   void k5_down(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wdown, w.sdown, static_cast<int>(m.h), static_cast<int>(m.Fl), m.int8);
-    p.pro = m.q8() ? gemm::PRO_QUANT : gemm::PRO_F16;
+    p.pro = m.q8g(3) ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.u;
     p.x_ld = static_cast<int>(m.Fl);
     p.amax_in = amslot(sh, 2 * l + 1);
-    if (m.xs_od && m.q8()) {
+    if (m.xs_od && m.q8g(3)) {
       prep(sh, ops::PREP_QUANT_I8, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, sh.u, p.x_ld,
            amslot(sh, 2 * l + 1), p.x_ld, true);
       p.pro = gemm::PRO_I8;
@@ -1205,8 +1208,17 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     m->B = rt->batch;
     m->max_ctx = static_cast<int>(rt->max_ctx);
     m->int8 = cfg->dtype_bytes == 1;
-    require(rt->int8_act == DSINF_INT8_W8A8 || rt->int8_act == DSINF_INT8_W8A16, "unknown int8_act");
-    m->a16 = m->int8 && rt->int8_act == DSINF_INT8_W8A16;
+    require(rt->int8_act == DSINF_INT8_W8A8 || rt->int8_act == DSINF_INT8_W8A16 || rt->int8_act == DSINF_INT8_AUTO,
+            "unknown int8_act");
+    // INT8 activation mode per GEMM (mask): W8A8 everywhere, W8A16 everywhere, or AUTO -- measured
+    // on B200 (GPT-J): W8A16 everywhere is faster up to B = 8 (1.04x at B=1, 1.07x at B=8), W8A8 at
+    // B = 16; mixed masks measured slower (DSINF_A16_MASK overrides for experiments)
+    if (m->int8) {
+      if (rt->int8_act == DSINF_INT8_W8A16) m->a16_mask = 0xf;
+      else if (rt->int8_act == DSINF_INT8_AUTO) m->a16_mask = rt->batch <= 8 ? 0xf : 0x0;
+      if (const char* am = std::getenv("DSINF_A16_MASK")) m->a16_mask = static_cast<int>(std::strtol(am, nullptr, 0)) & 0xf;
+    }
+    m->a16 = m->a16_mask != 0;
     require(!(m->a16 && rt->use_step_kernel), "the persistent step kernel runs W8A8 only");
     m->attn_chunks = ops::attention_chunks(m->B, static_cast<int>(m->Hl));
     {

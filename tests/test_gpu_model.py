@@ -22,7 +22,7 @@ SEED = 20220701
 
 
 def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, prompt_len=6, gen=4,
-               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=True, int8_act=0):
+               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=True, int8_act=0, oracle_int8_act=None):
     tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
     rng = np.random.default_rng(hidden + layers + batch)
     prompt = rng.integers(0, vocab, (batch, prompt_len)).astype(np.int32)
@@ -31,7 +31,7 @@ def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, pr
                        tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED,
                        use_step_kernel=step_kernel, int8_act=int8_act)
     ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=batch, max_ctx=max_ctx,
-                        seed=SEED, int8_act=int8_act)
+                        seed=SEED, int8_act=int8_act if oracle_int8_act is None else oracle_int8_act)
     gpu.set_prompt(prompt)
     worst = 0.0
     margins = []
@@ -302,3 +302,10 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
     (la, ha), (lb, hb) = outs
     assert np.array_equal(ha, hb)
     assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(lb).max()) + 1e-4
+
+
+@pytest.mark.parametrize("batch,oracle_act", [(1, 1), (8, 1), (16, 0)])
+def test_int8_auto_mode_matches_oracle(batch, oracle_act):
+    """DSINF_INT8_AUTO: weight-only up to batch 8, W8A8 above -- each against the oracle's same mode."""
+    run_parity(256, 2, 4, 1000, batch=batch, dtype_bytes=1, int8_act=capi.INT8_AUTO, step_kernel=False,
+               oracle_int8_act=oracle_act)
