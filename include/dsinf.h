@@ -38,6 +38,7 @@ extern "C" {
 #define DSINF_DT_F32 2
 #define DSINF_DT_I8 3  /* symmetric int8 with fp32 scales */
 #define DSINF_DT_F64 4 /* host-side only (reference container type) */
+#define DSINF_DT_BF16 5 /* bfloat16 (large-batch tensor-core GEMM) */
 
 const char* dsinf_last_error(void);
 const char* dsinf_version(void);
@@ -158,7 +159,7 @@ int dsinf_gemm(const dsinf_gemm_args* args, void* stream);
 #define DSINF_EPI_RESID 2 /* out (F32) += x.W^T + bias: residual-stream update */
 typedef struct dsinf_gemm_lb_args {
   const void* w;          /* [N][K] row-major, F16 or I8 */
-  int32_t w_dtype;        /* DSINF_DT_F16 or DSINF_DT_I8 (x has the same type) */
+  int32_t w_dtype;        /* DSINF_DT_F16, DSINF_DT_BF16 (F32 out, no bias) or DSINF_DT_I8 (x has the same type) */
   const float* w_scales;  /* I8: [N] */
   int64_t N, K, M;
   const void* x;          /* [M][K] row-major */

@@ -22,6 +22,7 @@ DT_F16 = 1
 DT_F32 = 2
 DT_I8 = 3
 DT_F64 = 4
+DT_BF16 = 5
 
 INT8_W8A8 = 0
 INT8_W8A16 = 1

@@ -94,8 +94,12 @@ int dsinf_gemm_large_batch(const dsinf_gemm_lb_args* a, void* stream) {
     require(a->w && a->x && a->out, "null pointer argument");
     require(a->N >= 1 && a->K >= 1 && a->M >= 1, "gemm shape dims must be positive");
     require(a->N < (1 << 30) && a->K < (1 << 28) && a->M < (1 << 30), "gemm shape too large");
-    require(a->w_dtype == DSINF_DT_F16 || a->w_dtype == DSINF_DT_I8, "w_dtype must be F16 or I8");
+    require(a->w_dtype == DSINF_DT_F16 || a->w_dtype == DSINF_DT_BF16 || a->w_dtype == DSINF_DT_I8,
+            "w_dtype must be F16, BF16 or I8");
     const bool i8 = a->w_dtype == DSINF_DT_I8;
+    const bool bf = a->w_dtype == DSINF_DT_BF16;
+    require(!bf || (a->out_dtype == DSINF_DT_F32 && a->bias == nullptr && a->epilogue != DSINF_EPI_GELU),
+            "BF16 GEMM: F32 output, no bias, no GeLU");
     require(!i8 || (a->w_scales && a->x_scales), "I8 needs w_scales and x_scales");
     require(a->out_dtype == DSINF_DT_F32 || a->out_dtype == DSINF_DT_F16, "out_dtype must be F32 or F16");
     tc::Params p{};
@@ -104,6 +108,7 @@ int dsinf_gemm_large_batch(const dsinf_gemm_lb_args* a, void* stream) {
     p.K = static_cast<int>(a->K);
     const int eb = i8 ? 1 : 2;
     tc::make_maps(p, a->x, p.K * eb, a->w, p.K * eb, eb);
+    p.bf16 = bf ? 1 : 0;
     p.x_scale = a->x_scales;
     p.w_scale = a->w_scales;
     p.bias = static_cast<const __half*>(a->bias);

@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ================= MMA issuer
-      constexpr uint32_t idesc = instr_desc<kInt8>();
+      const uint32_t idesc = instr_desc<kInt8>() | (!kInt8 && p.bf16 ? (1u << 7) | (1u << 10) : 0u);
       int it = 0, j = 0;
       for (int u = unit0; u < units; u += ustride, ++j) {
         const int a = j & 1;
@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
   } else if (warp == 1) {
     if (lane == 0) {
       // instruction descriptor with N = 128
-      constexpr uint32_t idesc = (instr_desc<kInt8>() & ~(0x3fu << 17)) | (static_cast<uint32_t>(kSBN >> 3) << 17);
+      const uint32_t idesc = ((instr_desc<kInt8>() & ~(0x3fu << 17)) | (static_cast<uint32_t>(kSBN >> 3) << 17)) |
+                             (!kInt8 && p.bf16 ? (1u << 7) | (1u << 10) : 0u);
       for (int i = 0; i < nk; ++i) {
         const int st = i % kSStages;
         ptx::mbar_wait(&full[st], (i / kSStages) & 1);

@@ -48,6 +48,7 @@ struct Params {
   int M, N, K;
   int k_blocks;                  // ceil(K * elem / 128)
   int pair;                      // cluster-pair mode (set by make_maps: >= 2 row tiles)
+  int bf16;                      // 16-bit operands are bfloat16 (kind::f16 with BF16 A/B formats)
   int split;                     // > 1: split-K mode for one row tile (M <= 128): 128-column tiles, a cluster of
                                  // `split` CTAs per tile reduces its partials through DSMEM
   const float* x_scale;          // int8: [M]

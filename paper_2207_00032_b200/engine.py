@@ -212,7 +212,7 @@ def gemm_large_batch(w, x, *, w_scales=None, x_scales=None, bias=None, out=None,
         out = torch.empty((M, N), dtype=od, device=x.device)
     a = capi.LbArgs()
     a.w = _dptr(w)
-    a.w_dtype = capi.DT_I8 if i8 else capi.DT_F16
+    a.w_dtype = capi.DT_I8 if i8 else (capi.DT_BF16 if w.dtype == torch.bfloat16 else capi.DT_F16)
     a.w_scales = _dptr(w_scales)
     a.N, a.K, a.M = N, K, M
     a.x = _dptr(x)

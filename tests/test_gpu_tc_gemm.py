@@ -95,3 +95,18 @@ def test_tc_int8_matches_decode_sbi_gemm():
     a = E.gemm(wp, xq, N, K, w_scales=ws, x_scales=xs).cpu().numpy()
     b = E.gemm_large_batch(wq_rm, xq, w_scales=ws_rm, x_scales=xs).cpu().numpy()
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("N,K,M", [(1024, 4096, 256), (4800, 1600, 128), (12288, 4096, 64)])
+def test_tc_bf16(N, K, M):
+    """BF16 operands on the same tcgen05 path (kind::f16 with BF16 A/B formats), fp32 out:
+    within 2e-3 * sum|w x| + 1e-3 of the fp64 product of the same bf16 values."""
+    g = torch.Generator().manual_seed(N + K + M)
+    W = (torch.randn(N, K, generator=g) * 0.05).bfloat16()
+    x = torch.randn(M, K, generator=g).bfloat16()
+    dev = torch.device("cuda")
+    out = E.gemm_large_batch(W.to(dev), x.to(dev)).cpu().double().numpy()
+    Wd, xd = W.double().numpy(), x.double().numpy()
+    ref = xd @ Wd.T
+    bound = np.abs(xd) @ np.abs(Wd).T
+    assert np.all(np.abs(out - ref) <= 2e-3 * bound + 1e-3)
