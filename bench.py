@@ -280,6 +280,41 @@ def decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, skip):
     return rows
 
 
+def tp_slice_sweep(E, capi, torch, args, stream, peak_gbs):
+    """The TP configs of BASELINE.json (NeoX-20B t=2, GPT-50B t=4, GPT3-175B t=8) measured per rank
+    on this one GPU: rank 0's shard alone (DSINF_TP_SLICE -- the same kernels and per-rank bytes,
+    the two per-layer all-reduces and the argmax all-gather skipped), device-timed like the main
+    line.  It is the compute floor of each rank's step; the TP=t step adds the collectives."""
+    rows = []
+    for name in ("gpt-neox-20b", "gpt-50b", "gpt3-175b"):
+        pr = E.PRESETS[name]
+        for dtype in ("fp16", "int8"):
+            for batch in (1, 16):
+                m = E.DecoderModel(pr.hidden, pr.layers, pr.heads, pr.vocab, dtype_bytes=1 if dtype == "int8" else 2,
+                                   batch=batch, max_ctx=args.prompt + args.warmup + args.steps + 8, tp_size=pr.tp,
+                                   tp_rank=0, tp_mode=capi.TP_SLICE, seed=SEED,
+                                   int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16,
+                                             "auto": capi.INT8_AUTO}[args.int8_act])
+                prompt = np.random.default_rng(SEED + batch).integers(0, pr.vocab, (batch, args.prompt)).astype(np.int32)
+                m.set_prompt(prompt, stream=stream)
+                m.prefill(stream=stream)
+                m.step(args.warmup, stream=stream)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                m.step(args.steps, stream=stream)
+                b.record(stream)
+                b.synchronize()
+                ms = a.elapsed_time(b)
+                pos0 = args.prompt + args.warmup
+                gb = sum(m.bytes_per_step(q) for q in range(pos0, pos0 + args.steps)) / (ms * 1e-3) / 1e9
+                rows.append({"config": name, "tp": pr.tp, "dtype": dtype, "batch": batch,
+                             "rank_ms_per_token": round(ms / args.steps, 4), "rank_step_gbs": round(gb, 1),
+                             "frac": round(gb / peak_gbs, 4)})
+                m.close()
+    return rows
+
+
 def kernel_roofline(E, torch, preset, tp, batch, dtype, peak_gbs, stream):
     """Times each SBI-GeMM shape of one layer (+ LM head) alone with CUDA events on the launching
     stream; 4 rotating weight copies (> L2) per shape.  Returns the per-kernel list and the byte-weighted
@@ -577,6 +612,12 @@ def run_ours(args, preset, rank, world, local_rank):
                          "frac": round(step_gbs / peak_gbs, 4)})
         line["decode_sweep"] = {"note": "BASELINE metric matrix on this GPU, same timing rules; frac = step GB/s "
                                         "(algorithmic bytes) / measured HBM peak", "rows": sweep}
+    if world == 1 and rank == 0 and not args.no_tp_slices:
+        line["tp_rank_slices"] = {
+            "note": "per-rank step of the TP configs on this one GPU: rank 0's shard alone (same kernels and "
+                    "per-rank bytes; the per-layer all-reduces and the argmax all-gather are skipped, so this "
+                    "is each rank's compute floor, not a TP=t number)",
+            "rows": tp_slice_sweep(E, capi, torch, args, stream, peak_gbs)}
     if comm is not None:
         capi.lib.dsinf_nccl_comm_destroy(comm)
     if rank == 0:
@@ -600,6 +641,7 @@ def main():
     ap.add_argument("--int8-act", choices=["w8a8", "w8a16", "auto"], default="auto",
                     help="int8 decode GEMMs: per-token int8 activations (int32 accumulate), weight-only, or the "
                          "measured per-batch choice (W8A16 for batch <= 8, W8A8 above)")
+    ap.add_argument("--no-tp-slices", action="store_true", help="skip the per-rank TP slice measurements")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--ref-step-budget", type=float, default=2.0, help="seconds per --impl reference step")

@@ -204,6 +204,8 @@ typedef struct dsinf_model_config { /* infersim::ModelConfig (model.hpp:42-64), 
 #define DSINF_TP_NONE 0
 #define DSINF_TP_NCCL 1  /* one process per GPU, NCCL all-reduce over NVLink */
 #define DSINF_TP_LOCAL 2 /* all shards on this device (single-GPU sharding check) */
+#define DSINF_TP_SLICE 3 /* rank tp_rank's shard alone on this device, collectives skipped: per-rank
+                            step timing of a TP model on one GPU (outputs are not the model's) */
 
 typedef struct dsinf_runtime_config {
   int32_t batch;        /* sequences per step, 1..16 per launch */

@@ -34,6 +34,7 @@ EPI_RESID = 2
 TP_NONE = 0
 TP_NCCL = 1
 TP_LOCAL = 2
+TP_SLICE = 3
 
 TILING_1D = 0
 TILING_2D = 1

@@ -302,7 +302,7 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   }
   sh.lnfg = make_vec(m, tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, -1, DSINF_T_LNF_G), 1.f, s);
   sh.lnfb = make_vec(m, tensor_map(h, m.H, m.V, m.t, r, m.rt.seed, -1, DSINF_T_LNF_B), 0.f, s);
-  if (r == 0 || m.rt.tp_mode == DSINF_TP_NCCL) {
+  if (r == 0 || m.rt.tp_mode != DSINF_TP_LOCAL) {
     sh.wte = m.alloc_n<__half>(m.V * h);
     ops::init_rowmajor_f16(synth_base(m.rt.seed, -1, DSINF_T_WTE), SynthScale::kWeight, m.V, h, sh.wte, s);
   } else {
@@ -811,7 +811,8 @@ struct Enqueuer {
 
   // Sum of the t partials of `which` (0 = d_attn, 1 = d_mlp).
   void allreduce(int which) {
-    if (m.t == 1 || m.fused_ar) return;  // fused: pushed by the GEMM epilogues, summed by the consumers
+    // fused: pushed by the GEMM epilogues, summed by the consumers; slice: no peers to sum with
+    if (m.t == 1 || m.fused_ar || m.rt.tp_mode == DSINF_TP_SLICE) return;
     const int64_t count = static_cast<int64_t>(m.B) * m.h;
     if (m.rt.tp_mode == DSINF_TP_NCCL) {
       Shard& sh = m.shards[0];
@@ -903,7 +904,7 @@ struct Enqueuer {
       const int64_t count = static_cast<int64_t>(M) * h;
       if (m.rt.tp_mode == DSINF_TP_NCCL) {
         nccl::allreduce_sum_f32(m.shards[0].pf.part, count, m.comm, s);
-      } else {
+      } else if (m.rt.tp_mode == DSINF_TP_LOCAL) {
         ops::LocalReduceParams lr{};
         lr.shards = m.t;
         lr.count = count;
@@ -991,8 +992,9 @@ struct Enqueuer {
     if (m.t > 1 && m.rt.tp_mode == DSINF_TP_NCCL)
       nccl::allgather_bytes(m.am_key + m.shards[0].rank * m.B, m.am_key, m.B * sizeof(unsigned long long), m.comm, s);
     ops::SelectParams sp{};
-    sp.keys = m.am_key;
-    sp.shards = m.t;
+    const bool slice = m.rt.tp_mode == DSINF_TP_SLICE;  // only this rank's vocab slice has a key
+    sp.keys = slice ? m.am_key + m.shards[0].rank * m.B : m.am_key;
+    sp.shards = slice ? 1 : m.t;
     sp.B = m.B;
     sp.next_tok = m.next_tok;
     sp.pos = m.pos;
@@ -1059,8 +1061,9 @@ struct Enqueuer {
       nccl::allgather_bytes(m.am_key + m.shards[0].rank * m.B, m.am_key, m.B * sizeof(unsigned long long), m.comm, s);
     }
     ops::SelectParams sp{};
-    sp.keys = m.am_key;
-    sp.shards = m.t;
+    const bool slice = m.rt.tp_mode == DSINF_TP_SLICE;  // only this rank's vocab slice has a key
+    sp.keys = slice ? m.am_key + m.shards[0].rank * m.B : m.am_key;
+    sp.shards = slice ? 1 : m.t;
     sp.B = m.B;
     sp.next_tok = m.next_tok;
     sp.pos = m.pos;
@@ -1132,8 +1135,10 @@ void validate_configs(const dsinf_model_config& c, const dsinf_runtime_config& r
   require(c.hidden_dim % 8 == 0, "hidden_dim must be a multiple of 8");
   require((c.hidden_dim / c.num_heads) % 2 == 0, "head dim must be even (rotary pairs)");
   require(r.max_ctx >= 1 && r.max_ctx <= c.max_seq, "max_ctx must be in [1, max_seq]");
-  if (r.tp_size > 1) require(r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_LOCAL, "tp_size > 1 needs a TP mode");
-  if (r.tp_mode == DSINF_TP_NCCL) require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
+  if (r.tp_size > 1)
+    require(r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_LOCAL || r.tp_mode == DSINF_TP_SLICE,
+            "tp_size > 1 needs a TP mode");
+  if (r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_SLICE) require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
 }
 
 void build_rope(Model& m, cudaStream_t s) {
@@ -1227,7 +1232,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // x-streaming plans need 16-byte rows of GEMM-ready x
       const int64_t Fl = 4 * m->h / m->t, Ol = m->h / m->t;
       const bool rows16 = m->q8() ? (m->h % 16 == 0 && Fl % 16 == 0 && Ol % 16 == 0) : (Ol % 8 == 0 && Fl % 8 == 0);
-      m->xs_ln = rows16 && gemm::prefer_x_stream(m->B);
+      m->xs_ln = rows16 && gemm::prefer_x_stream(m->B, m->t > 1);
       const char* od = std::getenv("DSINF_XS_OD");
       const int od_v = od ? std::atoi(od) : -1;
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
@@ -1250,7 +1255,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     cudaStream_t s = m->cap_stream;
     const int nshards = (rt->tp_mode == DSINF_TP_LOCAL) ? m->t : 1;
     m->shards.resize(nshards);
-    for (int i = 0; i < nshards; ++i) m->shards[i].rank = (rt->tp_mode == DSINF_TP_NCCL) ? rt->tp_rank : i;
+    for (int i = 0; i < nshards; ++i) m->shards[i].rank = (rt->tp_mode == DSINF_TP_LOCAL) ? i : rt->tp_rank;
     build_rope(*m, s);
     m->prompt_cap = m->max_ctx;
     m->prompt = m->alloc_n<int32_t>(static_cast<int64_t>(m->B) * m->prompt_cap);

@@ -499,9 +499,9 @@ void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words)
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (x) failed: " + std::to_string(static_cast<int>(r)));
 }
 
-bool prefer_x_stream(int B) {
+bool prefer_x_stream(int B, bool tp) {
   const int v = env_int("DSINF_XS", -1);
-  return v < 0 ? B >= kXsMinBatch : v != 0;
+  return v < 0 ? (B >= kXsMinBatch || tp) : v != 0;
 }
 
 bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {

@@ -155,7 +155,10 @@ void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words)
 bool x_streamable(const void* x, int x_ld, int K, bool int8_x);
 // Batch sizes that use the x-streaming plan (DSINF_XS=0 never, =1 always; default B >= kXsMinBatch).
 constexpr int kXsMinBatch = 4;
-bool prefer_x_stream(int B);
+// `tp`: the layer's LayerNorm input is an all-reduced sum (TP > 1), so its row statistics cannot
+// come from the producing GEMM's epilogue: one row_prep launch + x-streaming beats every CTA
+// re-deriving them (GPT3-175B t=8 rank slice at B = 1: 12.8 -> 9.7 ms fp16, 10.3 -> 7.4 ms int8)
+bool prefer_x_stream(int B, bool tp = false);
 void launch(const Params& p, const Plan& plan, bool int8_weights, cudaStream_t stream, bool pdl);
 
 }  // namespace gemm

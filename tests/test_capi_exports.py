@@ -36,3 +36,20 @@ def test_errors_map_to_reference_exceptions():
     else:
         raise AssertionError("ConfigError expected")
     assert capi.lib.dsinf_version().decode().startswith("dsinf-b200")
+
+
+def test_python_constants_match_header():
+    """Every integer #define of include/dsinf.h that _capi mirrors (DSINF_<NAME> -> <NAME>) has the
+    header's value, so the Python host API and a C caller agree on modes, dtypes and error codes."""
+    import re
+
+    from paper_2207_00032_b200 import _capi
+
+    src = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "dsinf.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"^#define DSINF_([A-Z0-9_]+) (\d+)", src, re.M)}
+    checked = 0
+    for name, value in defs.items():
+        if hasattr(_capi, name):
+            assert getattr(_capi, name) == value, name
+            checked += 1
+    assert checked >= 20 and "TP_SLICE" in defs

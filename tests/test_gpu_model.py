@@ -282,6 +282,7 @@ def test_fused_allreduce_tp_matches_oracle(dtype_bytes, tp, batch, monkeypatch):
     every rank's slots and bump a counter; the next LayerNorm prologue waits and sums the slots in
     rank order) against the TP-aware oracle, graph-replayed over several steps."""
     monkeypatch.setenv("DSINF_FUSED_AR", "1")
+    monkeypatch.setenv("DSINF_XS", "0")  # the fused slots are summed by the per-CTA LayerNorm prologues
     run_parity(512, 3, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, tp=tp, step_kernel=False, prompt_len=5, gen=4)
 
 
@@ -293,6 +294,7 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
     outs = []
     for fused in ("1", "0"):
         monkeypatch.setenv("DSINF_FUSED_AR", fused)
+        monkeypatch.setenv("DSINF_XS", "0")
         m = DecoderModel(512, 2, 8, 1000, batch=2, max_ctx=24, tp_size=4, tp_mode=capi.TP_LOCAL, seed=SEED)
         m.set_prompt(prompt)
         m.step(10)
@@ -309,3 +311,29 @@ def test_int8_auto_mode_matches_oracle(batch, oracle_act):
     """DSINF_INT8_AUTO: weight-only up to batch 8, W8A8 above -- each against the oracle's same mode."""
     run_parity(256, 2, 4, 1000, batch=batch, dtype_bytes=1, int8_act=capi.INT8_AUTO, step_kernel=False,
                oracle_int8_act=oracle_act)
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+def test_tp_slice_mode(dtype_bytes):
+    """DSINF_TP_SLICE (per-rank timing of a TP model on one GPU): rank r's shard alone, collectives
+    skipped.  Deterministic, greedy tokens come from the rank's own vocab slice, and the per-rank
+    step bytes equal 1/t of the TP=1 weight stream plus the replicated parts."""
+    rng = np.random.default_rng(9)
+    V, t = 1000, 4
+    prompt = rng.integers(0, V, (2, 6)).astype(np.int32)
+    vl = (V + 128 * t - 1) // (128 * t) * 128
+    for rank in (0, 3):
+        hists = []
+        for _ in range(2):
+            m = DecoderModel(512, 2, 8, V, dtype_bytes=dtype_bytes, batch=2, max_ctx=24, tp_size=t, tp_rank=rank,
+                             tp_mode=capi.TP_SLICE, seed=SEED)
+            m.set_prompt(prompt)
+            m.prefill()
+            m.step(6)
+            torch.cuda.synchronize()
+            _, hist = m.read_tokens()
+            hists.append(hist[:, 6:12].copy())
+            m.close()
+        assert np.array_equal(hists[0], hists[1])
+        lo, hi = rank * vl, min(V, (rank + 1) * vl)
+        assert ((hists[0] >= lo) & (hists[0] < hi)).all(), (rank, hists[0])

@@ -4,7 +4,7 @@ runs it): for each launch kind, the mean of
   pro      dependency release -> last CTA's prologue end
   loop     last prologue end -> last main-loop end
   epi      last main-loop end -> last CTA end
-python tools/phase_trace.py [cfg] [fp16|int8] [B]"""
+python tools/phase_trace.py [cfg] [fp16|int8|w8a16] [B] [--slice]"""
 import os
 import sys
 
@@ -20,8 +20,9 @@ cfg = args[0] if len(args) > 0 else "gptj-6b"
 dt = args[1] if len(args) > 1 else "fp16"
 B = int(args[2]) if len(args) > 2 else 1
 p = PRESETS[cfg]
+sl = dict(tp_size=p.tp, tp_rank=0, tp_mode=capi.TP_SLICE) if "--slice" in sys.argv else {}  # rank 0 of a TP config
 m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt in ("int8", "w8a16") else 2, batch=B, max_ctx=192,
-                 int8_act=1 if dt == "w8a16" else 0)
+                 int8_act=1 if dt == "w8a16" else 0, **sl)
 m.set_prompt(np.random.default_rng(0).integers(0, p.vocab, (B, 128)).astype(np.int32))
 m.step(128)
 tr = m.launch_trace(8).astype(np.float64)  # [steps][n][6]
