@@ -144,7 +144,7 @@ def test_context_capacity_is_enforced():
     m.close()
 
 
-# Both GEMM plans on both sides of the default batch threshold (gemm::kXsMinBatch = 4):
+# Both GEMM plans on both sides of the default batch threshold (gemm::kXsMinBatch = 2):
 #   xs:    x streamed by TMA per stage (row_prep launches for LayerNorm / int8 quantisation)
 #   slice: x normalised / quantised into a per-CTA smem slice by the GEMM prologue
 PLANS = {"xs": {"DSINF_XS": "1", "DSINF_XS_OD": "1"}, "slice": {"DSINF_XS": "0", "DSINF_XS_OD": "0"}}
