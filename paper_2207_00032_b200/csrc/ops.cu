@@ -1,5 +1,6 @@
 // Non-GEMM device operators: synthetic weight init / packing / quantisation, decode
 // attention over the KV cache, embedding, greedy argmax and the single-device shard reduce.
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 
@@ -324,42 +325,78 @@ __device__ __forceinline__ uint32_t prep_q(float y, float s) {
   return static_cast<uint32_t>(q) & 0xffu;
 }
 
+// Cluster-wide (S CTAs of one row) integer sums and float max, in rank order; `slot` is this
+// CTA's smem exchange word(s).  S == 1: the CTA's own values.
+__device__ __forceinline__ void prep_cluster_sum2(long long& a, long long& b, long long* slot, int S) {
+  if (S == 1) return;
+  if (threadIdx.x == 0) {
+    slot[0] = a;
+    slot[1] = b;
+  }
+  ptx::cluster_sync();
+  a = b = 0;
+  for (int q = 0; q < S; ++q) {
+    const uint32_t ad = ptx::map_shared_rank(slot, q);
+    const uint2 u0 = ptx::ld_dsmem_u2(ad), u1 = ptx::ld_dsmem_u2(ad + 8);
+    a += static_cast<long long>((static_cast<unsigned long long>(u0.y) << 32) | u0.x);
+    b += static_cast<long long>((static_cast<unsigned long long>(u1.y) << 32) | u1.x);
+  }
+}
+__device__ __forceinline__ float prep_cluster_max(float m, float* slot, int S) {
+  if (S == 1) return m;
+  if (threadIdx.x == 0) *slot = m;
+  ptx::cluster_sync();
+  for (int q = 0; q < S; ++q) m = fmaxf(m, ptx::ld_dsmem_f_nc(ptx::map_shared_rank(slot, q)));
+  return m;
+}
+
+// One row per cluster of S = gridDim.x CTAs (S = 1 for short rows): CTA r owns the float4 columns
+// r*kPrepThreads + tid + u*kPrepThreads*S; row sums and maxima are exchanged through DSMEM.
 __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_constant__ PrepParams p) {
   ptx::trace_begin(p.trace);
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const int b = blockIdx.x;
+  const int b = blockIdx.y;
+  const int S = gridDim.x;
+  const int c0 = blockIdx.x * kPrepThreads + threadIdx.x, cs = kPrepThreads * S;
   const int K4 = p.K / 4;
   __shared__ float red[kPrepThreads / 32];
+  __shared__ long long xsum[2];
+  __shared__ float xmax[2];
+  auto block_max = [&](float mx) {
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < kPrepThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+    return mx;
+  };
   if (p.mode == PREP_QUANT_I8) {
     float mx = 0.f;
     if (p.amax != nullptr) {
       for (int s = 0; s < gemm::kStatStripes; ++s) mx = fmaxf(mx, __uint_as_float(__ldcg(p.amax + s * 32 + b)));
     } else {  // row max computed here (large-batch path: rows beyond the producer's stripes)
       const uint2* row2 = reinterpret_cast<const uint2*>(p.x + static_cast<size_t>(b) * p.x_ld);
-      for (int c = threadIdx.x; c < K4; c += kPrepThreads) {
+      for (int c = c0; c < K4; c += cs) {
         const uint2 u = __ldcg(row2 + c);
         const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x), h23 = *reinterpret_cast<const __half2*>(&u.y);
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(__low2float(h01)), fabsf(__high2float(h01))),
                              fmaxf(fabsf(__low2float(h23)), fabsf(__high2float(h23)))));
       }
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-      __syncthreads();
-      mx = red[0];
-      for (int w = 1; w < kPrepThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+      mx = prep_cluster_max(block_max(mx), &xmax[0], S);
     }
     const float scale = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
-    if (threadIdx.x == 0) p.out_scale[b] = scale;
+    if (threadIdx.x == 0 && blockIdx.x == 0) p.out_scale[b] = scale;
     const __half* row = p.x + static_cast<size_t>(b) * p.x_ld;
     uint32_t* out = reinterpret_cast<uint32_t*>(static_cast<int8_t*>(p.out) + static_cast<size_t>(b) * p.K);
 #pragma unroll 4
-    for (int c = threadIdx.x; c < K4; c += kPrepThreads) {
+    for (int c = c0; c < K4; c += cs) {
       const uint2 u = __ldcg(reinterpret_cast<const uint2*>(row) + c);
       const __half2 h01 = *reinterpret_cast<const __half2*>(&u.x), h23 = *reinterpret_cast<const __half2*>(&u.y);
       out[c] = prep_q(__low2float(h01), scale) | (prep_q(__high2float(h01), scale) << 8) |
                (prep_q(__low2float(h23), scale) << 16) | (prep_q(__high2float(h23), scale) << 24);
     }
+    if (S > 1 && p.amax == nullptr) ptx::cluster_sync_relaxed();  // peers' DSMEM reads of xmax are done
     ptx::trace_end(p.trace);
     return;
   }
@@ -374,7 +411,7 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
   long long s1 = 0, s2 = 0;
 #pragma unroll
   for (int u = 0; u < kPrepVec; ++u) {
-    const int c = threadIdx.x + u * kPrepThreads;
+    const int c = c0 + u * cs;
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < K4) {
       v[u] = __ldcg(reinterpret_cast<const float4*>(p.res + rb) + c);
@@ -417,7 +454,7 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
       s1 += __ldcg(p.ln_stats + (s * gemm::kMaxB + b) * 2);
       s2 += __ldcg(p.ln_stats + (s * gemm::kMaxB + b) * 2 + 1);
     }
-  } else {  // integer block sum: exact, order-independent
+  } else {  // integer block (then cluster) sum: exact, order-independent
     for (int o = 16; o > 0; o >>= 1) {
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       s2 += __shfl_xor_sync(0xffffffffu, s2, o);
@@ -432,6 +469,7 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
       s1 += lred[0][w];
       s2 += lred[1][w];
     }
+    prep_cluster_sum2(s1, s2, xsum, S);
   }
   float mean, rstd;
   gemm::dev::ln_mean_rstd(s1, s2, p.inv_k, p.eps, mean, rstd);
@@ -439,7 +477,7 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
   float mx = 0.f;
 #pragma unroll
   for (int u = 0; u < kPrepVec; ++u) {
-    const int c = threadIdx.x + u * kPrepThreads;
+    const int c = c0 + u * cs;
     if (c < K4) {
       const uint2 g = *reinterpret_cast<const uint2*>(p.ln_g + 4 * c);
       const uint2 be = *reinterpret_cast<const uint2*>(p.ln_b + 4 * c);
@@ -459,29 +497,27 @@ __global__ void __launch_bounds__(kPrepThreads) row_prep_kernel(const __grid_con
     uint2* out = reinterpret_cast<uint2*>(static_cast<__half*>(p.out) + static_cast<size_t>(b) * p.K);
 #pragma unroll
     for (int u = 0; u < kPrepVec; ++u) {
-      const int c = threadIdx.x + u * kPrepThreads;
+      const int c = c0 + u * cs;
       if (c < K4) out[c] = hv[u];
     }
+    if (S > 1 && !p.ln_stats) ptx::cluster_sync_relaxed();  // peers' DSMEM reads of xsum are done
     ptx::trace_end(p.trace);
     return;
   }
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  mx = red[0];
-  for (int w = 1; w < kPrepThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  mx = prep_cluster_max(block_max(mx), &xmax[1], S);
   const float scale = mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f;
-  if (threadIdx.x == 0) p.out_scale[b] = scale;
+  if (threadIdx.x == 0 && blockIdx.x == 0) p.out_scale[b] = scale;
   uint32_t* out = reinterpret_cast<uint32_t*>(static_cast<int8_t*>(p.out) + static_cast<size_t>(b) * p.K);
 #pragma unroll
   for (int u = 0; u < kPrepVec; ++u) {
-    const int c = threadIdx.x + u * kPrepThreads;
+    const int c = c0 + u * cs;
     if (c < K4) {
       const __half2 h01 = *reinterpret_cast<const __half2*>(&hv[u].x), h23 = *reinterpret_cast<const __half2*>(&hv[u].y);
       out[c] = prep_q(__low2float(h01), scale) | (prep_q(__high2float(h01), scale) << 8) |
                (prep_q(__low2float(h23), scale) << 16) | (prep_q(__high2float(h23), scale) << 24);
     }
   }
+  if (S > 1) ptx::cluster_sync_relaxed();  // peers' DSMEM reads of xmax are done
   ptx::trace_end(p.trace);
 }
 
@@ -507,7 +543,24 @@ void row_prep(const PrepParams& p_in, cudaStream_t s, bool pdl) {
     throw ConfigError("row_prep: LayerNorm rows must be <= 16384 wide");
   if (p.mode == PREP_QUANT_I8 && (p.x_ld % 4 != 0 || (reinterpret_cast<uintptr_t>(p.x) & 7) != 0))
     throw ConfigError("row_prep: x rows must be 8-byte aligned");
-  launch_pdl(row_prep_kernel, dim3(p.B), dim3(kPrepThreads), 0, s, pdl, p);
+  // CTAs per row (a cluster): one SM's L2 request rate bounds a single-CTA pass over a long row.
+  // Measured (GPT-J, GPT3-175B t=8 rank): best S = 8 at B=1 (h=12288: 9.70 -> 8.89 ms fp16),
+  // 4 at B=4 (2.91 -> 2.78 ms), 2 at B=16 (3.15 -> 3.09 ms fp16, 2.67 -> 2.58 int8); at least
+  // 128 float4 per CTA.  DSINF_PREP_SPLIT overrides.
+  const char* fv = std::getenv("DSINF_PREP_SPLIT");  // read at enqueue / graph capture time only
+  const int forced = fv ? std::atoi(fv) : 0;
+  int S = 1;
+  if (forced > 0) {
+    S = forced;
+  } else {
+    S = 8;
+    while (S > 2 && p.B * S > 16) S >>= 1;
+    // long LayerNorm rows (two float4 streams per column): <= 1024 float4 per CTA (175B B=16: 10.44 -> 10.13)
+    while (p.mode != PREP_QUANT_I8 && S < 8 && p.K / 4 / S > 1024) S <<= 1;
+    while (S > 1 && p.K / 4 / S < 128) S >>= 1;
+  }
+  if (S != 1 && S != 2 && S != 4 && S != 8) throw ConfigError("row_prep: split must be 1, 2, 4 or 8");
+  launch_pdl(row_prep_kernel, dim3(S, p.B), dim3(kPrepThreads), 0, s, pdl, p, dim3(S, 1, 1));
 }
 
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s) {

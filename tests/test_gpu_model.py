@@ -337,3 +337,13 @@ def test_tp_slice_mode(dtype_bytes):
         assert np.array_equal(hists[0], hists[1])
         lo, hi = rank * vl, min(V, (rank + 1) * vl)
         assert ((hists[0] >= lo) & (hists[0] < hi)).all(), (rank, hists[0])
+
+
+@pytest.mark.parametrize("split", [2, 8])
+@pytest.mark.parametrize("dtype_bytes,tp", [(2, 1), (1, 1), (2, 2), (1, 2)], ids=["f16", "i8", "f16tp2", "i8tp2"])
+def test_row_prep_cluster_split(monkeypatch, split, dtype_bytes, tp):
+    """row_prep with each row split over a cluster of CTAs (row sums / maxima exchanged through
+    DSMEM; TP = 2 exercises the sums computed in the kernel) gives the same parity as one CTA."""
+    monkeypatch.setenv("DSINF_PREP_SPLIT", str(split))
+    monkeypatch.setenv("DSINF_XS", "1")
+    run_parity(512, 2, 8, 1000, tp=tp, batch=4, dtype_bytes=dtype_bytes, step_kernel=False)
