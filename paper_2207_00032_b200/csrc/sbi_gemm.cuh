@@ -154,7 +154,9 @@ void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words)
 // Whether x (fp16 [B][x_ld] or int8) can be streamed: alignment of base and row stride.
 bool x_streamable(const void* x, int x_ld, int K, bool int8_x);
 // Batch sizes that use the x-streaming plan (DSINF_XS=0 never, =1 always; default B >= kXsMinBatch).
-constexpr int kXsMinBatch = 2;  // GPT-J: B=2 fp16 2.98 -> 2.87 ms, int8 2.24 -> 2.11; B=1 stays on the slice plan
+// Measured with the cluster-split row_prep: x-streaming wins at every batch (GPT-J B=1 fp16 2.75 ->
+// 2.71 ms, int8 2.04 -> 1.98; GPT-2 int8 1.74 -> 1.60; B=2 fp16 2.98 -> 2.75)
+constexpr int kXsMinBatch = 1;
 // `tp`: the layer's LayerNorm input is an all-reduced sum (TP > 1), so its row statistics cannot
 // come from the producing GEMM's epilogue: one row_prep launch + x-streaming beats every CTA
 // re-deriving them (GPT3-175B t=8 rank slice at B = 1: 12.8 -> 9.7 ms fp16, 10.3 -> 7.4 ms int8)
