@@ -111,6 +111,12 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (carveout_max()) {
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
+  configure_step_kernels();
 }
 
 void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl) {

@@ -534,6 +534,22 @@ __global__ void local_allreduce_kernel(const __grid_constant__ LocalReduceParams
 
 }  // namespace
 
+bool carveout_max() {
+  const char* v = std::getenv("DSINF_CARVEOUT");
+  return v == nullptr || std::atoi(v) != 0;
+}
+
+// The small step kernels ask for the maximum shared-memory carveout like the GEMMs: an SM whose
+// L1/shared split was set for a low-smem kernel cannot take a GEMM CTA (PDL-launched next to it)
+// until it drains and reconfigures.
+void configure_step_kernels() {
+  if (!carveout_max()) return;
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(row_prep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(embed_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(local_allreduce_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+
 void row_prep(const PrepParams& p_in, cudaStream_t s, bool pdl) {
   PrepParams p = p_in;
   p.inv_k = 1.0 / static_cast<double>(p.K);

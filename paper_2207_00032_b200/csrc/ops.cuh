@@ -55,6 +55,8 @@ struct AttnParams {
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
 void configure();
+bool carveout_max();            // DSINF_CARVEOUT=0 leaves the driver's default L1/shared split
+void configure_step_kernels();  // called by configure()
 void attention(const AttnParams& p, int chunks, cudaStream_t s, bool pdl);
 
 // Row preparation for the x-streaming GEMM plan (large batch): one CTA per batch row writes the

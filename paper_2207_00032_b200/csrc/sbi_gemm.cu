@@ -385,6 +385,7 @@ template <bool kInt8, int kNB8, bool kXS, bool kA16 = false>
 void configure_one() {
   auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
