@@ -383,8 +383,11 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
     Launches overlap (programmatic dependent launch starts a GEMM's CTAs, and their weight prefetch,
     while the previous kernel still runs), so each launch is charged the INTERVAL from the previous
     launch's last-CTA end to its own last-CTA end: the intervals tile the step exactly, with no
-    double counting.  `achieved` = SBI-GeMM algorithmic bytes / SBI-GeMM intervals.  The
-    first-CTA-start -> last-CTA-end span is reported beside it.  Returns (GB/s, table) or None."""
+    double counting.  `achieved` = SBI-GeMM algorithmic bytes / (SBI-GeMM intervals + the row_prep
+    intervals: those launches exist only to feed the x-streamed GEMMs, and the GEMMs prefetch their
+    first ring stages under them, so charging the GEMMs alone would overstate them).  The GEMM-only
+    figure and the first-CTA-start -> last-CTA-end spans are reported beside it.
+    Returns (GB/s, table) or None."""
     from paper_2207_00032_b200 import _capi as capi
 
     tr = model.launch_trace(steps, stream=stream).astype(np.float64)
@@ -397,7 +400,7 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
     span = float(np.median((tr[:, -1, 1] - tr[:, 0, 0]) / 1e3))
     layer, lm = gemm_shapes(preset, tp)
     shapes = {n: (N, K) for n, N, K in layer + [lm]}
-    tot_b = tot_us = 0.0
+    tot_b = tot_us = prep_us = 0.0
     table = {}
     for k in dict.fromkeys(kinds):
         idx = [i for i, kk in enumerate(kinds) if kk == k]
@@ -412,10 +415,14 @@ def insitu_roofline(model, preset, tp, batch, dtype, peak_gbs, stream, steps=8):
             row["frac"] = round(row["gbs"] / peak_gbs, 4)
             tot_b += b * iv.size
             tot_us += float(iv.sum())
+        elif k == "prep":
+            prep_us += float(iv.sum())
         table[k] = row
     if tot_us == 0:
         return None
-    return tot_b / (tot_us * 1e-6) / 1e9, {"step_span_us": round(span, 1), "kinds": table}
+    gemm_only = tot_b / (tot_us * 1e-6) / 1e9
+    return tot_b / ((tot_us + prep_us) * 1e-6) / 1e9, {"step_span_us": round(span, 1),
+                                                        "gemm_only_gbs": round(gemm_only, 1), "kinds": table}
 
 
 def run_ours(args, preset, rank, world, local_rank):
@@ -560,9 +567,9 @@ def run_ours(args, preset, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(agg, 1), "peak": peak_gbs, "unit": "GB/s",
                 "frac": round(agg / peak_gbs, 4), "traffic": traffic, "traffic_launch": traffic_note,
                 "peak_kind": peak_kind,
-                "kernel": ("sbi_gemm_kernel: algorithmic bytes of every SBI-GeMM launch of 8 decode steps over the "
-                           "device-timeline intervals they own (previous launch's last-CTA end -> own last-CTA "
-                           "end, globaltimer)"
+                "kernel": ("sbi_gemm_kernel (+ the row_prep launches that feed it): algorithmic bytes of every "
+                           "SBI-GeMM launch of 8 decode steps over the device-timeline intervals the GEMMs and "
+                           "their row_preps own (previous launch's last-CTA end -> own last-CTA end, globaltimer)"
                            if insitu else "sbi_gemm_kernel (byte-weighted over one step's GEMM launches, timed alone)"),
                 "in_step": insitu[1] if insitu else None,
                 "alone": {"achieved": round(agg_alone, 1), "per_kernel": per_kernel},
