@@ -243,12 +243,19 @@ def run_reference(args, preset, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def auto_act(batch, tp):
+    """The per-GEMM INT8 activation modes DSINF_INT8_AUTO picks (model.cu, dsinf_model_create)."""
+    if batch <= 8:
+        return "w8a16"
+    return "w8a8 qkv + w8a16 attn_out/mlp" if tp == 1 else "w8a8"
+
+
 def workload_config(args, preset, world):
     cfg = {"workload": f"{preset.name} {args.dtype} greedy decode, batch {args.batch}, {args.prompt}-token prompt, "
                        f"TP={world}", "model": args.config, "global_batch": args.batch, "seq_len": args.prompt,
            "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
     if args.dtype == "int8":
-        cfg["int8_act"] = (("w8a16" if args.batch <= 8 else "w8a8") if args.int8_act == "auto" else args.int8_act)
+        cfg["int8_act"] = auto_act(args.batch, world) if args.int8_act == "auto" else args.int8_act
     return cfg
 
 
@@ -281,7 +288,7 @@ def decode_sweep(E, capi, torch, preset, args, stream, peak_gbs, skip):
             ms = a.elapsed_time(b)
             pos0 = args.prompt + args.warmup
             gb = sum(m.bytes_per_step(q) for q in range(pos0, pos0 + args.steps)) / (ms * 1e-3) / 1e9
-            mode = (("w8a16" if batch <= 8 else "w8a8") if args.int8_act == "auto" else args.int8_act) \
+            mode = (auto_act(batch, 1) if args.int8_act == "auto" else args.int8_act) \
                 if dtype == "int8" else None
             rows.append({"dtype": dtype, "batch": batch, "int8_act": mode, "ms_per_token": round(ms / args.steps, 4),
                          "tokens_per_s": round(batch * args.steps * 1e3 / ms, 1), "step_gbs": round(gb, 1),

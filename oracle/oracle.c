@@ -475,6 +475,9 @@ static void gemm8_a16(const int8_t* W, const float* ws, int64_t N, int64_t K, co
     }
 }
 
+/* Activation mode of layer GEMM g (0 QKV, 1 attn-out, 2 MLP-up, 3 MLP-down). */
+static int act_of(int int8_act, int g) { return (int8_act & 0x100) ? (int8_act >> g) & 1 : int8_act; }
+
 /* int8 path GEMM on fp16 activations: per-token quantisation, exact int32, fp32 dequant
  * (int8_act 1: weight-only, fp16 activations) */
 static void gemm8(int int8_act, const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B,
@@ -529,7 +532,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
       const int64_t Nq = 3 * Hl * d;
       /* K1: QKV + bias + RoPE + KV append */
       if (!i8) gemm16(w->wqkv, Nq, h, sm, xln, B, yd);
-      else gemm8(m->c.int8_act, w->qqkv, w->sqkv, Nq, h, xln, B, yf);
+      else gemm8(act_of(m->c.int8_act, 0), w->qqkv, w->sqkv, Nq, h, xln, B, yf);
       for (int64_t b = 0; b < B; ++b)
         for (int64_t n = 0; n < Nq; n += 2) {
           const int64_t sec = n / (Hl * d), rem = n % (Hl * d), hh = rem / d, i = rem % d;
@@ -607,7 +610,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wo, h, Hl * d, sm, xa, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(m->c.int8_act, w->qo, w->so, h, Hl * d, xa, B, yf);
+        gemm8(act_of(m->c.int8_act, 1), w->qo, w->so, h, Hl * d, xa, B, yf);
       }
       for (int64_t i = 0; i < B * h; ++i) dsum[i] = rk == 0 ? yf[i] : dsum[i] + yf[i];
       free(xa);
@@ -629,7 +632,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
           for (int64_t n = 0; n < Fl; ++n)
             u16[b * Fl + n] = f16r((float)gelu_tanh(yd[b * Fl + n] + ly->bup[rk * Fl + n]));
       } else {
-        gemm8(m->c.int8_act, w->qup, w->sup, Fl, h, xln, B, yf);
+        gemm8(act_of(m->c.int8_act, 2), w->qup, w->sup, Fl, h, xln, B, yf);
         for (int64_t b = 0; b < B; ++b)
           for (int64_t n = 0; n < Fl; ++n) {
             const float y = yf[b * Fl + n] + ly->bup[rk * Fl + n];
@@ -641,7 +644,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wdown, h, Fl, sm, u16, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(m->c.int8_act, w->qdown, w->sdown, h, Fl, u16, B, yf);
+        gemm8(act_of(m->c.int8_act, 3), w->qdown, w->sdown, h, Fl, u16, B, yf);
       }
       for (int64_t i = 0; i < B * h; ++i) dm[i] = rk == 0 ? yf[i] : dm[i] + yf[i];
     }

@@ -1216,11 +1216,13 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     require(rt->int8_act == DSINF_INT8_W8A8 || rt->int8_act == DSINF_INT8_W8A16 || rt->int8_act == DSINF_INT8_AUTO,
             "unknown int8_act");
     // INT8 activation mode per GEMM (mask): W8A8 everywhere, W8A16 everywhere, or AUTO -- measured
-    // on B200 (GPT-J): W8A16 everywhere is faster up to B = 8 (1.04x at B=1, 1.07x at B=8), W8A8 at
-    // B = 16; mixed masks measured slower (DSINF_A16_MASK overrides for experiments)
+    // on B200 with the x-streaming plans: W8A16 everywhere up to B = 8 (GPT-J B=8 2.40 -> 2.20 ms);
+    // at B = 16 W8A8 QKV + W8A16 attn-out / MLP at TP = 1 (GPT-J 2.62 -> 2.55, GPT-2 2.44 -> 2.35),
+    // W8A8 everywhere at TP > 1 (175B t=8 rank 8.04 vs 8.23, NeoX t=2 3.84 vs 4.05).
+    // DSINF_A16_MASK overrides for experiments.
     if (m->int8) {
       if (rt->int8_act == DSINF_INT8_W8A16) m->a16_mask = 0xf;
-      else if (rt->int8_act == DSINF_INT8_AUTO) m->a16_mask = rt->batch <= 8 ? 0xf : 0x0;
+      else if (rt->int8_act == DSINF_INT8_AUTO) m->a16_mask = rt->batch <= 8 ? 0xf : (m->t == 1 ? 0xe : 0x0);
       if (const char* am = std::getenv("DSINF_A16_MASK")) m->a16_mask = static_cast<int>(std::strtol(am, nullptr, 0)) & 0xf;
     }
     m->a16 = m->a16_mask != 0;

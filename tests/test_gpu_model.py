@@ -306,9 +306,10 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
     assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(lb).max()) + 1e-4
 
 
-@pytest.mark.parametrize("batch,oracle_act", [(1, 1), (8, 1), (16, 0)])
+@pytest.mark.parametrize("batch,oracle_act", [(1, 1), (8, 1), (16, 0x10e)])
 def test_int8_auto_mode_matches_oracle(batch, oracle_act):
-    """DSINF_INT8_AUTO: weight-only up to batch 8, W8A8 above -- each against the oracle's same mode."""
+    """DSINF_INT8_AUTO: weight-only up to batch 8; above, W8A8 QKV + weight-only attn-out / MLP
+    (TP = 1) -- each against the oracle's same per-GEMM modes."""
     run_parity(256, 2, 4, 1000, batch=batch, dtype_bytes=1, int8_act=capi.INT8_AUTO, step_kernel=False,
                oracle_int8_act=oracle_act)
 
@@ -347,3 +348,17 @@ def test_row_prep_cluster_split(monkeypatch, split, dtype_bytes, tp):
     monkeypatch.setenv("DSINF_PREP_SPLIT", str(split))
     monkeypatch.setenv("DSINF_XS", "1")
     run_parity(512, 2, 8, 1000, tp=tp, batch=4, dtype_bytes=dtype_bytes, step_kernel=False)
+
+
+def test_int8_auto_mode_tp_matches_oracle():
+    """DSINF_INT8_AUTO at TP > 1 and batch 16: W8A8 everywhere."""
+    run_parity(256, 2, 4, 1000, batch=16, dtype_bytes=1, tp=2, int8_act=capi.INT8_AUTO, step_kernel=False,
+               oracle_int8_act=0)
+
+
+@pytest.mark.parametrize("mask", [0x5, 0xa])
+def test_int8_mixed_mask_matches_oracle(monkeypatch, mask):
+    """Per-GEMM activation modes (DSINF_A16_MASK) against the oracle's per-GEMM mask."""
+    monkeypatch.setenv("DSINF_A16_MASK", hex(mask))
+    run_parity(256, 2, 4, 1000, batch=4, dtype_bytes=1, int8_act=capi.INT8_W8A8, step_kernel=False,
+               oracle_int8_act=0x100 | mask)

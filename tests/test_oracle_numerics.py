@@ -91,3 +91,19 @@ def test_oracle_w8a16_layer_gemm_matches_numpy():
     assert np.abs(la - lb).max() < 0.1 * np.abs(lf).max()
     for m in (a, b, f):
         m.close()
+
+
+def test_oracle_per_gemm_act_mask():
+    """int8_act = 0x100 | mask selects W8A16 per layer GEMM: an all-set mask equals mode 1, an empty
+    mask equals mode 0 (bit for bit), and a mixed mask differs from both."""
+    import numpy as np
+    from oracle import oracle as O
+    toks = np.array([3, 7], dtype=np.int32)
+    out = {}
+    for act in (0, 1, 0x100, 0x10f, 0x105):
+        m = O.OracleModel(128, 2, 4, 300, dtype_bytes=1, batch=2, max_ctx=8, int8_act=act)
+        out[act], _ = m.step(toks, 0)
+        m.close()
+    assert np.array_equal(out[0], out[0x100])
+    assert np.array_equal(out[1], out[0x10f])
+    assert not np.array_equal(out[0x105], out[0]) and not np.array_equal(out[0x105], out[1])
