@@ -376,7 +376,7 @@ void configure_prefill() {
 
 void prefill_attention(const PrefillAttnParams& p, cudaStream_t s) {
   if (p.d % 32 != 0 || p.d > 32 * kMaxDimsPerLane) throw ConfigError("prefill attention: head dim must be a multiple of 32, <= 256");
-  const bool use_mma = !std::getenv("DSINF_PREFILL_SIMT") && (p.d == 64 || p.d == 96 || p.d == 128);
+  const bool use_mma = !std::getenv("DSINF_PREFILL_SIMT") && (p.d == 64 || p.d == 96 || p.d == kFMaxD);
   if (use_mma) {
     const dim3 grid((p.P + kFQ - 1) / kFQ, p.H, p.B);
     const size_t sm = prefill_mma_smem(p.d);

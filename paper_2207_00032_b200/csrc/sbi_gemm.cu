@@ -162,7 +162,6 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     const unsigned long long t_rel = ptx::trace_release(p.trace, 32);
     const long long c_rel = ptx::clk();
 #else
-    constexpr unsigned long long t_rel = 0;
     constexpr long long c_rel = 0;
 #endif
     if (clog && threadIdx.x == 32) clog[2] = ptx::gtimer();
