@@ -1234,7 +1234,12 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // x-streaming plans need 16-byte rows of GEMM-ready x
       const int64_t Fl = 4 * m->h / m->t, Ol = m->h / m->t;
       const bool rows16 = m->q8() ? (m->h % 16 == 0 && Fl % 16 == 0 && Ol % 16 == 0) : (Ol % 8 == 0 && Fl % 8 == 0);
-      m->xs_ln = rows16 && gemm::prefer_x_stream(m->B, m->t > 1);
+      // a fused all-reduce request (below) selects the slice plan: its slots are summed by the
+      // per-CTA LayerNorm prologues
+      const char* far_req = std::getenv("DSINF_FUSED_AR");
+      const bool want_far = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) &&
+                            far_req != nullptr && std::atoi(far_req) != 0;
+      m->xs_ln = rows16 && !want_far && gemm::prefer_x_stream(m->B, m->t > 1);
       const char* od = std::getenv("DSINF_XS_OD");
       const int od_v = od ? std::atoi(od) : -1;
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
@@ -1242,7 +1247,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
       // fused all-reduce: on-device shards (DSINF_TP_LOCAL) for now -- across processes the slots
       // would be CUDA-IPC peer mappings (not exercised on a one-GPU box); the per-CTA LayerNorm
-      // prologue path (B <= 3) consumes the slots, the row_prep path handles the LM head
+      // prologue path (slice plan, DSINF_XS=0) consumes the slots, the row_prep path handles the LM head
       const char* far = std::getenv("DSINF_FUSED_AR");
       // opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
       // consumer CTA re-reads t slots), the win is hiding the NVLink exchange across GPUs

@@ -291,16 +291,18 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
     identical greedy tokens, logits within fp32 summation-order noise."""
     rng = np.random.default_rng(5)
     prompt = rng.integers(0, 1000, (2, 6)).astype(np.int32)
-    outs = []
+    outs, launches = [], []
     for fused in ("1", "0"):
+        # no DSINF_XS here: the fused request itself selects the slice plan it needs
         monkeypatch.setenv("DSINF_FUSED_AR", fused)
-        monkeypatch.setenv("DSINF_XS", "0")
         m = DecoderModel(512, 2, 8, 1000, batch=2, max_ctx=24, tp_size=4, tp_mode=capi.TP_LOCAL, seed=SEED)
         m.set_prompt(prompt)
         m.step(10)
         torch.cuda.synchronize()
         outs.append((m.full_logits(), m.read_tokens()[1]))
+        launches.append(m.get_info().kernels_per_step)
         m.close()
+    assert launches[0] < launches[1], launches  # the fused path has no all-reduce / row_prep launches
     (la, ha), (lb, hb) = outs
     assert np.array_equal(ha, hb)
     assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(lb).max()) + 1e-4
