@@ -103,10 +103,14 @@ int dsinf_unpack_weights_f64(const double* packed, int64_t packed_len,
 /* infersim::exec_reference (gemm.hpp:147-202) executed on the GPU.
  * Host fp64 in/out like the reference; the device computes in `compute_dtype`
  * (DSINF_DT_F16: fp16 operands, fp32 accumulate; DSINF_DT_I8: W8A8 int32 accumulate).
- * `packed` is the reference layout produced by pack_weights with schedule->pack_M. */
-int dsinf_exec_device(const double* packed, int64_t packed_len, const dsinf_gemm_shape* shape,
-                      const dsinf_gemm_schedule* schedule, const double* x, int64_t x_len,
-                      int64_t batch, int32_t compute_dtype, double* out, int64_t out_len);
+ * `packed` is the reference layout produced by pack_weights with `packed_pack_M`
+ * (PackedWeights::pack_M): the data is read with that M, as exec_reference reads it with
+ * packed.pack_M; schedule->pack_M only groups the iteration (gemm.hpp:180-183), so any
+ * packed_pack_M in {1, 2, 4} gives the same result under any schedule. */
+int dsinf_exec_device(const double* packed, int64_t packed_len, int32_t packed_pack_M,
+                      const dsinf_gemm_shape* shape, const dsinf_gemm_schedule* schedule,
+                      const double* x, int64_t x_len, int64_t batch, int32_t compute_dtype,
+                      double* out, int64_t out_len);
 
 /* ---- device-resident SBI-GeMM (the decode hot path; pointers are device pointers) */
 
@@ -243,7 +247,10 @@ int dsinf_model_set_prompt_device(dsinf_model* m, const int32_t* prompt_dev, int
 /* Prompt prefill in the large-batch regime (fusion.hpp:145-154): all B x P
  * prompt tokens through every layer at once on the tcgen05 tensor cores, leaving the model in the
  * state dsinf_decode_steps(m, P) would (KV cache rows 0..P-1, history, next token, position P).
- * Needs a prompt set at position 0, tp_size 1.  First call generates row-major weight copies. */
+ * Needs a prompt set at position 0.  Every TP mode is supported: TP_NONE, TP_LOCAL and TP_NCCL
+ * give the model's outputs (column-/row-parallel GEMMs, the row-parallel partials all-reduced,
+ * vocab-parallel LM head with the argmax keys gathered); TP_SLICE runs rank tp_rank's shard alone
+ * and its outputs are for timing only.  First call generates row-major weight copies. */
 int dsinf_model_prefill(dsinf_model* m, void* stream);
 int dsinf_decode_step(dsinf_model* m, void* stream);
 /* Enqueue `steps` decode steps back to back. */
@@ -268,7 +275,13 @@ typedef struct dsinf_model_info {
   int64_t kv_bytes;
   int32_t shards;              /* shards resident on this device */
   int32_t graph_ready;
+  int32_t fused_allreduce;     /* 1: row-parallel GEMM epilogues push to the peers' slots (no all-reduce launch) */
+  int32_t plan_flags;          /* DSINF_PLAN_* bits of the decode schedule in use */
 } dsinf_model_info;
+#define DSINF_PLAN_X_STREAM 1     /* LayerNorm'd x written once by row_prep and streamed by TMA */
+#define DSINF_PLAN_FUSED_STATS 2  /* LayerNorm row statistics fused into the producing epilogues */
+#define DSINF_PLAN_STEP_KERNEL 4  /* the persistent whole-step kernel */
+#define DSINF_PLAN_STREAM_KERNEL 8 /* the statically scheduled persistent decode kernel */
 int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out);
 /* Per-CTA phase timeline of the last persistent step (built with DSINF_STEP_TRACE=1):
  * [grid][phases][4] globaltimer ns (wait begins, wait satisfied, phase done, producer's last
@@ -421,6 +434,24 @@ int dsinf_fusion_savings(const dsinf_op_graph* g, const int32_t* region_of, int3
 int dsinf_canonical_layer_partition(int64_t hidden, int64_t batch, int32_t dtype_bytes,
                                     int32_t regime, int32_t region_of[8], int32_t* num_regions,
                                     int64_t* launches_saved, int64_t* bytes_saved);
+
+/* infersim::canonical_layer_graph (fusion.hpp:242-357) as a flattened graph.  Call once with
+ * node_kind == NULL to get num_nodes / num_edges / num_deps / num_prods, then with buffers of
+ * those sizes (dep_off: num_edges + 1, prod_off: num_deps + 1). */
+typedef struct dsinf_graph_buffers {
+  int32_t num_nodes, num_edges, num_deps, num_prods, dtype_bytes;
+  int32_t* node_kind;
+  int32_t* node_tile_count;
+  int64_t* node_out_elems;
+  int32_t* edge_from;
+  int32_t* edge_to;
+  int32_t* dep_off;
+  int32_t* dep_consumer;
+  int32_t* prod_off;
+  int32_t* dep_prod;
+} dsinf_graph_buffers;
+int dsinf_canonical_layer_graph(int64_t hidden, int64_t batch, int32_t dtype_bytes,
+                                dsinf_graph_buffers* out);
 
 #ifdef __cplusplus
 } /* extern "C" */

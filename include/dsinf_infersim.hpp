@@ -16,7 +16,7 @@
 //   packed_index           gemm.hpp:108-111     packed_index
 //   pack_weights           gemm.hpp:113-130     pack_weights
 //   unpack_weights         gemm.hpp:132-139     unpack_weights
-//   exec_reference         gemm.hpp:147-202     exec (same signature; runs SBI-GeMM on the GPU)
+//   exec_reference         gemm.hpp:147-202     exec_reference / exec (same signature; SBI-GeMM on the GPU)
 //   DeviceSpec             hardware.hpp:36-69   DeviceSpec (peak map -> three dtype slots)
 //   ModelConfig            model.hpp:42-64      ModelConfig (dense)
 //   param_count/bytes      model.hpp:93-105     param_count / param_bytes
@@ -24,12 +24,19 @@
 //   kv_cache_bytes         model.hpp:135-140    kv_cache_bytes
 //   KernelCost/kernel_time costmodel.hpp:31-56  KernelCost / kernel_time
 //   min_latency_bound      costmodel.hpp:113-125 min_latency_bound (flat topology arguments)
+//   CollectiveKind/collective_time costmodel.hpp:40,70-104  same (LinkSpec / Topology: the fields it reads)
+//   OpKind/OpNode/GraphEdge/OpGraph fusion.hpp:29-116  same (dims carried as names only)
+//   fusable / BatchRegime / partition_layer fusion.hpp:126-173  same
+//   FusionRegion / FusionSavings / fusion_savings fusion.hpp:118-215  same
+//   canonical_layer_graph  fusion.hpp:242-357   same (built by the library)
 //   ConfigError/InfeasibleError errors.hpp:24-34  same names, rethrown from the ABI return codes
 // plus the decode loop the reference only describes: DecoderSession (dsinf_model_*).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -171,10 +178,16 @@ inline std::vector<double> exec(const PackedWeights& packed, const std::vector<d
   const dsinf_gemm_shape cs = packed.shape.c();
   const dsinf_gemm_schedule sc = schedule.c();
   std::vector<double> out(static_cast<size_t>(batch * packed.shape.out_dim));
-  check(dsinf_exec_device(packed.data.data(), static_cast<std::int64_t>(packed.data.size()), &cs, &sc, x.data(),
+  check(dsinf_exec_device(packed.data.data(), static_cast<std::int64_t>(packed.data.size()), packed.pack_M, &cs, &sc, x.data(),
                           static_cast<std::int64_t>(x.size()), batch, compute_dtype, out.data(),
                           static_cast<std::int64_t>(out.size())));
   return out;
+}
+
+// The reference's name for the same call (gemm.hpp:147): a caller can keep writing exec_reference.
+inline std::vector<double> exec_reference(const PackedWeights& packed, const std::vector<double>& x,
+                                          std::int64_t batch, const GemmSchedule& schedule) {
+  return exec(packed, x, batch, schedule);
 }
 
 // ---------------------------------------------------------------- model.hpp (dense)
@@ -239,6 +252,172 @@ inline double min_latency_bound(const ModelConfig& cfg, int tp, int pp, const ds
   double v = 0;
   check(dsinf_min_latency_bound(&c, tp, pp, &topo, &v));
   return v;
+}
+
+enum class CollectiveKind {  // costmodel.hpp:40
+  allreduce = DSINF_COLL_ALLREDUCE,
+  allgather = DSINF_COLL_ALLGATHER,
+  alltoall = DSINF_COLL_ALLTOALL,
+  broadcast = DSINF_COLL_BROADCAST,
+  p2p = DSINF_COLL_P2P
+};
+struct LinkSpec {  // hardware.hpp:30-34
+  double bandwidth = 0.0;
+  double latency = 0.0;
+};
+struct Topology {  // the fields of hardware.hpp:80-123 collective_time and min_latency_bound read
+  int num_nodes = 1;
+  int gpus_per_node = 1;
+  DeviceSpec device;
+  LinkSpec intra, inter;
+  int device_count() const { return num_nodes * gpus_per_node; }
+  dsinf_topology c() const {
+    return {num_nodes, gpus_per_node, {intra.bandwidth, intra.latency}, {inter.bandwidth, inter.latency}, device.c()};
+  }
+};
+inline double collective_time(CollectiveKind kind, double bytes_per_rank, const std::vector<int>& group,
+                              const Topology& topo) {
+  const std::vector<std::int32_t> g(group.begin(), group.end());
+  const dsinf_topology t = topo.c();
+  double v = 0;
+  check(dsinf_collective_time(static_cast<std::int32_t>(kind), bytes_per_rank, g.data(),
+                              static_cast<std::int32_t>(g.size()), &t, &v));
+  return v;
+}
+inline double min_latency_bound(const ModelConfig& cfg, int tp, int pp, const Topology& topo) {
+  return min_latency_bound(cfg, tp, pp, topo.c());
+}
+
+// ---------------------------------------------------------------- fusion.hpp (Deep-Fusion)
+enum class OpKind {  // fusion.hpp:29
+  elementwise = DSINF_OP_ELEMENTWISE,
+  reduction = DSINF_OP_REDUCTION,
+  transpose = DSINF_OP_TRANSPOSE,
+  gemm = DSINF_OP_GEMM,
+  quantize = DSINF_OP_QUANTIZE
+};
+enum class BatchRegime { small_batch = DSINF_REGIME_SMALL_BATCH, large_batch = DSINF_REGIME_LARGE_BATCH };
+
+struct OpNode {  // fusion.hpp:39-65; legality depends on the tile structure only
+  std::string name;
+  OpKind kind = OpKind::elementwise;
+  std::int64_t out_elems = 0;
+  int tile_count = 1;
+};
+struct GraphEdge {  // fusion.hpp:68-72
+  int from = -1;
+  int to = -1;
+  std::map<int, std::set<int>> tile_dep;  // consumer tile -> producer tiles
+};
+struct OpGraph {  // fusion.hpp:74-116
+  std::vector<OpNode> nodes;
+  std::vector<GraphEdge> edges;
+  int dtype_bytes = 2;
+  std::int64_t edge_bytes(const GraphEdge& e) const { return nodes[e.from].out_elems * dtype_bytes; }
+};
+struct FusionRegion {  // fusion.hpp:118-121
+  std::vector<int> node_ids;
+  int launch_count = 1;
+};
+struct FusionSavings {  // fusion.hpp:175-178
+  std::int64_t launches_saved = 0;
+  std::int64_t bytes_saved = 0;
+};
+
+namespace detail {
+// Keeps the flattened (CSR) image of an OpGraph alive for one C-ABI call.
+struct FlatGraph {
+  std::vector<std::int32_t> kind, tiles, from, to, dep_off{0}, cons, prod_off{0}, prod;
+  std::vector<std::int64_t> elems;
+  dsinf_op_graph c{};
+  explicit FlatGraph(const OpGraph& g) {
+    for (const auto& n : g.nodes) {
+      kind.push_back(static_cast<std::int32_t>(n.kind));
+      tiles.push_back(n.tile_count);
+      elems.push_back(n.out_elems);
+    }
+    for (const auto& e : g.edges) {
+      from.push_back(e.from);
+      to.push_back(e.to);
+      for (const auto& [ct, ps] : e.tile_dep) {
+        cons.push_back(ct);
+        for (int p : ps) prod.push_back(p);
+        prod_off.push_back(static_cast<std::int32_t>(prod.size()));
+      }
+      dep_off.push_back(static_cast<std::int32_t>(cons.size()));
+    }
+    c = {static_cast<std::int32_t>(g.nodes.size()), kind.data(), tiles.data(), elems.data(),
+         static_cast<std::int32_t>(g.edges.size()), from.data(), to.data(), dep_off.data(), cons.data(),
+         prod_off.data(), prod.data(), g.dtype_bytes};
+  }
+};
+}  // namespace detail
+
+inline bool fusable(const OpGraph& graph, const GraphEdge& edge) {  // fusion.hpp:126-133
+  OpGraph one{graph.nodes, {edge}, graph.dtype_bytes};
+  detail::FlatGraph fg(one);
+  std::int32_t out = 0;
+  check(dsinf_fusable(&fg.c, 0, &out));
+  return out != 0;
+}
+inline std::vector<FusionRegion> partition_layer(const OpGraph& graph, BatchRegime regime) {  // fusion.hpp:140-173
+  detail::FlatGraph fg(graph);
+  std::vector<std::int32_t> region_of(std::max<size_t>(1, graph.nodes.size()));
+  std::int32_t nreg = 0;
+  check(dsinf_partition_layer(&fg.c, static_cast<std::int32_t>(regime), region_of.data(), &nreg));
+  std::vector<FusionRegion> regions(static_cast<size_t>(nreg));
+  for (size_t i = 0; i < graph.nodes.size(); ++i) regions[region_of[i]].node_ids.push_back(static_cast<int>(i));
+  return regions;
+}
+inline FusionSavings fusion_savings(const std::vector<FusionRegion>& regions, const OpGraph& graph) {  // :183-215
+  std::vector<std::int32_t> region_of(graph.nodes.size(), -1);
+  size_t covered = 0;
+  for (size_t r = 0; r < regions.size(); ++r)
+    for (int id : regions[r].node_ids) {
+      if (id < 0 || id >= static_cast<int>(graph.nodes.size()) || region_of[id] != -1)
+        throw ConfigError("regions must partition the graph");
+      region_of[id] = static_cast<std::int32_t>(r);
+      ++covered;
+    }
+  if (covered != graph.nodes.size()) throw ConfigError("regions must cover every node");
+  detail::FlatGraph fg(graph);
+  FusionSavings s;
+  check(dsinf_fusion_savings(&fg.c, region_of.data(), static_cast<std::int32_t>(regions.size()), &s.launches_saved,
+                             &s.bytes_saved));
+  return s;
+}
+inline OpGraph canonical_layer_graph(std::int64_t hidden, std::int64_t batch, int dtype_bytes = 2) {  // :242-357
+  static const char* const kNames[] = {"input_layernorm", "qkv_gemm", "attn_transpose", "attention",
+                                       "post_attn_layernorm", "intermediate_gemm", "bias_add", "residual_add"};
+  dsinf_graph_buffers gb{};
+  check(dsinf_canonical_layer_graph(hidden, batch, dtype_bytes, &gb));
+  std::vector<std::int32_t> kind(gb.num_nodes), tiles(gb.num_nodes), from(gb.num_edges), to(gb.num_edges),
+      dep_off(gb.num_edges + 1), cons(std::max(1, gb.num_deps)), prod_off(gb.num_deps + 1),
+      prod(std::max(1, gb.num_prods));
+  std::vector<std::int64_t> elems(gb.num_nodes);
+  gb.node_kind = kind.data();
+  gb.node_tile_count = tiles.data();
+  gb.node_out_elems = elems.data();
+  gb.edge_from = from.data();
+  gb.edge_to = to.data();
+  gb.dep_off = dep_off.data();
+  gb.dep_consumer = cons.data();
+  gb.prod_off = prod_off.data();
+  gb.dep_prod = prod.data();
+  check(dsinf_canonical_layer_graph(hidden, batch, dtype_bytes, &gb));
+  OpGraph g;
+  g.dtype_bytes = gb.dtype_bytes;
+  for (int i = 0; i < gb.num_nodes; ++i)
+    g.nodes.push_back({i < 8 ? kNames[i] : "node", static_cast<OpKind>(kind[i]), elems[i], tiles[i]});
+  for (int e = 0; e < gb.num_edges; ++e) {
+    GraphEdge ge;
+    ge.from = from[e];
+    ge.to = to[e];
+    for (int c = dep_off[e]; c < dep_off[e + 1]; ++c)
+      ge.tile_dep[cons[c]] = std::set<int>(prod.begin() + prod_off[c], prod.begin() + prod_off[c + 1]);
+    g.edges.push_back(std::move(ge));
+  }
+  return g;
 }
 
 // ---------------------------------------------------------------- the decode loop (new)

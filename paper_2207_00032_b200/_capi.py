@@ -121,7 +121,8 @@ class RuntimeConfig(C.Structure):
 class ModelInfo(C.Structure):
     _fields_ = [("weight_bytes", C.c_int64), ("bytes_per_token", C.c_int64), ("kernels_per_step", C.c_int64),
                 ("vocab_local", C.c_int64), ("heads_local", C.c_int64), ("kv_bytes", C.c_int64),
-                ("shards", C.c_int32), ("graph_ready", C.c_int32)]
+                ("shards", C.c_int32), ("graph_ready", C.c_int32), ("fused_allreduce", C.c_int32),
+                ("plan_flags", C.c_int32)]
 
 
 class KernelCost(C.Structure):
@@ -146,6 +147,16 @@ class OpGraph(C.Structure):
                 ("prod_off", C.POINTER(C.c_int32)), ("dep_prod", C.POINTER(C.c_int32)), ("dtype_bytes", C.c_int32)]
 
 
+class GraphBuffers(C.Structure):
+    _fields_ = [("num_nodes", C.c_int32), ("num_edges", C.c_int32), ("num_deps", C.c_int32),
+                ("num_prods", C.c_int32), ("dtype_bytes", C.c_int32),
+                ("node_kind", C.POINTER(C.c_int32)), ("node_tile_count", C.POINTER(C.c_int32)),
+                ("node_out_elems", C.POINTER(C.c_int64)), ("edge_from", C.POINTER(C.c_int32)),
+                ("edge_to", C.POINTER(C.c_int32)), ("dep_off", C.POINTER(C.c_int32)),
+                ("dep_consumer", C.POINTER(C.c_int32)), ("prod_off", C.POINTER(C.c_int32)),
+                ("dep_prod", C.POINTER(C.c_int32))]
+
+
 P = C.POINTER
 vp = C.c_void_p
 i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
@@ -161,7 +172,7 @@ SIGNATURES = {
     "dsinf_packed_index": (i64, [i64, i64, i64, i32]),
     "dsinf_pack_weights_f64": (C.c_int, [P(f64), i64, P(GemmShape), i32, P(f64), i64, P(i64)]),
     "dsinf_unpack_weights_f64": (C.c_int, [P(f64), i64, P(GemmShape), i32, P(f64), i64]),
-    "dsinf_exec_device": (C.c_int, [P(f64), i64, P(GemmShape), P(GemmSchedule), P(f64), i64, i64, i32, P(f64), i64]),
+    "dsinf_exec_device": (C.c_int, [P(f64), i64, i32, P(GemmShape), P(GemmSchedule), P(f64), i64, i64, i32, P(f64), i64]),
     "dsinf_pack_weights_device": (C.c_int, [vp, i32, i64, i64, i32, vp, vp]),
     "dsinf_quantize_weights_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
     "dsinf_quantize_activations_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
@@ -203,6 +214,7 @@ SIGNATURES = {
     "dsinf_partition_layer": (C.c_int, [P(OpGraph), i32, P(i32), P(i32)]),
     "dsinf_fusion_savings": (C.c_int, [P(OpGraph), P(i32), i32, P(i64), P(i64)]),
     "dsinf_canonical_layer_partition": (C.c_int, [i64, i64, i32, i32, P(i32), P(i32), P(i64), P(i64)]),
+    "dsinf_canonical_layer_graph": (C.c_int, [i64, i64, i32, P(GraphBuffers)]),
 }
 
 if not os.path.exists(LIB_PATH):

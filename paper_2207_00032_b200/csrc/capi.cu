@@ -196,16 +196,20 @@ int dsinf_attention_decode(const void* q, const void* kcache, const void* vcache
   });
 }
 
-int dsinf_exec_device(const double* packed, int64_t packed_len, const dsinf_gemm_shape* shape,
-                      const dsinf_gemm_schedule* schedule, const double* x, int64_t x_len, int64_t batch,
-                      int32_t compute_dtype, double* out, int64_t out_len) {
+int dsinf_exec_device(const double* packed, int64_t packed_len, int32_t packed_pack_M,
+                      const dsinf_gemm_shape* shape, const dsinf_gemm_schedule* schedule, const double* x,
+                      int64_t x_len, int64_t batch, int32_t compute_dtype, double* out, int64_t out_len) {
   return guarded([&] {
     require(packed && shape && schedule && x && out, "null pointer argument");
     const int64_t N = shape->out_dim, K = shape->in_dim;
     if (N < 1 || K < 1) throw ConfigError("gemm shape dims must be positive");
     if (batch < 1 || x_len != batch * K) throw ConfigError("input shape mismatch");  // gemm.hpp:153-154
-    const int M = schedule->pack_M;
+    // the data layout is the packed buffer's own M (exec_reference reads packed.pack_M,
+    // gemm.hpp:186); the schedule's pack_M only groups the reference's iteration
+    const int M = packed_pack_M;
     if (M != 1 && M != 2 && M != 4) throw ConfigError("pack_M must be one of {1, 2, 4}");
+    const int SM = schedule->pack_M;
+    if (SM != 1 && SM != 2 && SM != 4) throw ConfigError("pack_M must be one of {1, 2, 4}");
     const int64_t kp = (K + M - 1) / M * M;
     if (packed_len != N * kp) throw ConfigError("packed buffer size mismatch");
     if (out_len != batch * N) throw ConfigError("output buffer size mismatch");

@@ -513,4 +513,46 @@ int dsinf_canonical_layer_partition(int64_t hidden, int64_t batch, int32_t dtype
   });
 }
 
+// canonical_layer_graph (fusion.hpp:242-357) exported as the flattened CSR graph of dsinf.h.
+int dsinf_canonical_layer_graph(int64_t hidden, int64_t batch, int32_t dtype_bytes, dsinf_graph_buffers* out) {
+  return guarded([&] {
+    require(out, "null argument");
+    Graph g = canonical_graph(hidden, batch, dtype_bytes);
+    int32_t nd = 0, np = 0;
+    for (const auto& e : g.edges) {
+      nd += static_cast<int32_t>(e.dep.size());
+      for (const auto& [c, prods] : e.dep) np += static_cast<int32_t>(prods.size());
+    }
+    const bool query = !out->node_kind;
+    out->num_nodes = static_cast<int32_t>(g.kind.size());
+    out->num_edges = static_cast<int32_t>(g.edges.size());
+    out->num_deps = nd;
+    out->num_prods = np;
+    out->dtype_bytes = g.dtype_bytes;
+    if (query) return;
+    require(out->node_tile_count && out->node_out_elems && out->edge_from && out->edge_to && out->dep_off &&
+                out->dep_consumer && out->prod_off && out->dep_prod,
+            "null graph buffer");
+    for (size_t i = 0; i < g.kind.size(); ++i) {
+      out->node_kind[i] = g.kind[i];
+      out->node_tile_count[i] = g.tiles[i];
+      out->node_out_elems[i] = g.out_elems[i];
+    }
+    int32_t di = 0, pi = 0;
+    for (size_t e = 0; e < g.edges.size(); ++e) {
+      out->edge_from[e] = g.edges[e].from;
+      out->edge_to[e] = g.edges[e].to;
+      out->dep_off[e] = di;
+      for (const auto& [c, prods] : g.edges[e].dep) {
+        out->dep_consumer[di] = c;
+        out->prod_off[di] = pi;
+        for (int p : prods) out->dep_prod[pi++] = p;
+        ++di;
+      }
+    }
+    out->dep_off[g.edges.size()] = di;
+    out->prod_off[di] = pi;
+  });
+}
+
 }  // extern "C"

@@ -1124,6 +1124,19 @@ void map_reduction_peers(Model& m, cudaStream_t s) {
   }
 }
 
+// true iff every rank of `comm` passes true (a sum all-reduce of one flag, synchronous).
+bool nccl_vote_all(nccl::Comm comm, bool mine, int t) {
+  float* d = nullptr;
+  DSINF_CUDA_CHECK(cudaMalloc(&d, sizeof(float)));
+  const float v = mine ? 1.f : 0.f;
+  float all = 0.f;
+  DSINF_CUDA_CHECK(cudaMemcpy(d, &v, sizeof(float), cudaMemcpyHostToDevice));
+  nccl::allreduce_sum_f32(d, 1, comm, nullptr);
+  DSINF_CUDA_CHECK(cudaMemcpy(&all, d, sizeof(float), cudaMemcpyDeviceToHost));
+  DSINF_CUDA_CHECK(cudaFree(d));
+  return all == static_cast<float>(t);
+}
+
 void validate_configs(const dsinf_model_config& c, const dsinf_runtime_config& r) {
   require(c.hidden_dim > 0 && c.num_layers >= 0 && c.num_heads > 0 && c.vocab_size > 0, "bad model dims");
   require(c.hidden_dim % c.num_heads == 0, "hidden_dim must be divisible by num_heads");
@@ -1237,22 +1250,25 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // a fused all-reduce request (below) selects the slice plan: its slots are summed by the
       // per-CTA LayerNorm prologues
       const char* far_req = std::getenv("DSINF_FUSED_AR");
-      const bool want_far = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) &&
-                            far_req != nullptr && std::atoi(far_req) != 0;
+      bool want_far = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) &&
+                      far_req != nullptr && std::atoi(far_req) != 0;
+      if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
+        // the request is per process (environment) but every rank must pick the same plan, or one
+        // rank waits on slot counters the others never bump: fused only if all t ranks ask for it
+        require(nccl_comm != nullptr, "NCCL mode needs a communicator");
+        want_far = nccl_vote_all(static_cast<nccl::Comm>(nccl_comm), want_far, m->t);
+      }
       m->xs_ln = rows16 && !want_far && gemm::prefer_x_stream(m->B, m->t > 1);
       const char* od = std::getenv("DSINF_XS_OD");
       const int od_v = od ? std::atoi(od) : -1;
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
       const char* lm = std::getenv("DSINF_XS_LM");
       m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
-      // fused all-reduce: on-device shards (DSINF_TP_LOCAL) for now -- across processes the slots
-      // would be CUDA-IPC peer mappings (not exercised on a one-GPU box); the per-CTA LayerNorm
-      // prologue path (slice plan, DSINF_XS=0) consumes the slots, the row_prep path handles the LM head
-      const char* far = std::getenv("DSINF_FUSED_AR");
-      // opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
+      // fused all-reduce: on-device shards (DSINF_TP_LOCAL) or CUDA-IPC peer mappings across
+      // processes; the per-CTA LayerNorm prologue path (slice plan) consumes the slots, the row_prep
+      // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
       // consumer CTA re-reads t slots), the win is hiding the NVLink exchange across GPUs
-      m->fused_ar = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) && !m->xs_ln &&
-                    !m->fuse_ln && (far != nullptr && std::atoi(far) != 0);
+      m->fused_ar = want_far && !m->xs_ln && !m->fuse_ln;
     }
     if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
       require(nccl_comm != nullptr, "NCCL mode needs a communicator");
@@ -1517,6 +1533,9 @@ int dsinf_model_get_info(const dsinf_model* m, dsinf_model_info* out) {
     out->kv_bytes = 2LL * m->L * m->B * m->Hl * m->max_ctx * m->d * 2 * static_cast<int64_t>(m->shards.size());
     out->shards = static_cast<int32_t>(m->shards.size());
     out->graph_ready = m->exec != nullptr;
+    out->fused_allreduce = m->fused_ar ? 1 : 0;
+    out->plan_flags = (m->xs_ln ? DSINF_PLAN_X_STREAM : 0) | (m->fuse_ln ? DSINF_PLAN_FUSED_STATS : 0) |
+                      (m->step_prog.ready() ? DSINF_PLAN_STEP_KERNEL : 0);
   });
 }
 

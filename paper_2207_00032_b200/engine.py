@@ -162,6 +162,10 @@ class DecoderModel:
     def generate(self, prompt: np.ndarray, gen_tokens: int, stream=None) -> np.ndarray:
         """Prefill the prompt token by token, then greedy-decode `gen_tokens`; returns [B, gen]."""
         P = prompt.shape[1]
+        # the token sampled at step pos is stored at history[pos + 1]: the last one (pos = P + gen - 2)
+        # needs P + gen - 1 < max_ctx, else the returned slice would come back one column short
+        if P + gen_tokens > self.max_ctx:
+            raise capi.InfeasibleError(f"prompt {P} + {gen_tokens} generated tokens exceed max_ctx {self.max_ctx}")
         self.set_prompt(prompt, stream)
         self.step(P + gen_tokens - 1, stream)
         _, hist = self.read_tokens(stream)

@@ -138,7 +138,7 @@ def exec_device(packed: PackedWeights, x, batch: int, schedule: GemmSchedule,
     data = _f64(packed.data)
     out = np.zeros(batch * packed.shape.out_dim, dtype=np.float64)
     shape = GemmShape(packed.shape.out_dim, packed.shape.in_dim, batch, packed.shape.dtype_bytes)
-    capi.check(capi.lib.dsinf_exec_device(_ptr(data), data.size, C.byref(shape._c()), C.byref(schedule._c()),
+    capi.check(capi.lib.dsinf_exec_device(_ptr(data), data.size, packed.pack_M, C.byref(shape._c()), C.byref(schedule._c()),
                                           _ptr(xv), xv.size, batch, compute_dtype, _ptr(out), out.size))
     return out
 
@@ -383,6 +383,30 @@ def fusion_savings(regions: List[FusionRegion], graph: OpGraph) -> FusionSavings
 
 CANONICAL_NODE_NAMES = ("input_layernorm", "qkv_gemm", "attn_transpose", "attention", "post_attn_layernorm",
                         "intermediate_gemm", "bias_add", "residual_add")  # fusion.hpp:266-288
+
+
+def canonical_layer_graph(hidden: int, batch: int, dtype_bytes: int = 2) -> OpGraph:  # fusion.hpp:242-357
+    """The canonical decode-layer graph built by the library (dsinf_canonical_layer_graph)."""
+    gb = capi.GraphBuffers()
+    capi.check(capi.lib.dsinf_canonical_layer_graph(hidden, batch, dtype_bytes, C.byref(gb)))
+    n, e, nd, npr = gb.num_nodes, gb.num_edges, gb.num_deps, gb.num_prods
+    bufs = {"node_kind": (C.c_int32 * n)(), "node_tile_count": (C.c_int32 * n)(), "node_out_elems": (C.c_int64 * n)(),
+            "edge_from": (C.c_int32 * e)(), "edge_to": (C.c_int32 * e)(), "dep_off": (C.c_int32 * (e + 1))(),
+            "dep_consumer": (C.c_int32 * max(1, nd))(), "prod_off": (C.c_int32 * (nd + 1))(),
+            "dep_prod": (C.c_int32 * max(1, npr))()}
+    for k, v in bufs.items():
+        setattr(gb, k, C.cast(v, type(getattr(gb, k))))
+    capi.check(capi.lib.dsinf_canonical_layer_graph(hidden, batch, dtype_bytes, C.byref(gb)))
+    g = OpGraph(dtype_bytes=gb.dtype_bytes)
+    for i in range(n):
+        g.nodes.append(OpNode(CANONICAL_NODE_NAMES[i], OpKind(bufs["node_kind"][i]), bufs["node_out_elems"][i],
+                              bufs["node_tile_count"][i]))
+    for j in range(e):
+        dep = {}
+        for c in range(bufs["dep_off"][j], bufs["dep_off"][j + 1]):
+            dep[bufs["dep_consumer"][c]] = set(bufs["dep_prod"][bufs["prod_off"][c]:bufs["prod_off"][c + 1]])
+        g.edges.append(GraphEdge(bufs["edge_from"][j], bufs["edge_to"][j], dep))
+    return g
 
 
 def canonical_layer_partition(hidden: int, batch: int, regime: BatchRegime, dtype_bytes: int = 2):

@@ -116,6 +116,23 @@ def test_exec_device_matches_exec_reference():
     assert np.array_equal(out, x @ W.T)
 
 
+@pytest.mark.parametrize("pack_m", [1, 2, 4])
+@pytest.mark.parametrize("sched_m", [1, 2, 4])
+def test_exec_device_any_packed_layout(pack_m, sched_m):
+    """exec_reference reads the data with packed.pack_M (gemm.hpp:186): weights packed with any M in
+    {1, 2, 4} give the same result under any schedule (whose pack_M only groups the iteration)."""
+    rng = np.random.default_rng(pack_m * 10 + sched_m)
+    N, K, B = 130, 67, 3  # K a multiple of none of 2, 4: the padded sizes differ per M
+    W = rng.integers(-8, 9, (N, K)).astype(np.float64)
+    x = rng.integers(-8, 9, (B, K)).astype(np.float64)
+    shape = I.GemmShape(N, K, B, 2)
+    sch = I.derive_schedule(shape, I.b200_device())
+    sch.pack_M = sched_m
+    packed = I.pack_weights(W, shape, pack_m)
+    out = I.exec_device(packed, x, B, sch).reshape(B, N)
+    assert np.array_equal(out, x @ W.T)
+
+
 @pytest.mark.parametrize("N,K,B", [(4096, 4096, 1), (12288, 4096, 1), (4096, 16384, 1), (1024, 2048, 3),
                                    (4096, 4096, 8), (16384, 4096, 16), (640, 320, 5)])
 def test_int8_weight_only_w8a16(N, K, B):

@@ -300,7 +300,9 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
         m.step(10)
         torch.cuda.synchronize()
         outs.append((m.full_logits(), m.read_tokens()[1]))
-        launches.append(m.get_info().kernels_per_step)
+        info = m.get_info()
+        launches.append(info.kernels_per_step)
+        assert info.fused_allreduce == (1 if fused == "1" else 0)
         m.close()
     assert launches[0] < launches[1], launches  # the fused path has no all-reduce / row_prep launches
     (la, ha), (lb, hb) = outs
@@ -364,3 +366,14 @@ def test_int8_mixed_mask_matches_oracle(monkeypatch, mask):
     monkeypatch.setenv("DSINF_A16_MASK", hex(mask))
     run_parity(256, 2, 4, 1000, batch=4, dtype_bytes=1, int8_act=capi.INT8_W8A8, step_kernel=False,
                oracle_int8_act=0x100 | mask)
+
+
+def test_generate_fills_max_ctx_and_rejects_beyond():
+    """generate() returns exactly gen_tokens columns up to P + gen == max_ctx and raises past it."""
+    m = DecoderModel(256, 1, 4, 1000, max_ctx=12, seed=SEED)
+    prompt = np.arange(1, 5, dtype=np.int32).reshape(1, 4)
+    out = m.generate(prompt, 8)
+    assert out.shape == (1, 8)
+    with pytest.raises(capi.InfeasibleError):
+        m.generate(prompt, 9)
+    m.close()
