@@ -277,7 +277,14 @@ struct or_model {
   float *kc, *vc;             /* [L][B][H][max_ctx][d] */
   float* res;                 /* [B][h] */
   float* final_hidden;        /* [B][h] */
+  or_gemm_hook_fn hook;       /* optional fp16-path GEMM (the reference's exec_reference) */
+  void* hook_ctx;
 };
+
+void or_model_set_gemm_hook(or_model* m, or_gemm_hook_fn fn, void* ctx) {
+  m->hook = fn;
+  m->hook_ctx = ctx;
+}
 
 static float* falloc(int64_t n) { return (float*)calloc((size_t)(n > 0 ? n : 1), sizeof(float)); }
 
@@ -454,12 +461,15 @@ static void layernorm_row(const float* v, int64_t K, const float* g, const float
 static double gelu_tanh(double x) { return 0.5 * x * (1.0 + tanh(0.7978845608028654 * (x + 0.044715 * x * x * x))); }
 
 /* fp16 path GEMM: out[b][n] (double) over the rank's row-major shard with the rank's schedule */
+static or_gemm_hook_fn g_hook;
+static void* g_hook_ctx;
 static void gemm16(const float* W, int64_t N, int64_t K, int sm, const float* x16, int64_t B, double* out) {
   or_schedule s;
   or_derive_schedule(N, K, B, 2, sm, &s);
   double* xd = (double*)malloc(sizeof(double) * (size_t)(B * K));
   for (int64_t i = 0; i < B * K; ++i) xd[i] = x16[i];
-  or_gemm_f64(W, N, K, &s, xd, B, out);
+  if (g_hook) g_hook(W, N, K, xd, B, out, g_hook_ctx);
+  else or_gemm_f64(W, N, K, &s, xd, B, out);
   free(xd);
 }
 
@@ -499,6 +509,8 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
   const int i8 = m->c.dtype_bytes == 1;
   const int sm = m->c.sm_count;
   if (pos < 0 || pos >= mc) return 2;
+  g_hook = m->hook;
+  g_hook_ctx = m->hook_ctx;
   float* r = m->res;
   for (int64_t b = 0; b < B; ++b) {
     int32_t tok = tokens[b];

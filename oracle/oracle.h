@@ -82,6 +82,12 @@ void or_model_destroy(or_model* m);
 /* One decode step at position `pos` for tokens[B]; writes logits [B][vocab] (fp32) and the
  * greedy tokens.  Appends to the oracle's KV cache. */
 int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits, int32_t* next_tokens);
+/* Optional GEMM hook for the fp16 path (e.g. the reference's own exec_reference from oracle/_ref):
+ * out[B][N] = x[B][K] . W^T over a row-major fp32 [N][K] shard. NULL restores the built-in
+ * same-order restatement (bit-identical to exec_reference under -ffp-contract=off). */
+typedef void (*or_gemm_hook_fn)(const float* W, int64_t N, int64_t K, const double* x, int64_t B, double* out,
+                                void* ctx);
+void or_model_set_gemm_hook(or_model* m, or_gemm_hook_fn fn, void* ctx);
 /* Last step's final hidden (post-LN, fp16-rounded) [B][hidden], for debugging. */
 void or_model_final_hidden(const or_model* m, float* out);
 

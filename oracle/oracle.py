@@ -75,6 +75,7 @@ if _or is not None:
     _or.or_model_destroy.argtypes = [C.c_void_p]
     _or.or_model_step.argtypes = [C.c_void_p, P(C.c_int32), C.c_int64, P(C.c_float), P(C.c_int32)]
     _or.or_model_final_hidden.argtypes = [C.c_void_p, P(C.c_float)]
+    _or.or_model_set_gemm_hook.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 
 if _ref is not None:
     _ref.ref_packed_index.restype = C.c_int64
@@ -86,6 +87,13 @@ if _ref is not None:
     _ref.ref_time_exec.restype = C.c_double
     _ref.ref_time_exec.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int,
                                    C.c_uint64, f64p]
+    _ref.ref_step_create.restype = C.c_void_p
+    _ref.ref_step_create.argtypes = [P(C.c_int64), P(C.c_int64), C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                     C.c_uint64]
+    _ref.ref_step_run.restype = C.c_double
+    _ref.ref_step_run.argtypes = [C.c_void_p, C.c_int]
+    _ref.ref_step_destroy.argtypes = [C.c_void_p]
+    _ref.ref_gemm_hook_clear.argtypes = []
     _ref.ref_param_count.argtypes = [C.c_int64] * 5 + [C.c_int, P(C.c_int64)]
     _ref.ref_layer_flops.argtypes = [C.c_int64] * 5 + [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, f64p]
     _ref.ref_kv_cache_bytes.argtypes = [C.c_int64] * 5 + [C.c_int, C.c_int64, C.c_int64, C.c_int64, P(C.c_int64)]
@@ -197,6 +205,19 @@ class OracleModel:
             raise ValueError("oracle step failed")
         return logits, nxt
 
+    def use_reference_gemm(self, on=True):
+        """Route every fp16-path GEMM through the reference's own exec_reference (oracle/_ref,
+        compiled from the reference headers) instead of the same-order restatement."""
+        ref = ref_lib()
+        if on and ref is None:
+            raise RuntimeError("oracle/_ref is not built")
+        if on:
+            self._sm = C.c_int(self.cfg.sm_count)
+            fn = C.cast(ref.ref_gemm_hook, C.c_void_p)
+            oracle_lib().or_model_set_gemm_hook(self._h, fn, C.cast(C.pointer(self._sm), C.c_void_p))
+        else:
+            oracle_lib().or_model_set_gemm_hook(self._h, None, None)
+
     def final_hidden(self):
         out = np.zeros((self.batch, self.hidden), dtype=np.float32)
         oracle_lib().or_model_final_hidden(self._h, out.ctypes.data_as(P(C.c_float)))
@@ -204,6 +225,8 @@ class OracleModel:
 
     def close(self):
         if self._h:
+            if ref_lib() is not None:
+                ref_lib().ref_gemm_hook_clear()
             oracle_lib().or_model_destroy(self._h)
             self._h = None
 

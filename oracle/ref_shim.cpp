@@ -5,6 +5,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <random>
 #include <thread>
 #include <vector>
@@ -285,6 +288,143 @@ int ref_partition_graph(int n_nodes, const int32_t* kind, const int32_t* tiles, 
     *launches = s.launches_saved;
     *bytes = s.bytes_saved;
   });
+}
+
+
+// ---------------------------------------------------------------- whole decode steps
+// One decode step of the reference's CPU path: every per-rank GEMM of every layer plus the LM head,
+// each one full exec_reference over its output rows (rows split into `threads` packed blocks run
+// concurrently; per-output arithmetic identical to one call).  The weights of each distinct shape
+// are generated and packed once (not timed); a step runs shape g reps[g] times (L for the layer
+// GEMMs, 1 for the LM head) -- the same work as L distinct layers, whose weights (0.1-1.7 GB of
+// fp64 each) could not stay cached anyway.
+struct RefStep {
+  struct Shape {
+    GemmSchedule sch;
+    int64_t reps;
+    std::vector<PackedWeights> blocks;
+  };
+  std::vector<Shape> shapes;
+  std::vector<double> x;
+  int64_t B;
+  double checksum = 0.0;
+};
+
+void* ref_step_create(const int64_t* nk, const int64_t* reps, int G, int64_t B, int dtype, int sm_count, int threads,
+                      uint64_t seed) {
+  auto st = std::make_unique<RefStep>();
+  st->B = B;
+  if (threads < 1) threads = 1;
+  int64_t kmax = 1;
+  for (int g = 0; g < G; ++g) kmax = std::max<int64_t>(kmax, nk[2 * g + 1]);
+  auto unit = [](uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return static_cast<double>(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  };
+  st->x.resize(B * kmax);
+  for (int64_t i = 0; i < B * kmax; ++i) st->x[i] = unit(seed ^ (0x1000000000ull + i));
+  for (int g = 0; g < G; ++g) {
+    const int64_t N = nk[2 * g], K = nk[2 * g + 1];
+    RefStep::Shape sh;
+    sh.sch = derive_schedule(GemmShape{N, K, B, dtype}, device(sm_count));
+    sh.reps = reps[g];
+    const int64_t per = (N + threads - 1) / threads;
+    const int nblk = static_cast<int>((N + per - 1) / per);
+    sh.blocks.resize(nblk);
+#pragma omp parallel for schedule(static, 1) num_threads(threads)
+    for (int t = 0; t < nblk; ++t) {
+      const int64_t r0 = t * per, r1 = std::min(N, r0 + per);
+      std::vector<double> w((r1 - r0) * K);
+      for (int64_t i = 0; i < static_cast<int64_t>(w.size()); ++i)
+        w[i] = unit(seed + (static_cast<uint64_t>(g) << 40) + static_cast<uint64_t>(r0 * K + i));
+      sh.blocks[t] = pack_weights(w, GemmShape{r1 - r0, K, B, dtype}, sh.sch.pack_M);
+    }
+    st->shapes.push_back(std::move(sh));
+  }
+  return st.release();
+}
+
+// Runs one step; returns its wall time in seconds (exec_reference calls only).
+double ref_step_run(void* h, int threads) {
+  auto* st = static_cast<RefStep*>(h);
+  double sum = 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (auto& sh : st->shapes) {
+    const int64_t K = sh.blocks.empty() ? 0 : sh.blocks[0].shape.in_dim;
+    const std::vector<double> x(st->x.begin(), st->x.begin() + st->B * K);
+    for (int64_t r = 0; r < sh.reps; ++r) {
+#pragma omp parallel for schedule(static, 1) num_threads(threads) reduction(+ : sum)
+      for (int t = 0; t < static_cast<int>(sh.blocks.size()); ++t) {
+        const std::vector<double> o = exec_reference(sh.blocks[t], x, st->B, sh.sch);
+        sum += o.empty() ? 0.0 : o[0];
+      }
+    }
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  st->checksum += sum;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+void ref_step_destroy(void* h) { delete static_cast<RefStep*>(h); }
+
+// GEMM hook for the oracle decoder (or_model_set_gemm_hook): out[B][N] = exec_reference over W
+// (row-major fp32 N x K, packed once per W pointer and cached), rows split across the OpenMP
+// threads.  With it the oracle's decode runs every GEMM through the reference's own function.
+namespace {
+struct HookCache {
+  std::mutex mu;
+  std::map<const float*, std::pair<GemmSchedule, std::vector<PackedWeights>>> packed;
+};
+HookCache& hook_cache() {
+  static HookCache c;
+  return c;
+}
+}  // namespace
+
+void ref_gemm_hook(const float* W, int64_t N, int64_t K, const double* x, int64_t B, double* out, void* ctx) {
+  const int sm = ctx ? *static_cast<const int*>(ctx) : 148;
+  HookCache& c = hook_cache();
+  std::pair<GemmSchedule, std::vector<PackedWeights>>* entry = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.packed.find(W);
+    if (it == c.packed.end() || it->second.second.empty() || it->second.second[0].shape.in_dim != K) {
+      const GemmSchedule sch = derive_schedule(GemmShape{N, K, B, 2}, device(sm));
+      const int threads = std::max(1, static_cast<int>(std::thread::hardware_concurrency()));
+      const int64_t per = (N + threads - 1) / threads;
+      const int nblk = static_cast<int>((N + per - 1) / per);
+      std::vector<PackedWeights> blocks(nblk);
+#pragma omp parallel for schedule(static, 1)
+      for (int t = 0; t < nblk; ++t) {
+        const int64_t r0 = t * per, r1 = std::min(N, r0 + per);
+        std::vector<double> w((r1 - r0) * K);
+        for (int64_t i = 0; i < static_cast<int64_t>(w.size()); ++i) w[i] = W[r0 * K + i];
+        blocks[t] = pack_weights(w, GemmShape{r1 - r0, K, B, 2}, sch.pack_M);
+      }
+      c.packed[W] = {sch, std::move(blocks)};
+    }
+    entry = &c.packed[W];
+  }
+  // the schedule is derived for the call's batch (derive_schedule ignores B)
+  const GemmSchedule sch = entry->first;
+  const std::vector<double> xv(x, x + B * K);
+  auto& blocks = entry->second;
+  const int64_t per = blocks.empty() ? 0 : blocks[0].shape.out_dim;
+#pragma omp parallel for schedule(static, 1)
+  for (int t = 0; t < static_cast<int>(blocks.size()); ++t) {
+    const std::vector<double> o = exec_reference(blocks[t], xv, B, sch);
+    const int64_t r0 = t * per, n = blocks[t].shape.out_dim;
+    for (int64_t b = 0; b < B; ++b)
+      for (int64_t i = 0; i < n; ++i) out[b * N + r0 + i] = o[b * n + i];
+  }
+}
+
+void ref_gemm_hook_clear() {
+  std::lock_guard<std::mutex> lk(hook_cache().mu);
+  hook_cache().packed.clear();
 }
 
 }  // extern "C"

@@ -7,7 +7,6 @@ on torch tensors (torch is only the device allocator and stream provider here).
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
@@ -20,26 +19,7 @@ except ImportError:  # pragma: no cover
     torch = None
 
 
-# ---------------------------------------------------------------- model presets (BASELINE.json configs)
-
-@dataclass(frozen=True)
-class Preset:
-    name: str
-    hidden: int
-    layers: int
-    heads: int
-    tp: int
-    vocab: int = 50257
-    max_seq: int = 2048
-
-
-PRESETS = {
-    "gpt2-1.5b": Preset("GPT-2 1.5B", 1600, 48, 25, 1),
-    "gptj-6b": Preset("GPT-J 6B", 4096, 32, 32, 1),
-    "gpt-neox-20b": Preset("GPT-NeoX 20B", 6144, 44, 64, 2),
-    "gpt-50b": Preset("GPT-50B", 8192, 62, 64, 4),
-    "gpt3-175b": Preset("GPT3-175B", 12288, 96, 96, 8),
-}
+from .presets import PRESETS, Preset  # noqa: E402,F401  (BASELINE.json configs)
 
 
 def _stream_ptr(stream) -> Optional[int]:

@@ -94,3 +94,25 @@ def test_fusability_rules():  # test_fusion.cpp:66-101
     assert not I.fusable(g, I.GraphEdge(0, 1, {0: {0, 1, 2, 3}, 1: {1}, 2: {2}, 3: {3}}))
     assert not I.fusable(g, I.GraphEdge(0, 1, {}))  # missing consumer tiles block fusion
     assert I.fusable(g, I.GraphEdge(0, 1, {i * 2 + j: {j * 2 + i} for i in range(2) for j in range(2)}))
+
+
+@pytest.mark.skipif(O.ref_lib() is None, reason="oracle/_ref not built (no reference tree)")
+def test_oracle_decoder_gemms_equal_exec_reference():
+    """The oracle decoder with every GEMM run by the reference's own exec_reference (oracle/_ref)
+    produces bit-identical logits to its same-order restatement: the fp16 path's GEMM arithmetic is
+    the reference's, end to end through two layers and four decode steps."""
+    prompt = np.array([[3, 17, 250, 999], [1, 2, 3, 4]], dtype=np.int32)
+    outs = []
+    for hook in (False, True):
+        m = O.OracleModel(192, 2, 3, 1000, batch=2, max_ctx=8, seed=11)
+        if hook:
+            m.use_reference_gemm()
+        res = []
+        for pos in range(4):
+            lg, nxt = m.step(prompt[:, pos], pos)
+            res.append((lg.copy(), nxt.copy()))
+        m.close()
+        outs.append(res)
+    for (la, na), (lb, nb) in zip(*outs):
+        assert np.array_equal(la, lb)
+        assert np.array_equal(na, nb)
