@@ -222,6 +222,7 @@ static int8_t q_one(float x, float s) {
 }
 
 void or_quant_rows(const float* x, int64_t rows, int64_t K, int8_t* q, float* scales) {
+#pragma omp parallel for schedule(static) if (rows * K > (1 << 20))
   for (int64_t r = 0; r < rows; ++r) {
     float mx = 0.0f;
     for (int64_t k = 0; k < K; ++k) {
@@ -281,6 +282,8 @@ struct or_model {
   void* hook_ctx;
 };
 
+void or_model_set_int8_act(or_model* m, int32_t int8_act) { m->c.int8_act = int8_act; }
+
 void or_model_set_gemm_hook(or_model* m, or_gemm_hook_fn fn, void* ctx) {
   m->hook = fn;
   m->hook_ctx = ctx;
@@ -321,6 +324,24 @@ static void gen_shard_i8(int8_t* q, float* scales, int64_t Nl, int64_t Kl, int64
     scales[n] = s;
     for (int64_t k = 0; k < Kl; ++k) q[n * Kl + k] = q_one(gval(base, gr, col_off + k, Kg), s);
   }
+}
+
+/* Whole global tensors for the sequence oracle (oracle/seq_oracle.py): the same values the
+ * per-rank shards above take (gval / synth_v), rows >= valid_rows zero. */
+void or_synth_matrix(uint64_t seed, int32_t layer, int32_t tensor, int64_t rows, int64_t cols, int64_t valid_rows,
+                     float* out) {
+  gen_shard(out, rows, cols, cols, rows, rows, 0, 0, valid_rows, or_synth_base(seed, layer, tensor));
+}
+
+void or_synth_vector(uint64_t seed, int32_t layer, int32_t tensor, int64_t n, float* out) {
+  float offset = 0.f, amp = kAmpB;
+  if (tensor == T_LN1_G || tensor == T_LN2_G || tensor == T_LNF_G) {
+    offset = 1.f;
+    amp = kAmpG;
+  } else if (tensor == T_LN1_B || tensor == T_LN2_B || tensor == T_LNF_B) {
+    amp = kAmpBeta;
+  }
+  gen_vec(out, n, or_synth_base(seed, layer, tensor), offset, amp);
 }
 
 or_model* or_model_create(const or_config* cfg) {

@@ -63,6 +63,12 @@ void or_gemm_i8(const int8_t* wq, const float* ws, const int8_t* xq, const float
 uint64_t or_synth_base(uint64_t seed, int32_t layer, int32_t tensor);
 float or_synth_unit(uint64_t base, uint64_t flat);
 
+/* Whole global synthetic tensors (tensor ids: include/dsinf.h DSINF_T_*): a [rows][cols] matrix
+ * with rows >= valid_rows zero, or a bias / LayerNorm vector with its offset and amplitude. */
+void or_synth_matrix(uint64_t seed, int32_t layer, int32_t tensor, int64_t rows, int64_t cols, int64_t valid_rows,
+                     float* out);
+void or_synth_vector(uint64_t seed, int32_t layer, int32_t tensor, int64_t n, float* out);
+
 /* ------------------------------------------------------------------ decoder model */
 typedef struct or_config {
   int64_t hidden, layers, heads, vocab, max_ctx;
@@ -82,6 +88,8 @@ void or_model_destroy(or_model* m);
 /* One decode step at position `pos` for tokens[B]; writes logits [B][vocab] (fp32) and the
  * greedy tokens.  Appends to the oracle's KV cache. */
 int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits, int32_t* next_tokens);
+/* Switch the int8 activation mode between steps (e.g. the W8A8 prompt prefill, then decode modes). */
+void or_model_set_int8_act(or_model* m, int32_t int8_act);
 /* Optional GEMM hook for the fp16 path (e.g. the reference's own exec_reference from oracle/_ref):
  * out[B][N] = x[B][K] . W^T over a row-major fp32 [N][K] shard. NULL restores the built-in
  * same-order restatement (bit-identical to exec_reference under -ffp-contract=off). */

@@ -75,6 +75,10 @@ if _or is not None:
     _or.or_model_destroy.argtypes = [C.c_void_p]
     _or.or_model_step.argtypes = [C.c_void_p, P(C.c_int32), C.c_int64, P(C.c_float), P(C.c_int32)]
     _or.or_model_final_hidden.argtypes = [C.c_void_p, P(C.c_float)]
+    _or.or_synth_matrix.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                                    P(C.c_float)]
+    _or.or_synth_vector.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int64, P(C.c_float)]
+    _or.or_model_set_int8_act.argtypes = [C.c_void_p, C.c_int32]
     _or.or_model_set_gemm_hook.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 
 if _ref is not None:
@@ -204,6 +208,9 @@ class OracleModel:
         if rc:
             raise ValueError("oracle step failed")
         return logits, nxt
+
+    def set_int8_act(self, mode):
+        oracle_lib().or_model_set_int8_act(self._h, mode)
 
     def use_reference_gemm(self, on=True):
         """Route every fp16-path GEMM through the reference's own exec_reference (oracle/_ref,

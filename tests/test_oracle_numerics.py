@@ -107,3 +107,40 @@ def test_oracle_per_gemm_act_mask():
     assert np.array_equal(out[0], out[0x100])
     assert np.array_equal(out[1], out[0x10f])
     assert not np.array_equal(out[0x105], out[0]) and not np.array_equal(out[0x105], out[1])
+
+
+import pytest  # noqa: E402
+
+from oracle.seq_oracle import SeqOracle  # noqa: E402
+
+
+def _step_logits(hidden, layers, heads, vocab, tokens, *, dtype_bytes, tp, prompt_len, prefill_mode, decode_mode):
+    S, T = tokens.shape
+    m = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=S, max_ctx=T, seed=77,
+                      int8_act=prefill_mode)
+    out = []
+    for p in range(T):
+        if p == prompt_len:
+            m.set_int8_act(decode_mode)
+        lg, _ = m.step(tokens[:, p], p)
+        out.append(lg.copy())
+    m.close()
+    return np.stack(out, axis=1)  # [S][T][V]
+
+
+@pytest.mark.parametrize("dtype_bytes,tp,prefill_mode,decode_mode", [
+    (2, 1, 0, 0), (2, 2, 0, 0), (1, 1, 0, 0), (1, 2, 0, 0), (1, 1, 0, 1), (1, 2, 0, 0x10e), (1, 1, 1, 0x101)])
+def test_seq_oracle_matches_step_oracle(dtype_bytes, tp, prefill_mode, decode_mode):
+    """The teacher-forced sequence oracle (numpy fp64 BLAS, all positions at once) reproduces the
+    step oracle (or_model_step, exec_reference-order GEMMs, one position at a time) on the same
+    tokens: fp16 logits to 1e-9 relative, int8 identical up to fp64 summation-order noise."""
+    hidden, layers, heads, vocab = 128, 2, 4, 300
+    S, T, P = 3, 9, 5
+    tokens = np.random.default_rng(5).integers(0, vocab, (S, T))
+    ref = _step_logits(hidden, layers, heads, vocab, tokens, dtype_bytes=dtype_bytes, tp=tp, prompt_len=P,
+                       prefill_mode=prefill_mode, decode_mode=decode_mode)
+    so = SeqOracle(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, seed=77)
+    got = so.forward(tokens, list(range(T)), prompt_len=P, prefill_mode=prefill_mode, decode_mode=decode_mode)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= 1e-12, err  # bit-identical here; BLAS kernels elsewhere may reorder fp64 sums
+    assert np.array_equal(got.argmax(axis=2), ref.argmax(axis=2))

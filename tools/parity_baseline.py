@@ -1,0 +1,188 @@
+#!/usr/bin/env python3
+"""Parity of the BENCHED decode path against the CPU oracle at BASELINE.json's configs.
+
+The GPU side is exactly what bench.py times: a DecoderModel with the CUDA graph, PDL, the default
+(x-streaming, per-kernel) plans, INT8 in the AUTO activation mode, the 128-token prompt prefilled on
+the tcgen05 tensor cores, then greedy decode steps.  8 greedy tokens per sequence are produced
+(PAPER.md:1334): the prefill's token and 7 decode steps; the logits behind each are read back.
+
+The oracle is teacher-forced (oracle/seq_oracle.py): it is given the prompt plus the GPU's own
+greedy tokens and returns, for every one of the 8 positions, the logits the token-by-token decode
+would compute from that prefix -- in fp64, with the GPU's storage points and INT8 recipes (prompt
+rows W8A8 as the tcgen05 prefill, generated rows in the decode's per-GEMM modes).
+
+Checks per (sequence, position):
+  - max |logit_gpu - logit_oracle| <= tol, tol = 0.03 std + 0.01 (fp16), 0.06 std + 0.02 (int8);
+  - the GPU's greedy token equals the oracle's argmax, or the mismatch is a near tie: the oracle's
+    logit of the GPU token is within 2 max|dlogit| of its top logit (logged with both numbers);
+  - reported: the number of positions whose oracle top-1/top-2 margin is below tol (where a flip
+    would be within tolerance), and every mismatch.
+
+  python tools/parity_baseline.py --suite gptj|tp|all [--out profiles/r2_parity.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+SEED = 20220701
+PROMPT = 128
+GEN = 8
+
+
+def tolerance(dtype):
+    return (0.03, 0.01) if dtype == "fp16" else (0.06, 0.02)
+
+
+def gpu_run(hidden, layers, heads, vocab, *, dtype, batch, prompts, tp=1):
+    """The bench path: returns (tokens [B][P+GEN], logits [B][GEN][V], info dict)."""
+    import torch
+
+    from paper_2207_00032_b200 import _capi as capi
+    from paper_2207_00032_b200.engine import DecoderModel
+
+    m = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=1 if dtype == "int8" else 2, batch=batch,
+                     max_ctx=PROMPT + GEN + 8, tp_size=tp, tp_mode=capi.TP_LOCAL if tp > 1 else capi.TP_NONE,
+                     seed=SEED, int8_act=capi.INT8_AUTO)
+    info = m.get_info()
+    m.set_prompt(prompts[:batch])
+    m.prefill()
+    torch.cuda.synchronize()
+    logits = [m.full_logits().copy()]
+    for _ in range(GEN - 1):
+        m.step(1)
+        torch.cuda.synchronize()
+        logits.append(m.full_logits().copy())
+    _, hist = m.read_tokens()
+    m.close()
+    meta = {"plan_flags": int(info.plan_flags), "kernels_per_step": int(info.kernels_per_step),
+            "fused_allreduce": int(info.fused_allreduce)}
+    return hist[:, :PROMPT + GEN].copy(), np.stack(logits, axis=1), meta
+
+
+def auto_mask(batch, tp):
+    """The oracle image of DSINF_INT8_AUTO (model.cu dsinf_model_create): W8A16 everywhere up to
+    B = 8; at B = 16 W8A8 QKV + W8A16 the rest at TP = 1, W8A8 everywhere at TP > 1."""
+    if batch <= 8:
+        return 0x10f
+    return 0x10e if tp == 1 else 0x100
+
+
+def compare(name, dtype, tokens, glog, olog):
+    tr, ta = tolerance(dtype)
+    rows = []
+    worst = 0.0
+    near, mism, bad = 0, [], []
+    B = tokens.shape[0]
+    for b in range(B):
+        for k in range(GEN):
+            g, o = glog[b, k], olog[b, k]
+            err = float(np.abs(g - o).max())
+            tol = tr * float(o.std()) + ta
+            worst = max(worst, err / tol)
+            srt = np.sort(o)
+            margin = float(srt[-1] - srt[-2])
+            near += margin <= tol
+            gt = int(tokens[b, PROMPT + k])
+            ot = int(np.argmax(o))
+            row = {"b": b, "k": k, "err": round(err, 5), "tol": round(tol, 5), "margin": round(margin, 5)}
+            if err > tol:
+                bad.append(row)
+            if gt != ot:
+                gap = float(o[ot] - o[gt])
+                row.update({"gpu_token": gt, "oracle_token": ot, "oracle_gap": round(gap, 6)})
+                mism.append(row)
+                if gap > 2 * err:
+                    bad.append(dict(row, why="token mismatch beyond 2 max|dlogit|"))
+            rows.append(row)
+    return {"case": name, "dtype": dtype, "positions": B * GEN, "worst_err_over_tol": round(worst, 4),
+            "max_abs_err": round(max(r["err"] for r in rows), 5), "near_ties_below_tol": int(near),
+            "token_mismatches": mism, "failures": bad, "ok": not bad,
+            "tokens_identical": sum(1 for r in rows if "gpu_token" not in r)}
+
+
+def run_config(label, hidden, layers, heads, vocab, *, tp, dtypes, batches, log=print):
+    """All (dtype, batch) cases of one model shape; the oracle runs once per (dtype, INT8 mode) over
+    the distinct sequences the GPU runs produced."""
+    from oracle.seq_oracle import SeqOracle
+
+    prompts = np.random.default_rng(SEED).integers(0, vocab, (max(batches), PROMPT)).astype(np.int32)
+    results = []
+    for dtype in dtypes:
+        runs = {}
+        for B in batches:
+            t0 = time.time()
+            toks, lg, meta = gpu_run(hidden, layers, heads, vocab, dtype=dtype, batch=B, prompts=prompts, tp=tp)
+            runs[B] = (toks, lg, meta)
+            log(f"[{label}] gpu {dtype} B={B}: {time.time() - t0:.1f}s tokens[0]={toks[0, PROMPT:].tolist()}")
+        groups = {}
+        for B in batches:
+            mode = auto_mask(B, tp) if dtype == "int8" else 0
+            groups.setdefault(mode, []).append(B)
+        for mode, bs in groups.items():
+            seqs = {}
+            for B in bs:
+                for b in range(B):
+                    seqs.setdefault(tuple(runs[B][0][b, :PROMPT + GEN - 1].tolist()), None)
+            keys = list(seqs)
+            t0 = time.time()
+            so = SeqOracle(hidden, layers, heads, vocab, dtype_bytes=1 if dtype == "int8" else 2, tp=tp, seed=SEED)
+            olog = so.forward(np.array(keys), list(range(PROMPT - 1, PROMPT + GEN - 1)), prompt_len=PROMPT,
+                              prefill_mode=0, decode_mode=mode)
+            log(f"[{label}] oracle {dtype} mode={mode:#x}: {len(keys)} sequences, {time.time() - t0:.1f}s")
+            index = {k: i for i, k in enumerate(keys)}
+            for B in bs:
+                toks, lg, meta = runs[B]
+                ol = np.stack([olog[index[tuple(toks[b, :PROMPT + GEN - 1].tolist())]] for b in range(B)])
+                r = compare(f"{label} {dtype} B={B}", dtype, toks, lg, ol)
+                r.update({"batch": B, "tp": tp, "layers": layers, "hidden": hidden, "int8_oracle_mode": mode,
+                          "gpu": meta})
+                log(f"[{label}] {dtype} B={B}: worst err/tol {r['worst_err_over_tol']}, max|dlogit| "
+                    f"{r['max_abs_err']}, tokens identical {r['tokens_identical']}/{r['positions']}, near ties "
+                    f"{r['near_ties_below_tol']}, mismatches {len(r['token_mismatches'])}, ok {r['ok']}")
+                results.append(r)
+    return results
+
+
+SUITES = {
+    # BASELINE configs[1]: GPT-J-6B at full depth, batch 1 / 8 / 16, fp16 and int8 (the bench line)
+    "gptj": [("GPT-J 6B", 4096, 32, 32, 50257, 1, (1, 8, 16))],
+    # the TP configs at full width and reduced depth, all shards on this GPU (DSINF_TP_LOCAL)
+    "tp": [("GPT-NeoX 20B t=2 (2 layers)", 6144, 2, 64, 50257, 2, (1, 16)),
+           ("GPT-50B t=4 (2 layers)", 8192, 2, 64, 50257, 4, (1, 16)),
+           ("GPT3-175B t=8 (2 layers)", 12288, 2, 96, 50257, 8, (1, 16))],
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--suite", choices=["gptj", "tp", "all"], default="all")
+    ap.add_argument("--dtypes", default="fp16,int8")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    names = ["gptj", "tp"] if args.suite == "all" else [args.suite]
+    res = []
+    for n in names:
+        for label, h, L, H, V, tp, bs in SUITES[n]:
+            res += run_config(label, h, L, H, V, tp=tp, dtypes=args.dtypes.split(","), batches=bs)
+    summary = {"cases": len(res), "ok": all(r["ok"] for r in res),
+               "positions": sum(r["positions"] for r in res),
+               "tokens_identical": sum(r["tokens_identical"] for r in res),
+               "near_ties_below_tol": sum(r["near_ties_below_tol"] for r in res), "results": res}
+    print(json.dumps({k: v for k, v in summary.items() if k != "results"}))
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(summary, f, indent=1)
+    sys.exit(0 if summary["ok"] else 1)
+
+
+if __name__ == "__main__":
+    main()
