@@ -85,7 +85,7 @@ class SeqOracle:
     requested positions of every sequence; weights are regenerated per layer (nothing kept)."""
 
     def __init__(self, hidden, layers, heads, vocab=50257, *, dtype_bytes=2, tp=1, seed=20220701, ln_eps=1e-5,
-                 rope_base=10000.0):
+                 rope_base=10000.0, acc="f64"):
         self.h, self.L, self.H, self.V = hidden, layers, heads, vocab
         self.d = hidden // heads
         self.t = tp
@@ -96,6 +96,11 @@ class SeqOracle:
         self.seed = seed
         self.eps = ln_eps
         self.rope_base = rope_base
+        # acc="f32": the same algorithm with fp32 GEMM and attention accumulation (the device's
+        # accumulation width) -- a second correct implementation whose distance from the fp64 one
+        # measures the intrinsic noise floor of the INT8 W8A8 activation quantisation (parity_baseline)
+        assert acc in ("f64", "f32")
+        self.ft = np.float64 if acc == "f64" else np.float32
         vq = 128 * tp
         self.Vpad = (vocab + vq - 1) // vq * vq
 
@@ -108,13 +113,13 @@ class SeqOracle:
 
     # ---- GEMMs: out[M][N] for x[M][K] over the full (global) weight; K sliced per rank when row-parallel
     def _gemm16(self, x16, W):
-        return x16.astype(np.float64) @ W.astype(np.float64).T
+        return (x16.astype(self.ft) @ W.astype(self.ft).T).astype(np.float64)
 
     def _gemm8(self, mode, x16, Wq, ws):
         """gemm8 (oracle.c): W8A16 y = fp32(sum q x) * s_w; W8A8 per-token int8 x, exact int32,
         y = fp32(fp32(acc) * s_x) * s_w."""
         if mode == 1:
-            a = x16.astype(np.float64) @ Wq.astype(np.float64).T
+            a = x16.astype(self.ft) @ Wq.astype(self.ft).T
             return a.astype(np.float32) * ws[None, :]
         xq, xs = _quant_rows(x16)
         acc = xq.astype(np.float64) @ Wq.astype(np.float64).T  # exact integers (< 2^53)
@@ -219,9 +224,9 @@ class SeqOracle:
             scale = 1.0 / math.sqrt(d)
             for sq in range(S):
                 rows = inv[sq * T:(sq + 1) * T]  # flattened rows of this sequence in position order
-                qs = q[rows].astype(np.float64).transpose(1, 0, 2)  # [H][T][d]
-                ks = k[rows].astype(np.float64).transpose(1, 0, 2)
-                vs = v[rows].astype(np.float64).transpose(1, 0, 2)
+                qs = q[rows].astype(self.ft).transpose(1, 0, 2)  # [H][T][d]
+                ks = k[rows].astype(self.ft).transpose(1, 0, 2)
+                vs = v[rows].astype(self.ft).transpose(1, 0, 2)
                 sc = (qs @ ks.transpose(0, 2, 1)) * scale  # [H][T][T]
                 mask = np.triu(np.ones((T, T), dtype=bool), 1)
                 sc[:, mask] = -np.inf

@@ -214,20 +214,23 @@ int dsinf_exec_device(const double* packed, int64_t packed_len, int32_t packed_p
     if (packed_len != N * kp) throw ConfigError("packed buffer size mismatch");
     if (out_len != batch * N) throw ConfigError("output buffer size mismatch");
     require(compute_dtype == DSINF_DT_F16 || compute_dtype == DSINF_DT_I8, "compute_dtype must be F16 or I8");
-    // unpack (host) -> fp16 row-major on device -> device pack / quantise -> SBI-GeMM
-    std::vector<uint16_t> w16(static_cast<size_t>(N * K));
+    // unpack (host) -> fp16 row-major on device -> device pack / quantise -> SBI-GeMM.  The TMA view
+    // of the packed weights needs N % 4 == 0 (16-byte row stride): out_dim is padded with zero rows
+    // and the padding columns are dropped from the output (exec_reference takes any N).
+    const int64_t Np = (N + 3) / 4 * 4;
+    std::vector<uint16_t> w16(static_cast<size_t>(Np * K), 0);
     for (int64_t n = 0; n < N; ++n)
       for (int64_t k = 0; k < K; ++k)
         w16[n * K + k] = f32_to_f16_bits(static_cast<float>(packed[(k / M) * (N * M) + n * M + (k % M)]));
     std::vector<uint16_t> x16(static_cast<size_t>(batch * K));
     for (int64_t i = 0; i < batch * K; ++i) x16[i] = f32_to_f16_bits(static_cast<float>(x[i]));
     cudaStream_t s = nullptr;
-    DeviceBuffer dw(w16.size() * 2), dx(x16.size() * 2), dout(static_cast<size_t>(batch * N) * 4);
+    DeviceBuffer dw(w16.size() * 2), dx(x16.size() * 2), dout(static_cast<size_t>(batch * Np) * 4);
     DSINF_CUDA_CHECK(cudaMemcpy(dw.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
     DSINF_CUDA_CHECK(cudaMemcpy(dx.p, x16.data(), x16.size() * 2, cudaMemcpyHostToDevice));
     gemm::configure();
     dsinf_gemm_args a{};
-    a.N = N;
+    a.N = Np;
     a.K = K;
     a.B = batch;
     a.x = dx.p;
@@ -236,15 +239,15 @@ int dsinf_exec_device(const double* packed, int64_t packed_len, int32_t packed_p
     a.out_dtype = DSINF_DT_F32;
     a.epilogue = DSINF_EPI_NONE;
     if (compute_dtype == DSINF_DT_F16) {
-      DeviceBuffer dp(static_cast<size_t>((K + 1) / 2 * 2 * N) * 2);
-      ops::pack_f16(dw.p, false, N, K, 2, static_cast<__half*>(dp.p), s);
+      DeviceBuffer dp(static_cast<size_t>((K + 1) / 2 * 2 * Np) * 2);
+      ops::pack_f16(dw.p, false, Np, K, 2, static_cast<__half*>(dp.p), s);
       a.w_packed = dp.p;
       a.w_dtype = DSINF_DT_F16;
       run_gemm(a, s);
       DSINF_CUDA_CHECK(cudaDeviceSynchronize());
     } else {
-      DeviceBuffer dp(static_cast<size_t>((K + 3) / 4 * 4 * N)), ds(static_cast<size_t>(N) * 4);
-      ops::quantize_weights_i8(static_cast<const __half*>(dw.p), N, K, static_cast<int8_t*>(dp.p),
+      DeviceBuffer dp(static_cast<size_t>((K + 3) / 4 * 4 * Np)), ds(static_cast<size_t>(Np) * 4);
+      ops::quantize_weights_i8(static_cast<const __half*>(dw.p), Np, K, static_cast<int8_t*>(dp.p),
                                static_cast<float*>(ds.p), s);
       a.w_packed = dp.p;
       a.w_dtype = DSINF_DT_I8;
@@ -252,9 +255,10 @@ int dsinf_exec_device(const double* packed, int64_t packed_len, int32_t packed_p
       run_gemm(a, s);
       DSINF_CUDA_CHECK(cudaDeviceSynchronize());
     }
-    std::vector<float> o(static_cast<size_t>(batch * N));
+    std::vector<float> o(static_cast<size_t>(batch * Np));
     DSINF_CUDA_CHECK(cudaMemcpy(o.data(), dout.p, o.size() * 4, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < o.size(); ++i) out[i] = o[i];
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t n = 0; n < N; ++n) out[b * N + n] = o[b * Np + n];
   });
 }
 

@@ -449,10 +449,14 @@ void build_step_program(Model& m) {
   float* r = sh.res[0];
   const int h = static_cast<int>(m.h), HD = static_cast<int>(m.Hl * m.d), Fl = static_cast<int>(m.Fl);
   const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
+  require(sh.lnstats != nullptr, "the persistent step kernel needs the producer-fused LayerNorm sums (DSINF_FUSE_STATS)");
+  auto slot = [&](int i) { return sh.lnstats + static_cast<int64_t>(i) * gemm::kLnSlotWords; };
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = sh.layers[l];
     gemm::Params q = base_params(m, w.wqkv, w.sqkv, 3 * HD, h, m.int8);
+    q.a16 = m.int8 ? 1 : 0;
     q.pro = gemm::PRO_LN;
+    q.ln_stats_in = slot(2 * l);
     q.res_in = r;
     q.ln_g = w.ln1g;
     q.ln_b = w.ln1b;
@@ -467,14 +471,18 @@ void build_step_program(Model& m) {
     q.head_dim = static_cast<int>(m.d);
     q.max_seq = m.max_ctx;
     gemm::Params o = base_params(m, w.wo, w.so, h, HD, m.int8);
-    o.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    o.a16 = q.a16;
+    o.pro = gemm::PRO_F16;
     o.x = sh.a;
     o.x_ld = HD;
     o.epi = gemm::EPI_RESID;
     o.out = r;
     o.bias = w.bo;
+    o.ln_stats_out = slot(2 * l + 1);
     gemm::Params u = base_params(m, w.wup, w.sup, Fl, h, m.int8);
+    u.a16 = q.a16;
     u.pro = gemm::PRO_LN;
+    u.ln_stats_in = slot(2 * l + 1);
     u.res_in = r;
     u.ln_g = w.ln2g;
     u.ln_b = w.ln2b;
@@ -482,12 +490,14 @@ void build_step_program(Model& m) {
     u.bias = w.bup;
     u.out = sh.u;
     gemm::Params dn = base_params(m, w.wdown, w.sdown, h, Fl, m.int8);
-    dn.pro = m.int8 ? gemm::PRO_QUANT : gemm::PRO_F16;
+    dn.a16 = q.a16;
+    dn.pro = gemm::PRO_F16;
     dn.x = sh.u;
     dn.x_ld = Fl;
     dn.epi = gemm::EPI_RESID;
     dn.out = r;
     dn.bias = w.bdown;
+    dn.ln_stats_out = slot(2 * l + 2);
     D.gemms.push_back(q);
     D.gemms.push_back(o);
     D.gemms.push_back(u);
@@ -496,6 +506,7 @@ void build_step_program(Model& m) {
   }
   gemm::Params lm = base_params(m, sh.wlm, nullptr, static_cast<int>(m.Vl), h, false);
   lm.pro = gemm::PRO_LN;
+  lm.ln_stats_in = slot(2 * static_cast<int>(m.L));
   lm.res_in = r;
   lm.ln_g = sh.lnfg;
   lm.ln_b = sh.lnfb;
@@ -503,6 +514,8 @@ void build_step_program(Model& m) {
   lm.out = sh.logits;
   D.gemms.push_back(lm);
   D.embed = embed_params(m, sh);
+  D.embed.ln_stats_out = slot(0);
+  D.am_key = m.am_key;
   D.logits = sh.logits;
   D.next_tok = m.next_tok;
   D.hist = m.hist;
@@ -1006,6 +1019,9 @@ struct Enqueuer {
 
   void step() {
     if (m.step_prog.ready()) {  // TP = 1: the whole step is one persistent kernel
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.am_key, 0, sizeof(unsigned long long) * m.B, s));
+      DSINF_CUDA_CHECK(cudaMemsetAsync(m.shards[0].lnstats, 0,
+                                       (2 * m.L + 1) * gemm::kLnSlotWords * sizeof(long long), s));
       m.step_prog.launch(s);
       ++launches;
       return;
@@ -1239,7 +1255,11 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       if (const char* am = std::getenv("DSINF_A16_MASK")) m->a16_mask = static_cast<int>(std::strtol(am, nullptr, 0)) & 0xf;
     }
     m->a16 = m->a16_mask != 0;
-    require(!(m->a16 && rt->use_step_kernel), "the persistent step kernel runs W8A8 only");
+    if (rt->use_step_kernel && m->int8) {  // the persistent step kernel runs INT8 weight-only
+      require(rt->int8_act != DSINF_INT8_W8A8, "the persistent step kernel runs INT8 as W8A16 (weight-only)");
+      m->a16_mask = 0xf;
+      m->a16 = true;
+    }
     m->attn_chunks = ops::attention_chunks(m->B, static_cast<int>(m->Hl));
     {
       const char* fs = std::getenv("DSINF_FUSE_STATS");

@@ -241,18 +241,25 @@ __global__ void __launch_bounds__(kFThreads) prefill_attention_mma_kernel(const 
       mrow[r] = mn;
       lrow[r] *= corr[r];
     }
-    uint32_t pa[kFK / 16][4];
+    // P as a sum of two fp16 terms (hi + lo, ~22 significant bits): the P.V product then carries
+    // the fp32 probabilities of the decode attention instead of fp16-rounded ones.  A 2^-11
+    // relative error in the attention output is harmless in fp16 but flips int8 quantisation
+    // steps of the attn-out activations (W8A8) often enough to show in the logits.
+    uint32_t pa[kFK / 16][4], pl[kFK / 16][4];
 #pragma unroll
     for (int n = 0; n < kFK / 8; ++n) {
-      float pe[4];
+      float pe[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float m = mrow[e >> 1];
         pe[e] = sc[n][e] == -INFINITY ? 0.f : expf(sc[n][e] - m);
         lrow[e >> 1] += pe[e];
+        lo[e] = pe[e] - __half2float(__float2half_rn(pe[e]));
       }
       pa[n >> 1][(n & 1) * 2 + 0] = gemm::dev::pack_h2(pe[0], pe[1]);
       pa[n >> 1][(n & 1) * 2 + 1] = gemm::dev::pack_h2(pe[2], pe[3]);
+      pl[n >> 1][(n & 1) * 2 + 0] = gemm::dev::pack_h2(lo[0], lo[1]);
+      pl[n >> 1][(n & 1) * 2 + 1] = gemm::dev::pack_h2(lo[2], lo[3]);
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -272,12 +279,15 @@ __global__ void __launch_bounds__(kFThreads) prefill_attention_mma_kernel(const 
         // A fragment order (a0 a1 a2 a3) = (row g k0-7, row g+8 k0-7, row g k8-15, row g+8 k8-15)
         ptx::mma_f16(o[2 * n2], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
         ptx::mma_f16(o[2 * n2 + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+        ptx::mma_f16(o[2 * n2], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b0, b1);
+        ptx::mma_f16(o[2 * n2 + 1], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b2, b3);
       }
       if constexpr (NT % 2 == 1) {
         uint32_t b0, b1, b2, b3;
         const int n = NT - 1;
         ldsm_x4_t(ptx::smem_u32(vs + key * LD + n * 8), b0, b1, b2, b3);
         ptx::mma_f16(o[n], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+        ptx::mma_f16(o[n], pl[kk][0], pl[kk][1], pl[kk][2], pl[kk][3], b0, b1);
       }
     }
   }

@@ -19,7 +19,7 @@ constexpr int kColTile = kWarpCols * kConsumerWarps;       // 128 output columns
 constexpr int kRowsPerStage = 32;                          // packed rows per pipeline stage
 constexpr int kBoxBytes = kWarpCols * 4 * kRowsPerStage;   // 4 KB: one 128B-swizzled TMA box
 constexpr int kStageBytes = kBoxBytes * kConsumerWarps;    // 16 KB
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;                             // ring slots (persistent step kernel: up to 13)
 constexpr int kMaxB = 16;                                  // batch rows per launch
 constexpr int kMaxSplit = 16;                              // K splits per column tile (cluster size)
 constexpr int kPartLd = kColTile + 4;                      // split-K partial row stride (floats)

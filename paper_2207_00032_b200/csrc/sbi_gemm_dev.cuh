@@ -601,9 +601,11 @@ struct Consumer {
         }
   }
   // W8A16 main loop; xword(it, kk, bt) returns the (b0, b1) x words of batch tile bt.
+  // `step` > 1: this warp group consumes every step-th ring slot (the persistent step kernel's
+  // interleaved consumer groups; stages % step == 0).
   template <class XWord>
   __device__ __forceinline__ void run_a16(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
-                                          uint32_t& phase, int n_iters, int cw, int lane, XWord xword) {
+                                          uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step = 1) {
     const uint8_t* wbox = ring + cw * kBoxBytes;
     for (int it = 0; it < n_iters; ++it) {
       ptx::mbar_wait(&hd.full[s], phase);
@@ -626,8 +628,8 @@ struct Consumer {
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
-      if (++s == stages) {
-        s = 0;
+      if ((s += step) >= stages) {
+        s -= stages;
         phase ^= 1;
       }
     }
@@ -641,7 +643,7 @@ struct Consumer {
         for (int e = 0; e < 4; ++e) acc[j][bt][e] = 0;
   }
   __device__ __forceinline__ void run(const uint8_t* ring, Header& hd, int stages, int& s, uint32_t& phase,
-                                      int n_iters, const uint32_t* sx, int xrw, int B, int cw, int lane) {
+                                      int n_iters, const uint32_t* sx, int xrw, int B, int cw, int lane, int step = 1) {
     const uint32_t* xrow[kNB8];
     bool xvalid[kNB8];
 #pragma unroll
@@ -653,7 +655,7 @@ struct Consumer {
     for (int it = 0; it < n_iters; ++it) {
       ptx::mbar_wait(&hd.full[s], phase);
       const uint8_t* sw = wbox + s * kStageBytes;
-      const int xr0 = it * kRowsPerStage;
+      const int xr0 = it * kRowsPerStage * step;
 #pragma unroll
       for (int ks = 0; ks < kRowsPerStage / 8; ++ks) {
         uint32_t b0[kNB8], b1[kNB8];
@@ -682,8 +684,8 @@ struct Consumer {
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);
-      if (++s == stages) {
-        s = 0;
+      if ((s += step) >= stages) {
+        s -= stages;
         phase ^= 1;
       }
     }

@@ -1,5 +1,6 @@
 // Persistent decode-step kernel: one launch runs a whole decode step (embedding, every layer's
-// Deep-Fusion regions, LM head and greedy argmax) for tensor-parallel degree 1.
+// Deep-Fusion regions, LM head and greedy argmax) for tensor-parallel degree 1, fp16 or INT8
+// weight-only (W8A16) weights, on a static per-CTA schedule (step_kernel.cu).
 #pragma once
 
 #include <cstdint>
@@ -16,9 +17,11 @@ namespace step {
 // Host description of one step; pointers are device pointers owned by the model.
 struct StepDesc {
   int B = 1, L = 0, H = 1, d = 64, max_ctx = 0, V = 0, Vl = 0;
-  bool int8 = false;
-  // per layer, in order: qkv (PRO_LN, EPI_QKV), attn-out (PRO_F16/QUANT, EPI_RESID),
-  // up (PRO_LN, EPI_GELU_F16), down (PRO_F16/QUANT, EPI_RESID); then the LM head (EPI_F32).
+  bool int8 = false;  // int8 layer weights (then every layer GEMM must be W8A16: Params::a16)
+  // per layer, in order: qkv (PRO_LN, EPI_QKV), attn-out (PRO_F16, EPI_RESID), up (PRO_LN,
+  // EPI_GELU_F16), down (PRO_F16, EPI_RESID); then the LM head (PRO_LN, EPI_F32).  The LayerNorm
+  // GEMMs read their row sums from ln_stats_in; the residual GEMMs (and the embedding) write the
+  // next LayerNorm's into ln_stats_out (slots zeroed per step by the caller, as am_key).
   std::vector<gemm::Params> gemms;
   std::vector<ops::AttnParams> attn;  // per layer
   ops::EmbedParams embed{};
@@ -26,6 +29,7 @@ struct StepDesc {
   int32_t* next_tok = nullptr;
   int32_t* hist = nullptr;
   int* pos = nullptr;
+  unsigned long long* am_key = nullptr;  // [B] greedy-argmax keys, zeroed before every launch
 };
 
 class StepProgram {
@@ -39,11 +43,13 @@ class StepProgram {
   void release();
   ~StepProgram() { release(); }
   int grid() const { return grid_; }
+  int stages() const { return stages_; }
   bool ready() const { return built_; }
 
  private:
   bool built_ = false;
   int grid_ = 0;
+  int stages_ = 0;
   size_t smem_ = 0;
   int variant_ = 0;
   int n_phases_ = 0;

@@ -7,7 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2207_00032_b200.engine import PRESETS, DecoderModel  # noqa: E402
+from paper_2207_00032_b200.engine import DecoderModel
+from paper_2207_00032_b200.presets import PRESETS  # noqa: E402
 
 p = PRESETS[os.environ.get("CFG", "gptj-6b")]
 variants = {"pdl": (dict(use_pdl=True), None), "nopdl": (dict(use_pdl=False), None), "pdl_mask0": (dict(use_pdl=True), "0"), "pdl_mask4": (dict(use_pdl=True), "4")}

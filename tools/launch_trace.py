@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 from paper_2207_00032_b200 import _capi as capi  # noqa: E402
-from paper_2207_00032_b200.engine import PRESETS, DecoderModel  # noqa: E402
+from paper_2207_00032_b200.engine import DecoderModel
+from paper_2207_00032_b200.presets import PRESETS  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 cfg = args[0] if len(args) > 0 else "gptj-6b"

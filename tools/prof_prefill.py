@@ -8,7 +8,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2207_00032_b200.engine import PRESETS, DecoderModel  # noqa: E402
+from paper_2207_00032_b200.engine import DecoderModel
+from paper_2207_00032_b200.presets import PRESETS  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "gptj-6b"
 dt = sys.argv[2] if len(sys.argv) > 2 else "fp16"

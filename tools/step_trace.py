@@ -14,13 +14,15 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2207_00032_b200 import _capi as capi  # noqa: E402
-from paper_2207_00032_b200.engine import PRESETS, DecoderModel  # noqa: E402
+from paper_2207_00032_b200.engine import DecoderModel
+from paper_2207_00032_b200.presets import PRESETS  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "gptj-6b"
 dt = sys.argv[2] if len(sys.argv) > 2 else "fp16"
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 p = PRESETS[cfg]
-m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt == "int8" else 2, batch=B, max_ctx=160, use_step_kernel=True)
+m = DecoderModel(p.hidden, p.layers, p.heads, p.vocab, dtype_bytes=1 if dt == "int8" else 2, batch=B, max_ctx=160,
+                 use_step_kernel=True, int8_act=capi.INT8_W8A16 if dt == "int8" else 0)
 m.set_prompt(np.random.default_rng(0).integers(0, p.vocab, (B, 128)).astype(np.int32))
 m.step(130)
 torch.cuda.synchronize()
