@@ -109,6 +109,7 @@ struct Prog {
   int max_ctx;
   int B, H, d, stages;
   int nomma;     // timing experiment: consumers only drain the ring
+  int inflight;  // producer in-flight cap (stages; 0 = ring depth)
   int l2_ahead;  // stages warmed into L2 beyond the ring while the ring is full
   int xrw;    // x slice row stride (words, == 8 mod 32)
   int x_cap;  // x words per row per chunk (multiple of 64)
@@ -134,7 +135,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 // slot: 0 consumer reaches the phase, 1 dependency satisfied, 2 consumer done, 3 producer issued the
-//       phase, 4 epilogue warp took a unit of the phase, 5 (unused), 6 a tile of the phase published
+//       phase, 4 epilogue warp took a unit of the phase, 5 first x slice built, 6 a tile of the phase published
 __device__ __forceinline__ void trace_rec(const Prog& P, int cta, int p, int slot) {
   if (P.trace) P.trace[(static_cast<size_t>(cta) * P.n_phases + p) * 8 + slot] = gtime();
 }
@@ -243,6 +244,17 @@ __device__ void producer(const Prog& P, uint8_t* ring, Header& hd, int cta, int 
     if (ld.p != last_p) {
       if (last_p >= 0) trace_rec(P, cta, last_p, 3);
       last_p = ld.p;
+    }
+    // in-flight cap: stage it - inflight must have landed before stage it is issued, so at most
+    // `inflight` stages per SM sit in the memory system's queues (the ring still buffers up to S
+    // landed stages); dependent loads of the consumers then queue behind ~inflight x 148 x 16 KB
+    // instead of S x 148 x 16 KB
+    if (P.inflight > 0 && it >= P.inflight) {
+      const int j = it - P.inflight;
+      const int sj = j % S;
+      const uint32_t pj = static_cast<uint32_t>((j / S) & 1);
+      while (!ptx::mbar_test_wait(&hd.full[sj], pj)) {
+      }
     }
     if (it >= S) {
       while (!ptx::mbar_test_wait(&hd.empty[s], ph ^ 1)) {
@@ -554,6 +566,11 @@ __device__ __forceinline__ void push_unit(Extra& ex, RingPos& rp, int phase, int
 
 __device__ void fill_x_attn(const Prog& P, const gemm::Params& gp, uint32_t* sx, float* mw, int row0, int nrows,
                             int ctid);
+template <int kR = 8>
+__device__ void fill_x_ln_fast(const gemm::Params& gp, uint32_t* sx, Header& hd, int row0, int nrows, int xrw,
+                               int ctid);
+template <int kR = 8>
+__device__ void fill_x_f16_fast(const gemm::Params& gp, uint32_t* sx, int row0, int nrows, int xrw, int ctid);
 
 template <bool kA16, int kNB8>
 __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch, int cta, int G, Header& hd,
@@ -597,9 +614,10 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
       });
     }
     if (lead) trace_rec(P, cta, p, 1);
-    if (full_x) gemm::dev::fill_x_ln_f16_pre(gp, sx, hd, 0, gp.K / 2, ctid);
+    if (full_x) fill_x_ln_fast(gp, sx, hd, 0, gp.K / 2, P.xrw, ctid);
   }
   if (full_x) all_bar();
+  if (full_x && lead) trace_rec(P, cta, p, 5);
   const int cap = full_x ? f.spt : P.x_cap / (kRowsPerStage * f.xw);  // stages per x chunk
   using Cons = gemm::dev::Consumer<kA16, kNB8, kA16>;
   Cons c;
@@ -625,13 +643,14 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
             });
           }
           if (gp.pro == gemm::PRO_LN)
-            gemm::dev::fill_x_ln_f16_pre(gp, sx, hd, row0, nrows, ctid);
+            fill_x_ln_fast(gp, sx, hd, row0, nrows, P.xrw, ctid);
           else if (f.dep == DEP_HEADS)
             fill_x_attn(P, gp, sx, mw, row0, nrows, ctid);
           else
-            gemm::dev::fill_x_slice<false>(gp, sx, hd, row0, nrows, ctid);
+            fill_x_f16_fast(gp, sx, row0, nrows, P.xrw, ctid);
         }
         all_bar();
+        if (lead && i == a && c0 == 0) trace_rec(P, cta, p, 5);
       }
       const uint32_t* xs = (full_x ? sx + row0 : sx);
       const int j0 = my_first(rp.gidx), cnt = my_count(rp.gidx, nn);
@@ -721,47 +740,173 @@ __device__ void attn_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
   if (ctid == 0) trace_rec(P, cta, p, 2);
 }
 
+// x builders: every load of a round is issued before any is used, so a build costs ONE dependent
+// L2 round trip (a round trip under full HBM streaming is a few microseconds: the generic
+// chunked builders' 3-5 sequential round trips made the x build the longest part of a phase).
+
+// LayerNorm'd fp16 words [row0, row0 + nrows) of every row (nrows, row0 even): the residual /
+// gamma / beta loads of a round (kR float4 per thread) are in flight together with the read of
+// the producer's fixed-point row sums.
+template <int kR>
+__device__ void fill_x_ln_fast(const gemm::Params& gp, uint32_t* sx, Header& hd, int row0, int nrows, int xrw,
+                               int ctid) {
+  const int K = gp.K, B = gp.B;
+  const int n2 = nrows / 2;  // float4 units (4 k = 2 fp16 words)
+  const int total = B * n2;
+  bool have_stats = false;
+  for (int base = ctid;; base += 128 * kR) {
+    float4 r[kR];
+    uint2 g[kR], be[kR];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int i = base + 128 * j;
+      r[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      g[j] = be[j] = make_uint2(0u, 0u);
+      if (i < total) {
+        const int b = i / n2;
+        const int k = 2 * row0 + 4 * (i - b * n2);
+        if (k < K) {  // K % 8 == 0
+          r[j] = __ldcg(reinterpret_cast<const float4*>(gp.res_in + static_cast<size_t>(b) * K + k));
+          g[j] = __ldg(reinterpret_cast<const uint2*>(gp.ln_g + k));
+          be[j] = __ldg(reinterpret_cast<const uint2*>(gp.ln_b + k));
+        }
+      }
+    }
+    if (!have_stats) {
+      if (ctid < B) gemm::dev::ln_from_sums(gp.ln_stats_in, ctid, gp.ln_inv_k, gp.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+      consumer_bar();
+      have_stats = true;
+    }
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int i = base + 128 * j;
+      if (i < total) {
+        const int b = i / n2, u = i - b * n2;
+        const int k = 2 * row0 + 4 * u;
+        uint2 w = make_uint2(0u, 0u);
+        if (k < K) {
+          const float mean = hd.mean[b], rstd = hd.rstd[b];
+          const __half2 g01 = *reinterpret_cast<const __half2*>(&g[j].x), g23 = *reinterpret_cast<const __half2*>(&g[j].y);
+          const __half2 b01 = *reinterpret_cast<const __half2*>(&be[j].x), b23 = *reinterpret_cast<const __half2*>(&be[j].y);
+          w.x = gemm::dev::pack_h2((r[j].x - mean) * rstd * __low2float(g01) + __low2float(b01),
+                                   (r[j].y - mean) * rstd * __high2float(g01) + __high2float(b01));
+          w.y = gemm::dev::pack_h2((r[j].z - mean) * rstd * __low2float(g23) + __low2float(b23),
+                                   (r[j].w - mean) * rstd * __high2float(g23) + __high2float(b23));
+        }
+        *reinterpret_cast<uint2*>(sx + b * xrw + 2 * u) = w;
+      }
+    }
+    if (base + 128 * kR >= total) break;
+  }
+}
+
+// Plain fp16 x (PRO_F16, x_ld % 8 == 0, 16-byte aligned base) words [row0, row0 + nrows)
+// (row0, nrows multiples of 4): 16-byte loads, kR per thread per round.
+template <int kR>
+__device__ void fill_x_f16_fast(const gemm::Params& gp, uint32_t* sx, int row0, int nrows, int xrw, int ctid) {
+  const int K = gp.K, B = gp.B;
+  const __half* x = static_cast<const __half*>(gp.x);
+  const int n4 = nrows / 4;  // uint4 units (8 k)
+  const int total = B * n4;
+  for (int base = ctid; base < total; base += 128 * kR) {
+    uint4 v[kR];
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int i = base + 128 * j;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (i < total) {
+        const int b = i / n4;
+        const int k = 2 * row0 + 8 * (i - b * n4);
+        if (k < K) v[j] = __ldcg(reinterpret_cast<const uint4*>(x + static_cast<size_t>(b) * gp.x_ld + k));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kR; ++j) {
+      const int i = base + 128 * j;
+      if (i < total) {
+        const int b = i / n4;
+        *reinterpret_cast<uint4*>(sx + b * xrw + 4 * (i - b * n4)) = v[j];
+      }
+    }
+  }
+}
+
 // attn-out x slice (fp16 words [row0, row0 + nrows) of every row) from the attention partials:
 // per (row, head) the C chunks merge as exp(m_c - M)-weighted sums divided by the total sum --
 // the standalone attention kernel's merge, in the same order.  `mw` holds the merge weights.
 __device__ void fill_x_attn(const Prog& P, const gemm::Params& gp, uint32_t* sx, float* mw, int row0, int nrows,
                             int ctid) {
+  constexpr int kW = 4, kMaxC = 8;
   const int C = P.attn_chunks, d = P.d, H = P.H, B = gp.B;
   const int k0 = 2 * row0, k1 = min(gp.K, 2 * (row0 + nrows));
   const int h0 = k0 / d, nh = (k1 - 1) / d - h0 + 1;
-  for (int i = ctid; i < B * nh; i += 128) {
-    const int b = i / nh, h = h0 + (i - b * nh);
-    const float* base = P.attn_ws + (static_cast<size_t>(b) * H + h) * C * (d + 2);
-    float M = -INFINITY;
-    for (int c = 0; c < C; ++c) M = fmaxf(M, __ldcg(base + c * (d + 2) + d));
-    float L = 0.f;
-    for (int c = 0; c < C; ++c) {
-      const float mc = __ldcg(base + c * (d + 2) + d);
-      const float w = mc == -INFINITY ? 0.f : expf(mc - M);
-      mw[i * (C + 1) + c] = w;
-      L += mc == -INFINITY ? 0.f : __ldcg(base + c * (d + 2) + d + 1) * w;
-    }
-    mw[i * (C + 1) + C] = 1.0f / L;
-  }
-  consumer_bar();
   const int xrw = P.xrw;
-  for (int i = ctid; i < B * nrows; i += 128) {
-    const int b = i / nrows, w = i - b * nrows;
-    const int k = 2 * (row0 + w);
-    uint32_t word = 0u;
-    if (k < gp.K) {
-      const int h = k / d, dim = k - h * d;
-      const float* base = P.attn_ws + (static_cast<size_t>(b) * H + h) * C * (d + 2) + dim;
-      const float* wt = mw + (b * nh + (h - h0)) * (C + 1);
-      float a0 = 0.f, a1 = 0.f;
-      for (int c = 0; c < C; ++c) {
-        const float2 o = __ldcg(reinterpret_cast<const float2*>(base + c * (d + 2)));
-        a0 = fmaf(wt[c], o.x, a0);
-        a1 = fmaf(wt[c], o.y, a1);
-      }
-      word = gemm::dev::pack_h2(a0 * wt[C], a1 * wt[C]);
+  const int total = B * nrows;
+  bool have_w = false;
+  for (int base = ctid;; base += 128 * kW) {
+    // the partial outputs of this round's words, issued before the merge weights are read
+    float2 o[kW][kMaxC];
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      const int i = base + 128 * j;
+      const int b = i / nrows, w = i - b * nrows;
+      const int k = 2 * (row0 + w);
+      const bool ok = i < total && k < gp.K;
+      const int h = ok ? k / d : 0, dim = k - h * d;
+      const float* pb = P.attn_ws + (static_cast<size_t>(b) * H + h) * C * (d + 2) + dim;
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)
+        o[j][c] = (ok && c < C) ? __ldcg(reinterpret_cast<const float2*>(pb + c * (d + 2))) : make_float2(0.f, 0.f);
     }
-    sx[b * xrw + w] = word;
+    if (!have_w) {
+      // per (row, head): chunk weights exp(m_c - M) and 1 / sum (the standalone kernel's merge)
+      for (int i = ctid; i < B * nh; i += 128) {
+        const int b = i / nh, h = h0 + (i - b * nh);
+        const float* pb = P.attn_ws + (static_cast<size_t>(b) * H + h) * C * (d + 2);
+        float mc[kMaxC], lc[kMaxC];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          mc[c] = c < C ? __ldcg(pb + c * (d + 2) + d) : -INFINITY;
+          lc[c] = c < C ? __ldcg(pb + c * (d + 2) + d + 1) : 0.f;
+        }
+        float M = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) M = fmaxf(M, mc[c]);
+        float L = 0.f;
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          if (c >= C) break;
+          const float wgt = mc[c] == -INFINITY ? 0.f : expf(mc[c] - M);
+          mw[i * (C + 1) + c] = wgt;
+          L += mc[c] == -INFINITY ? 0.f : lc[c] * wgt;
+        }
+        mw[i * (C + 1) + C] = 1.0f / L;
+      }
+      consumer_bar();
+      have_w = true;
+    }
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      const int i = base + 128 * j;
+      if (i >= total) break;
+      const int b = i / nrows, w = i - b * nrows;
+      const int k = 2 * (row0 + w);
+      uint32_t word = 0u;
+      if (k < gp.K) {
+        const int h = k / d;
+        const float* wt = mw + (b * nh + (h - h0)) * (C + 1);
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c) {
+          if (c >= C) break;
+          a0 = fmaf(wt[c], o[j][c].x, a0);
+          a1 = fmaf(wt[c], o[j][c].y, a1);
+        }
+        word = gemm::dev::pack_h2(a0 * wt[C], a1 * wt[C]);
+      }
+      sx[b * xrw + w] = word;
+    }
+    if (base + 128 * kW >= total) break;
   }
 }
 
@@ -958,6 +1103,9 @@ void StepProgram::build(const StepDesc& D) {
     gemm::Params& gp = params[idx];
     require(gp.N % 4 == 0, "step kernel: out_dim must be a multiple of 4");
     require(gp.K % 8 == 0, "step kernel: in_dim must be a multiple of 8");
+    if (gp.pro == gemm::PRO_F16 && dep == DEP_TILES)
+      require(gp.x_ld % 8 == 0 && (reinterpret_cast<uintptr_t>(gp.x) & 15) == 0,
+              "step kernel: fp16 x rows must be 16-byte aligned");
     Phase f{};
     f.kind = kind;
     f.idx = idx;
@@ -1060,6 +1208,7 @@ void StepProgram::build(const StepDesc& D) {
   P.stages = stages;
   P.nomma = env_int("DSINF_STEP_NOMMA", 0);
   P.l2_ahead = std::max(0, env_int("DSINF_STEP_L2", 0));
+  P.inflight = std::max(0, env_int("DSINF_STEP_INFLIGHT", 0));
   P.xrw = xrw;
   P.x_cap = x_cap;
   P.x_bytes = static_cast<int>(x_bytes);

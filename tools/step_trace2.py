@@ -47,22 +47,23 @@ def pct(a):
     return f"{np.percentile(a, 50):6.2f} {np.percentile(a, 90):6.2f} {np.max(a):6.2f}"
 
 
-print("kind   dep-wait p50/p90/max     work p50/p90/max      release->published   prev-published->release")
+print("kind   dep-wait p50/p90/max     work p50/p90/max      x-build p50/p90/max   release->published   prev-published->release")
 for kind in ("qkv", "attn", "o", "up", "down", "lm"):
     idx = [i for i in range(1, ph.value) if names[i] == kind]
     if kind != "lm":
         idx = idx[2:-1] if len(idx) > 4 else idx
-    w, k, spans, gaps = [], [], [], []
+    w, k, xb, spans, gaps = [], [], [], [], []
     for i in idx:
         c = t[:, i, :]
         w.append(c[:, 1] - c[:, 0])
         k.append(c[:, 2] - c[:, 1])
+        xb.append(c[:, 5] - c[:, 1])
         pub = np.nanmax(c[:, 6]) if kind != "attn" else np.nanmax(c[:, 2])
         spans.append(pub - np.nanmin(c[:, 1]))
         prev = t[:, i - 1, :]
         ppub = np.nanmax(prev[:, 6]) if names[i - 1] != "attn" else np.nanmax(prev[:, 2])
         gaps.append(np.nanmin(c[:, 1]) - ppub)
-    print(f"{kind:5s} {pct(np.concatenate(w))}   {pct(np.concatenate(k))}   {np.nanmean(spans):8.2f}   {np.nanmean(gaps):8.2f}")
+    print(f"{kind:5s} {pct(np.concatenate(w))}   {pct(np.concatenate(k))}   {pct(np.concatenate(xb))}   {np.nanmean(spans):8.2f}   {np.nanmean(gaps):8.2f}")
 print("layer 3 timeline (us): phase  first-release  last-consumer-end  last-publish  producer-issued(max)")
 for i in range(1 + 5 * 3, 1 + 5 * 4):
     c = t[:, i, :]
