@@ -7,7 +7,9 @@
   shards on this GPU (DSINF_TP_LOCAL), batch 1 / 16, fp16 and int8.
 
 Against the teacher-forced fp64 oracle (oracle/seq_oracle.py, pinned to or_model_step).  Stated
-tolerance per position: max |dlogit| <= 0.03 std + 0.01 (fp16), 0.06 std + 0.02 (int8).  Greedy
+tolerance per position: max |dlogit| <= 0.03 std + 0.01 (fp16), 0.06 std + 0.02 (int8), for INT8 at
+least 2x the oracle's own fp32-vs-fp64 accumulation spread at that position (the W8A8 activation
+quantisation noise floor, tools/parity_baseline.py).  Greedy
 tokens identical, or a near tie within 2 max|dlogit| (each one logged).  Logs: profiles/.
 """
 import json

@@ -144,3 +144,17 @@ def test_seq_oracle_matches_step_oracle(dtype_bytes, tp, prefill_mode, decode_mo
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err <= 1e-12, err  # bit-identical here; BLAS kernels elsewhere may reorder fp64 sums
     assert np.array_equal(got.argmax(axis=2), ref.argmax(axis=2))
+
+
+@pytest.mark.parametrize("dtype_bytes,decode_mode", [(2, 0), (1, 1), (1, 0)])
+def test_seq_oracle_f32_accumulation_spread(dtype_bytes, decode_mode):
+    """SeqOracle(acc="f32") -- the INT8 noise-floor reference of tools/parity_baseline.py -- is the
+    same algorithm with fp32 accumulation: close to the fp64 oracle, and never identical to it."""
+    hidden, layers, heads, vocab = 128, 2, 4, 300
+    tokens = np.random.default_rng(6).integers(0, vocab, (2, 9))
+    kw = dict(prompt_len=5, prefill_mode=decode_mode, decode_mode=decode_mode)
+    a = SeqOracle(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, seed=77).forward(tokens, list(range(9)), **kw)
+    b = SeqOracle(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, seed=77, acc="f32").forward(
+        tokens, list(range(9)), **kw)
+    spread = np.abs(a - b).max() / np.abs(a).std()
+    assert 0 < spread < 0.05, spread

@@ -13,6 +13,12 @@ rows W8A8 as the tcgen05 prefill, generated rows in the decode's per-GEMM modes)
 
 Checks per (sequence, position):
   - max |logit_gpu - logit_oracle| <= tol, tol = 0.03 std + 0.01 (fp16), 0.06 std + 0.02 (int8);
+    INT8 additionally allows 2x the oracle's own noise floor at that position: the same oracle with
+    fp32 instead of fp64 GEMM/attention accumulation (SeqOracle(acc="f32"), a second correct
+    implementation) differs from the fp64 one by `spread`, and tol_int8 = max(tol, 2 spread).
+    W8A8 activation quantisation is discontinuous -- an fp16-ulp difference in an activation moves
+    its int8 code by one step -- so every W8A8 row (the prompt rows of the tcgen05 prefill, all
+    decode rows at TP > 1 and B = 16) carries this floor; W8A16 rows do not quantise activations;
   - the GPU's greedy token equals the oracle's argmax, or the mismatch is a near tie: the oracle's
     logit of the GPU token is within 2 max|dlogit| of its top logit (logged with both numbers);
   - reported: the number of positions whose oracle top-1/top-2 margin is below tol (where a flip
@@ -76,7 +82,8 @@ def auto_mask(batch, tp):
     return 0x10e if tp == 1 else 0x100
 
 
-def compare(name, dtype, tokens, glog, olog):
+def compare(name, dtype, tokens, glog, olog, spread=None):
+    """spread [B][GEN]: max |oracle_f64 - oracle_f32| per position (INT8 noise floor) or None."""
     tr, ta = tolerance(dtype)
     rows = []
     worst = 0.0
@@ -86,14 +93,21 @@ def compare(name, dtype, tokens, glog, olog):
         for k in range(GEN):
             g, o = glog[b, k], olog[b, k]
             err = float(np.abs(g - o).max())
-            tol = tr * float(o.std()) + ta
+            tol = tol_base = tr * float(o.std()) + ta
+            floor = None
+            if spread is not None:
+                floor = float(spread[b, k])
+                tol = max(tol, 2.0 * floor)
             worst = max(worst, err / tol)
             srt = np.sort(o)
             margin = float(srt[-1] - srt[-2])
             near += margin <= tol
             gt = int(tokens[b, PROMPT + k])
             ot = int(np.argmax(o))
-            row = {"b": b, "k": k, "err": round(err, 5), "tol": round(tol, 5), "margin": round(margin, 5)}
+            row = {"b": b, "k": k, "err": round(err, 5), "tol": round(tol, 5), "tol_base": round(tol_base, 5),
+                   "margin": round(margin, 5)}
+            if floor is not None:
+                row["oracle_f32_spread"] = round(floor, 5)
             if err > tol:
                 bad.append(row)
             if gt != ot:
@@ -105,6 +119,8 @@ def compare(name, dtype, tokens, glog, olog):
             rows.append(row)
     return {"case": name, "dtype": dtype, "positions": B * GEN, "worst_err_over_tol": round(worst, 4),
             "max_abs_err": round(max(r["err"] for r in rows), 5), "near_ties_below_tol": int(near),
+            "max_oracle_f32_spread": None if spread is None else round(float(np.max(spread)), 5),
+            "positions_above_base_tol": sum(1 for r in rows if r["err"] > r["tol_base"]),
             "token_mismatches": mism, "failures": bad, "ok": not bad,
             "tokens_identical": sum(1 for r in rows if "gpu_token" not in r)}
 
@@ -138,15 +154,28 @@ def run_config(label, hidden, layers, heads, vocab, *, tp, dtypes, batches, log=
             olog = so.forward(np.array(keys), list(range(PROMPT - 1, PROMPT + GEN - 1)), prompt_len=PROMPT,
                               prefill_mode=0, decode_mode=mode)
             log(f"[{label}] oracle {dtype} mode={mode:#x}: {len(keys)} sequences, {time.time() - t0:.1f}s")
+            ospread = None
+            if dtype == "int8":  # the INT8 noise floor: the fp32-accumulation oracle on the same sequences
+                t0 = time.time()
+                so32 = SeqOracle(hidden, layers, heads, vocab, dtype_bytes=1, tp=tp, seed=SEED, acc="f32")
+                olog32 = so32.forward(np.array(keys), list(range(PROMPT - 1, PROMPT + GEN - 1)), prompt_len=PROMPT,
+                                      prefill_mode=0, decode_mode=mode)
+                ospread = np.abs(olog.astype(np.float64) - olog32.astype(np.float64)).max(axis=2)
+                del olog32
+                log(f"[{label}] oracle f32 {dtype} mode={mode:#x}: {time.time() - t0:.1f}s, "
+                    f"spread max {ospread.max():.4f}")
             index = {k: i for i, k in enumerate(keys)}
             for B in bs:
                 toks, lg, meta = runs[B]
-                ol = np.stack([olog[index[tuple(toks[b, :PROMPT + GEN - 1].tolist())]] for b in range(B)])
-                r = compare(f"{label} {dtype} B={B}", dtype, toks, lg, ol)
+                ix = [index[tuple(toks[b, :PROMPT + GEN - 1].tolist())] for b in range(B)]
+                ol = np.stack([olog[i] for i in ix])
+                sp = None if ospread is None else np.stack([ospread[i] for i in ix])
+                r = compare(f"{label} {dtype} B={B}", dtype, toks, lg, ol, sp)
                 r.update({"batch": B, "tp": tp, "layers": layers, "hidden": hidden, "int8_oracle_mode": mode,
                           "gpu": meta})
                 log(f"[{label}] {dtype} B={B}: worst err/tol {r['worst_err_over_tol']}, max|dlogit| "
-                    f"{r['max_abs_err']}, tokens identical {r['tokens_identical']}/{r['positions']}, near ties "
+                    f"{r['max_abs_err']} (oracle f32 spread {r['max_oracle_f32_spread']}, above base tol "
+                    f"{r['positions_above_base_tol']}), tokens identical {r['tokens_identical']}/{r['positions']}, near ties "
                     f"{r['near_ties_below_tol']}, mismatches {len(r['token_mismatches'])}, ok {r['ok']}")
                 results.append(r)
     return results
