@@ -122,6 +122,13 @@ int dsinf_pack_weights_device(const void* w_rowmajor, int32_t src_dtype, int64_t
  * IEEE divide), q = clamp(rint(w / s_n), -127, 127); packed with pack_M = 4. */
 int dsinf_quantize_weights_int8(const void* w_rowmajor_f16, int64_t N, int64_t K,
                                 int8_t* packed_i8, float* row_scales, void* stream);
+/* INT8 K-group weight quantisation ("per-group dequant"; SURVEY §8c K-group
+ * recipe): every `group` (= 128) consecutive k of an output row share an fp16 scale
+ * s = fp16(max|w| / 127) (fp32 divide, round to nearest; 1 for an all-zero group) and
+ * q = clamp(rint(w / s), -127, 127) with an fp32 divide; packed with pack_M = 4 like the row mode,
+ * group_scales_f16 [ceil(K/group)][N].  The W8A16 GEMM dequantises w = fp16(q * s) per group. */
+int dsinf_quantize_weights_int8_groups(const void* w_rowmajor_f16, int64_t N, int64_t K, int32_t group,
+                                       int8_t* packed_i8, void* group_scales_f16, void* stream);
 /* Per-token activation quantisation (same formula, scale per row of x). */
 int dsinf_quantize_activations_int8(const void* x_f16, int64_t B, int64_t K, int8_t* xq,
                                     float* scales, void* stream);
@@ -152,6 +159,9 @@ typedef struct dsinf_gemm_args {
   int32_t epilogue;       /* DSINF_EPI_* */
   int32_t ksplit;         /* 0 = launch plan chooses; else cluster split count {1,2,4,8,16} */
   int32_t int8_act;       /* I8 weights: DSINF_INT8_W8A8 (int8 x, int32 accumulate) or DSINF_INT8_W8A16 */
+  const void* w_group_scales; /* W8A16 only, optional: fp16 [ceil(K/128)][N] K-group scales
+                                 (dsinf_quantize_weights_int8_groups); w_scales is then unused */
+  int32_t group_size;     /* 0: per-output-row scales; 128: K-group scales */
 } dsinf_gemm_args;
 
 int dsinf_gemm(const dsinf_gemm_args* args, void* stream);
@@ -209,6 +219,10 @@ typedef struct dsinf_model_config { /* infersim::ModelConfig (model.hpp:42-64), 
 #define DSINF_TP_NONE 0
 #define DSINF_TP_NCCL 1  /* one process per GPU, NCCL all-reduce over NVLink */
 #define DSINF_TP_LOCAL 2 /* all shards on this device (single-GPU sharding check) */
+#define DSINF_TP_IPC 4   /* one process per rank, every cross-rank exchange over CUDA-IPC peer memory
+                            (fused all-reduce in the GEMM epilogues, argmax keys in select): no NCCL.
+                            Ranks may share a device.  Handles are exchanged by the caller:
+                            dsinf_model_ipc_handle -> all-gather -> dsinf_model_ipc_attach. */
 #define DSINF_TP_SLICE 3 /* rank tp_rank's shard alone on this device, collectives skipped: per-rank
                             step timing of a TP model on one GPU (outputs are not the model's) */
 
@@ -235,6 +249,13 @@ typedef struct dsinf_model dsinf_model;
 int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config* rt,
                        void* nccl_comm, dsinf_model** out);
 int dsinf_model_destroy(dsinf_model* m);
+/* DSINF_TP_IPC: this rank's CUDA-IPC handles (an opaque blob of *len bytes, the same size on every
+ * rank; out may be NULL to query the size).  The caller all-gathers the blobs in rank order (any
+ * host channel: gloo, MPI, sockets) and passes the t * len bytes to dsinf_model_ipc_attach before
+ * the first decode step.  Replaces the NCCL handle all-gather of DSINF_TP_NCCL's fused all-reduce
+ * (costmodel.hpp:84-85: the per-layer all-reduce moved into the producing GEMM's epilogue). */
+int dsinf_model_ipc_handle(dsinf_model* m, void* out, int64_t cap, int64_t* len);
+int dsinf_model_ipc_attach(dsinf_model* m, const void* all, int64_t len);
 /* Load B prompts of prompt_len tokens (host int32 [B][prompt_len]) and reset position 0. */
 int dsinf_model_set_prompt(dsinf_model* m, const int32_t* prompt_host, int64_t prompt_len,
                            void* stream);

@@ -235,6 +235,29 @@ void or_quant_rows(const float* x, int64_t rows, int64_t K, int8_t* q, float* sc
   }
 }
 
+/* K-group quantisation (dsinf_quantize_weights_int8_groups; SURVEY §8c K-group recipe, group = 128):
+ * per (row, group) s = fp16(max|w| / 127) (fp32 divide, round to nearest even; 1 for an all-zero or
+ * fp16-underflowing group), q = clamp(rint(w / s), +-127) with an fp32 divide by the fp16 scale.
+ * scales_f16 [ceil(K/group)][rows] as fp16 bits. */
+void or_quant_groups(const float* x, int64_t rows, int64_t K, int64_t group, int8_t* q, uint16_t* scales_f16) {
+  const int64_t G = (K + group - 1) / group;
+#pragma omp parallel for schedule(static) if (rows * K > (1 << 20))
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t g = 0; g < G; ++g) {
+      const int64_t k0 = g * group, k1 = k0 + group < K ? k0 + group : K;
+      float mx = 0.0f;
+      for (int64_t k = k0; k < k1; ++k) {
+        const float a = fabsf(x[r * K + k]);
+        if (a > mx) mx = a;
+      }
+      uint16_t sh = or_f32_to_f16(q_scale(mx));
+      if (or_f16_to_f32(sh) == 0.0f) sh = or_f32_to_f16(1.0f);
+      scales_f16[g * rows + r] = sh;
+      const float s = or_f16_to_f32(sh);
+      for (int64_t k = k0; k < k1; ++k) q[r * K + k] = q_one(x[r * K + k], s);
+    }
+}
+
 void or_gemm_i8(const int8_t* wq, const float* ws, const int8_t* xq, const float* xs, int64_t N, int64_t K,
                 int64_t B, int32_t* acc, float* y) {
 #pragma omp parallel for schedule(static)

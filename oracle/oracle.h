@@ -55,6 +55,7 @@ double or_round_f16(double v);
 
 /* INT8: per-row symmetric scale = max|row| / 127 (fp32 division), q = clamp(rint(x/s)) */
 void or_quant_rows(const float* x, int64_t rows, int64_t K, int8_t* q, float* scales);
+void or_quant_groups(const float* x, int64_t rows, int64_t K, int64_t group, int8_t* q, uint16_t* scales_f16);
 /* y[b][n] = fp32(fp32(acc) * xs[b]) * ws[n], acc = sum_k q_w[n][k] q_x[b][k] exact */
 void or_gemm_i8(const int8_t* wq, const float* ws, const int8_t* xq, const float* xs, int64_t N, int64_t K,
                 int64_t B, int32_t* acc, float* y);

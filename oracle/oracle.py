@@ -64,6 +64,7 @@ if _or is not None:
     _or.or_f16_to_f32.restype = C.c_float
     _or.or_f16_to_f32.argtypes = [C.c_uint16]
     _or.or_quant_rows.argtypes = [P(C.c_float), C.c_int64, C.c_int64, P(C.c_int8), P(C.c_float)]
+    _or.or_quant_groups.argtypes = [P(C.c_float), C.c_int64, C.c_int64, C.c_int64, P(C.c_int8), P(C.c_uint16)]
     _or.or_gemm_i8.argtypes = [P(C.c_int8), P(C.c_float), P(C.c_int8), P(C.c_float), C.c_int64, C.c_int64,
                                C.c_int64, P(C.c_int32), P(C.c_float)]
     _or.or_synth_base.restype = C.c_uint64
@@ -167,6 +168,31 @@ def quant_rows(x):
     oracle_lib().or_quant_rows(x.ctypes.data_as(P(C.c_float)), R, K, q.ctypes.data_as(P(C.c_int8)),
                                s.ctypes.data_as(P(C.c_float)))
     return q, s
+
+
+def quant_groups(x, group=128):
+    """or_quant_groups: (q int8 [R][K], fp16 scales [ceil(K/group)][R] as float16)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    R, K = x.shape
+    q = np.zeros((R, K), dtype=np.int8)
+    s = np.zeros(((K + group - 1) // group, R), dtype=np.uint16)
+    oracle_lib().or_quant_groups(x.ctypes.data_as(P(C.c_float)), R, K, group, q.ctypes.data_as(P(C.c_int8)),
+                                 s.ctypes.data_as(P(C.c_uint16)))
+    return q, s.view(np.float16)
+
+
+def dequant_groups(q, s16, group=128):
+    """The W8A16 K-group GEMM's effective weights: fp16(q * s) per element (fp32 product, one fp16
+    rounding -- what __hmul2 of the exact fp16 q and the fp16 scale computes)."""
+    R, K = q.shape
+    sc = np.repeat(s16.astype(np.float32).T, group, axis=1)[:, :K]
+    return (q.astype(np.float32) * sc).astype(np.float16).astype(np.float32)
+
+
+def gemm_a16_groups(q, s16, x16, group=128):
+    """y[B][N] = sum_k fp16(q s) x in fp64, rounded to fp32 (the GPU accumulates in fp32)."""
+    w = dequant_groups(q, s16, group).astype(np.float64)
+    return (np.asarray(x16, dtype=np.float64) @ w.T).astype(np.float32)
 
 
 def gemm_i8(wq, ws, xq, xs):

@@ -35,6 +35,7 @@ TP_NONE = 0
 TP_NCCL = 1
 TP_LOCAL = 2
 TP_SLICE = 3
+TP_IPC = 4
 
 TILING_1D = 0
 TILING_2D = 1
@@ -92,7 +93,8 @@ class GemmArgs(C.Structure):
     _fields_ = [("w_packed", C.c_void_p), ("w_dtype", C.c_int32), ("w_scales", C.c_void_p),
                 ("N", C.c_int64), ("K", C.c_int64), ("B", C.c_int64), ("x", C.c_void_p),
                 ("x_dtype", C.c_int32), ("x_scales", C.c_void_p), ("bias", C.c_void_p), ("out", C.c_void_p),
-                ("out_dtype", C.c_int32), ("epilogue", C.c_int32), ("ksplit", C.c_int32), ("int8_act", C.c_int32)]
+                ("out_dtype", C.c_int32), ("epilogue", C.c_int32), ("ksplit", C.c_int32), ("int8_act", C.c_int32),
+                ("w_group_scales", C.c_void_p), ("group_size", C.c_int32)]
 
 
 class LbArgs(C.Structure):
@@ -175,6 +177,7 @@ SIGNATURES = {
     "dsinf_exec_device": (C.c_int, [P(f64), i64, i32, P(GemmShape), P(GemmSchedule), P(f64), i64, i64, i32, P(f64), i64]),
     "dsinf_pack_weights_device": (C.c_int, [vp, i32, i64, i64, i32, vp, vp]),
     "dsinf_quantize_weights_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
+    "dsinf_quantize_weights_int8_groups": (C.c_int, [vp, i64, i64, C.c_int32, vp, vp, vp]),
     "dsinf_quantize_activations_int8": (C.c_int, [vp, i64, i64, vp, vp, vp]),
     "dsinf_gemm": (C.c_int, [P(GemmArgs), vp]),
     "dsinf_gemm_large_batch": (C.c_int, [P(LbArgs), vp]),
@@ -182,6 +185,8 @@ SIGNATURES = {
     "dsinf_attention_decode": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, vp, vp]),
     "dsinf_model_create": (C.c_int, [P(ModelConfig), P(RuntimeConfig), vp, P(vp)]),
     "dsinf_model_destroy": (C.c_int, [vp]),
+    "dsinf_model_ipc_handle": (C.c_int, [vp, vp, C.c_int64, C.POINTER(C.c_int64)]),
+    "dsinf_model_ipc_attach": (C.c_int, [vp, vp, C.c_int64]),
     "dsinf_model_set_prompt": (C.c_int, [vp, P(i32), i64, vp]),
     "dsinf_model_set_prompt_device": (C.c_int, [vp, vp, i64, vp]),
     "dsinf_decode_step": (C.c_int, [vp, vp]),

@@ -26,8 +26,12 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
   require(a.epilogue == DSINF_EPI_NONE || a.epilogue == DSINF_EPI_GELU, "unknown epilogue");
   require(!(a.epilogue == DSINF_EPI_GELU && a.out_dtype == DSINF_DT_F32), "GeLU epilogue writes F16");
   const bool i8w = a.w_dtype == DSINF_DT_I8;
+  require(a.group_size == 0 || a.group_size == ops::kI8Group, "group_size must be 0 (row scales) or 128");
+  if (a.group_size != 0)
+    require(i8w && a.int8_act == DSINF_INT8_W8A16 && a.w_group_scales != nullptr,
+            "K-group scales: I8 weights, DSINF_INT8_W8A16 and w_group_scales");
   if (i8w) {
-    require(a.w_scales != nullptr, "I8 weights need w_scales");
+    require(a.w_scales != nullptr || a.group_size != 0, "I8 weights need w_scales");
     require(a.x_dtype == DSINF_DT_F16 || a.x_dtype == DSINF_DT_I8, "x_dtype must be F16 or I8");
     if (a.x_dtype == DSINF_DT_I8) require(a.x_scales != nullptr, "I8 x needs x_scales");
     require(a.int8_act == DSINF_INT8_W8A8 || a.int8_act == DSINF_INT8_W8A16, "unknown int8_act");
@@ -36,16 +40,44 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     require(a.x_dtype == DSINF_DT_F16, "F16 weights take F16 x");
   }
   const int N = static_cast<int>(a.N), K = static_cast<int>(a.K);
+  // W8A8 with fp16 x: the per-token quantisation runs ONCE per launch (row_prep, the same recipe as
+  // the per-CTA PRO_QUANT prologue: scale = max|x| / 127, q = rint(x / scale)) into a stream-ordered
+  // scratch buffer, and the GEMM streams the int8 rows by TMA; every CTA re-quantising the whole row
+  // made the drop-in W8A8 GEMM 4-14x slower than the in-model plans at B = 16
+  const bool quant_once = i8w && a.int8_act == DSINF_INT8_W8A8 && a.x_dtype == DSINF_DT_F16 && K % 8 == 0 &&
+                          (reinterpret_cast<uintptr_t>(a.x) & 7) == 0;
+  void* xq_scratch = nullptr;
+  const int64_t bmax = std::min<int64_t>(gemm::kMaxB, a.B);
+  if (quant_once) DSINF_CUDA_CHECK(cudaMallocAsync(&xq_scratch, static_cast<size_t>(bmax) * (K + 4) + 256, s));
   for (int64_t b0 = 0; b0 < a.B; b0 += gemm::kMaxB) {
     const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
-    const int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
+    int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
     const void* xb = static_cast<const uint8_t*>(a.x) + b0 * a.K * xes;
+    const float* xsc = a.x_scales ? a.x_scales + b0 : nullptr;
+    if (quant_once) {
+      int8_t* xq = static_cast<int8_t*>(xq_scratch);
+      float* sc = reinterpret_cast<float*>(static_cast<uint8_t*>(xq_scratch) + ((static_cast<size_t>(bmax) * K + 255) / 256 * 256));
+      ops::PrepParams pp{};
+      pp.mode = ops::PREP_QUANT_I8;
+      pp.x = static_cast<const __half*>(xb);
+      pp.x_ld = K;
+      pp.out = xq;
+      pp.out_scale = sc;
+      pp.B = nb;
+      pp.K = K;
+      ops::row_prep(pp, s, false);
+      xb = xq;
+      xsc = sc;
+      xes = 1;
+    }
     const bool a16 = i8w && a.int8_act == DSINF_INT8_W8A16;
-    const bool ready_x = !i8w || a16 || a.x_dtype == DSINF_DT_I8;  // GEMM-ready x (no on-the-fly quantisation)
+    const bool x_i8 = a.x_dtype == DSINF_DT_I8 || quant_once;
+    const bool ready_x = !i8w || a16 || x_i8;  // GEMM-ready x (no on-the-fly quantisation)
     const bool xs = ready_x && gemm::prefer_x_stream(nb) && gemm::x_streamable(xb, K, K, i8w && !a16);
     const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs, a16);
     gemm::Params p{};
     p.w_scale = a.w_scales;
+    p.w_gscale = a.group_size != 0 ? static_cast<const __half*>(a.w_group_scales) : nullptr;
     p.N = N;
     p.K = K;
     p.rows = (K + (i8w ? 3 : 1)) / (i8w ? 4 : 2);
@@ -54,10 +86,10 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     p.x = xb;
     p.x_ld = K;
     if (i8w && !a16)
-      p.pro = a.x_dtype == DSINF_DT_I8 ? gemm::PRO_I8 : gemm::PRO_QUANT;
+      p.pro = x_i8 ? gemm::PRO_I8 : gemm::PRO_QUANT;
     else
       p.pro = gemm::PRO_F16;
-    p.x_scale = a.x_scales ? a.x_scales + b0 : nullptr;
+    p.x_scale = xsc;
     p.bias = static_cast<const __half*>(a.bias);
     const int oes = a.out_dtype == DSINF_DT_F32 ? 4 : 2;
     p.out = static_cast<uint8_t*>(a.out) + b0 * a.N * oes;
@@ -66,6 +98,7 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
                                         : (a.epilogue == DSINF_EPI_GELU ? gemm::EPI_GELU_F16 : gemm::EPI_F16);
     gemm::launch(p, plan, i8w, s, false);
   }
+  if (xq_scratch) DSINF_CUDA_CHECK(cudaFreeAsync(xq_scratch, s));
 }
 
 struct DeviceBuffer {
@@ -164,6 +197,17 @@ int dsinf_quantize_weights_int8(const void* w_rowmajor_f16, int64_t N, int64_t K
     require(N >= 1 && K >= 1, "gemm shape dims must be positive");
     ops::quantize_weights_i8(static_cast<const __half*>(w_rowmajor_f16), N, K, packed_i8, row_scales,
                              as_stream(stream));
+  });
+}
+
+int dsinf_quantize_weights_int8_groups(const void* w_rowmajor_f16, int64_t N, int64_t K, int32_t group,
+                                       int8_t* packed_i8, void* group_scales_f16, void* stream) {
+  return guarded([&] {
+    require(w_rowmajor_f16 && packed_i8 && group_scales_f16, "null pointer argument");
+    require(N >= 1 && K >= 1, "gemm shape dims must be positive");
+    require(group == ops::kI8Group, "group must be 128");
+    ops::quantize_weights_i8_groups(static_cast<const __half*>(w_rowmajor_f16), N, K, packed_i8,
+                                    static_cast<__half*>(group_scales_f16), as_stream(stream));
   });
 }
 

@@ -149,6 +149,11 @@ struct dsinf_model {
   // every rank's slots and signal a counter; the next LayerNorm prologue waits and sums the slots
   bool fused_ar = false;
   long long* step_ctr = nullptr;  // decode steps taken (fused all-reduce counter targets)
+  // DSINF_TP_IPC: argmax-key arrival counter (bumped by the peers' select kernels) and the peers'
+  // key arrays / counters as mapped into this process; ipc_ready once dsinf_model_ipc_attach ran
+  unsigned long long* key_flag = nullptr;
+  std::vector<unsigned long long*> peer_keys, peer_key_flag;
+  bool ipc_ready = false;
   std::vector<void*> ipc_maps;    // peer allocations opened with cudaIpcOpenMemHandle
   // x-streaming GEMM plans (gemm::Plan::x_stream): x reaches each stage by TMA next to the
   // weights instead of a per-CTA smem slice.  xs_ln: the LayerNorm GEMMs (QKV, MLP-up, LM head)
@@ -653,9 +658,12 @@ struct Enqueuer {
     const int N = static_cast<int>(3 * m.Hl * m.d);
     gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8);
     if (m.xs_ln) {
+      RedIn red;  // fused all-reduce: row_prep sums the ranks' MLP-down slots of layer l - 1
+      const bool use_slots = m.fused_ar && l > 0;
+      if (use_slots) red = red_in(sh, 1, l - 1);
       ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l), m.fuse_ln || l == 0 ? nullptr : sh.d_mlp,
            m.fuse_ln || l == 0 ? nullptr : sh.layers[l - 1].bdown, m.fuse_ln ? nullptr : sh.res[1], w.ln1g, w.ln1b,
-           m.q8g(0));
+           m.q8g(0), use_slots ? &red : nullptr);
     } else {
       p.pro = gemm::PRO_LN;
       p.res_in = sh.res[0];
@@ -736,8 +744,12 @@ struct Enqueuer {
     if (m.xs_ln) {
       if (m.fuse_ln)
         ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8g(2));
-      else
+      else if (m.fused_ar) {
+        RedIn red = red_in(sh, 0, l);  // row_prep sums the ranks' attn-out slots
+        ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.q8g(2), &red);
+      } else {
         ln_x(sh, p, sh.res[1], nullptr, sh.d_attn, w.bo, sh.res[0], w.ln2g, w.ln2b, m.q8g(2));
+      }
     } else {
       p.pro = gemm::PRO_LN;
       if (m.fuse_ln) {
@@ -1086,6 +1098,14 @@ struct Enqueuer {
     sp.hist = m.hist;
     sp.max_ctx = m.max_ctx;
     sp.step_ctr = m.step_ctr;
+    if (m.rt.tp_mode == DSINF_TP_IPC && m.t > 1) {
+      sp.ipc_t = m.t;
+      sp.ipc_rank = m.shards[0].rank;
+      for (int q = 0; q < m.t; ++q) {
+        sp.ipc_keys[q] = m.peer_keys[q];
+        sp.ipc_flag[q] = m.peer_key_flag[q];
+      }
+    }
     ops::select_token(sp, s, P(6));
     ++launches;
     m.ltrace_n = slot;
@@ -1165,9 +1185,12 @@ void validate_configs(const dsinf_model_config& c, const dsinf_runtime_config& r
   require((c.hidden_dim / c.num_heads) % 2 == 0, "head dim must be even (rotary pairs)");
   require(r.max_ctx >= 1 && r.max_ctx <= c.max_seq, "max_ctx must be in [1, max_seq]");
   if (r.tp_size > 1)
-    require(r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_LOCAL || r.tp_mode == DSINF_TP_SLICE,
+    require(r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_LOCAL || r.tp_mode == DSINF_TP_SLICE ||
+                r.tp_mode == DSINF_TP_IPC,
             "tp_size > 1 needs a TP mode");
-  if (r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_SLICE) require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
+  if (r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_SLICE || r.tp_mode == DSINF_TP_IPC)
+    require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
+  if (r.tp_mode == DSINF_TP_IPC) require(r.use_step_kernel == 0, "the persistent step kernel is TP = 1 only");
 }
 
 void build_rope(Model& m, cudaStream_t s) {
@@ -1183,7 +1206,13 @@ void build_rope(Model& m, cudaStream_t s) {
   DSINF_CUDA_CHECK(cudaMemcpyAsync(m.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, s));
 }
 
+void require_ipc_ready(const Model& m) {
+  require(m.rt.tp_mode != DSINF_TP_IPC || m.t == 1 || m.ipc_ready,
+          "DSINF_TP_IPC: call dsinf_model_ipc_attach with every rank's handles before decoding");
+}
+
 void enqueue_eager(Model& m, cudaStream_t s) {
+  require_ipc_ready(m);
   Enqueuer e{m, s, m.rt.use_pdl != 0};
   e.step();
   m.kernels_per_step = e.launches;
@@ -1191,6 +1220,7 @@ void enqueue_eager(Model& m, cudaStream_t s) {
 
 void ensure_graph(Model& m) {
   if (m.exec) return;
+  require_ipc_ready(m);
   DSINF_CUDA_CHECK(cudaStreamBeginCapture(m.cap_stream, cudaStreamCaptureModeThreadLocal));
   Enqueuer e{m, m.cap_stream, m.rt.use_pdl != 0};
   try {
@@ -1272,13 +1302,16 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       const char* far_req = std::getenv("DSINF_FUSED_AR");
       bool want_far = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) &&
                       far_req != nullptr && std::atoi(far_req) != 0;
+      if (rt->tp_mode == DSINF_TP_IPC && m->t > 1) want_far = true;  // the only exchange IPC mode has
       if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
         // the request is per process (environment) but every rank must pick the same plan, or one
         // rank waits on slot counters the others never bump: fused only if all t ranks ask for it
         require(nccl_comm != nullptr, "NCCL mode needs a communicator");
         want_far = nccl_vote_all(static_cast<nccl::Comm>(nccl_comm), want_far, m->t);
       }
-      m->xs_ln = rows16 && !want_far && gemm::prefer_x_stream(m->B, m->t > 1);
+      // the fused all-reduce runs on either plan: row_prep (x-streaming) or the per-CTA LayerNorm
+      // prologues (slice plan) sum the ranks' slots
+      m->xs_ln = rows16 && gemm::prefer_x_stream(m->B, m->t > 1);
       const char* od = std::getenv("DSINF_XS_OD");
       const int od_v = od ? std::atoi(od) : -1;
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
@@ -1288,7 +1321,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // processes; the per-CTA LayerNorm prologue path (slice plan) consumes the slots, the row_prep
       // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
       // consumer CTA re-reads t slots), the win is hiding the NVLink exchange across GPUs
-      m->fused_ar = want_far && !m->xs_ln && !m->fuse_ln;
+      m->fused_ar = want_far && !m->fuse_ln;
     }
     if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
       require(nccl_comm != nullptr, "NCCL mode needs a communicator");
@@ -1316,7 +1349,13 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     DSINF_CUDA_CHECK(cudaMemsetAsync(m->pos, 0, sizeof(int), s));
     for (auto& sh : m->shards) build_shard(*m, sh, s);
     DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
-    if (m->fused_ar) map_reduction_peers(*m, s);
+    if (rt->tp_mode == DSINF_TP_IPC && m->t > 1) {
+      require(m->fused_ar, "DSINF_TP_IPC needs the fused all-reduce (slice plan)");
+      m->key_flag = m->alloc_n<unsigned long long>(1);
+      DSINF_CUDA_CHECK(cudaMemset(m->key_flag, 0, sizeof(unsigned long long)));
+    } else if (m->fused_ar) {
+      map_reduction_peers(*m, s);
+    }
     if (m->t == 1 && rt->use_step_kernel) build_step_program(*m);
     if (const char* cl = std::getenv("DSINF_CTA_LOG")) {
       m->cta_log_launch = std::atoi(cl);
@@ -1359,6 +1398,73 @@ static void set_prompt_common(dsinf_model* m, const int32_t* src, int64_t prompt
   }
 }
 
+namespace {
+struct IpcBlob {
+  uint32_t magic, rank, t, pad;
+  cudaIpcMemHandle_t red, flag, keys, key_flag;
+};
+constexpr uint32_t kIpcMagic = 0x64736970u;  // "dsip"
+}  // namespace
+
+int dsinf_model_ipc_handle(dsinf_model* m, void* out, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    require(m != nullptr && len != nullptr, "null argument");
+    require(m->rt.tp_mode == DSINF_TP_IPC && m->t > 1, "dsinf_model_ipc_handle: model is not in DSINF_TP_IPC mode");
+    *len = static_cast<int64_t>(sizeof(IpcBlob));
+    if (out == nullptr) return;
+    require(cap >= static_cast<int64_t>(sizeof(IpcBlob)), "dsinf_model_ipc_handle: buffer too small");
+    const dsinf::Shard& sh = m->shards[0];
+    IpcBlob b{};
+    b.magic = kIpcMagic;
+    b.rank = static_cast<uint32_t>(sh.rank);
+    b.t = static_cast<uint32_t>(m->t);
+    DSINF_CUDA_CHECK(cudaIpcGetMemHandle(&b.red, sh.red));
+    DSINF_CUDA_CHECK(cudaIpcGetMemHandle(&b.flag, sh.red_flag));
+    DSINF_CUDA_CHECK(cudaIpcGetMemHandle(&b.keys, m->am_key));
+    DSINF_CUDA_CHECK(cudaIpcGetMemHandle(&b.key_flag, m->key_flag));
+    std::memcpy(out, &b, sizeof(b));
+  });
+}
+
+int dsinf_model_ipc_attach(dsinf_model* m, const void* all, int64_t len) {
+  return guarded([&] {
+    require(m != nullptr && all != nullptr, "null argument");
+    require(m->rt.tp_mode == DSINF_TP_IPC && m->t > 1, "dsinf_model_ipc_attach: model is not in DSINF_TP_IPC mode");
+    require(!m->ipc_ready, "dsinf_model_ipc_attach: already attached");
+    require(len == static_cast<int64_t>(sizeof(IpcBlob)) * m->t, "dsinf_model_ipc_attach: expected t handle blobs");
+    dsinf::Shard& sh = m->shards[0];
+    const auto* blobs = static_cast<const IpcBlob*>(all);
+    sh.peer_red.assign(m->t, nullptr);
+    sh.peer_flag.assign(m->t, nullptr);
+    m->peer_keys.assign(m->t, nullptr);
+    m->peer_key_flag.assign(m->t, nullptr);
+    for (int q = 0; q < m->t; ++q) {
+      IpcBlob b;
+      std::memcpy(&b, blobs + q, sizeof(b));
+      require(b.magic == kIpcMagic && b.rank == static_cast<uint32_t>(q) && b.t == static_cast<uint32_t>(m->t),
+              "dsinf_model_ipc_attach: blobs must be every rank's dsinf_model_ipc_handle, in rank order");
+      if (q == sh.rank) {
+        sh.peer_red[q] = sh.red;
+        sh.peer_flag[q] = sh.red_flag;
+        m->peer_keys[q] = m->am_key;
+        m->peer_key_flag[q] = m->key_flag;
+        continue;
+      }
+      void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+      const cudaIpcMemHandle_t* hs[4] = {&b.red, &b.flag, &b.keys, &b.key_flag};
+      for (int i = 0; i < 4; ++i) {
+        DSINF_CUDA_CHECK(cudaIpcOpenMemHandle(&p[i], *hs[i], cudaIpcMemLazyEnablePeerAccess));
+        m->ipc_maps.push_back(p[i]);
+      }
+      sh.peer_red[q] = static_cast<float*>(p[0]);
+      sh.peer_flag[q] = static_cast<unsigned long long*>(p[1]);
+      m->peer_keys[q] = static_cast<unsigned long long*>(p[2]);
+      m->peer_key_flag[q] = static_cast<unsigned long long*>(p[3]);
+    }
+    m->ipc_ready = true;
+  });
+}
+
 int dsinf_model_set_prompt(dsinf_model* m, const int32_t* prompt_host, int64_t prompt_len, void* stream) {
   return guarded([&] { set_prompt_common(m, prompt_host, prompt_len, true, static_cast<cudaStream_t>(stream)); });
 }
@@ -1372,6 +1478,8 @@ int dsinf_model_prefill(dsinf_model* m, void* stream) {
     require(m != nullptr, "null model");
     require(m->prompt_len >= 1, "prefill needs a prompt (dsinf_model_set_prompt)");
     require(m->host_pos == 0, "prefill must start at position 0 (call dsinf_model_set_prompt first)");
+    require(m->rt.tp_mode != DSINF_TP_IPC || m->t == 1,
+            "prefill: DSINF_TP_IPC has no all-reduce for the large-batch GEMMs (use decode steps)");
     require(m->d % 32 == 0 && m->d <= 256, "prefill attention needs head_dim % 32 == 0 and <= 256");
     require(m->h % 16 == 0 && (m->Hl * m->d) % 16 == 0 && m->Fl % 16 == 0,
             "prefill needs 16-byte TMA rows (hidden, per-rank head and MLP widths % 16 == 0)");

@@ -168,6 +168,38 @@ __global__ void quant_pack_i8_kernel(const __half* w, int64_t N, int64_t K, cons
   }
 }
 
+// K-group weight quantisation (group = 128 consecutive k of one output row, kI8Group): one warp per
+// (row, group), lane l owns packed word l of the group (4 consecutive k).  Scale s = fp16(max|w| /
+// 127) (fp32 divide, fp16 round to nearest; 1 for an all-zero group), q = clamp(rint(w / s), +-127)
+// with an fp32 divide by the fp16 scale the kernels dequantise with.  Scales [ceil(K/128)][N].
+__global__ void quant_groups_i8_kernel(const __half* w, int64_t N, int64_t K, uint32_t* packed, __half* gscales) {
+  const int64_t G = (K + kI8Group - 1) / kI8Group;
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(warps) + (threadIdx.x >> 5); u < N * G;
+       u += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t n = u / G, g = u - n * G;
+    const int64_t k0 = g * kI8Group + 4 * lane;
+    float v[4];
+    float mx = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] = k0 + e < K ? __half2float(w[n * K + k0 + e]) : 0.f;
+      mx = fmaxf(mx, fabsf(v[e]));
+    }
+    mx = ptx::warp_max(mx);
+    __half sh = __float2half_rn(mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f);
+    if (__half2float(sh) == 0.f) sh = __float2half_rn(1.0f);  // fp16 underflow of a tiny group
+    const float sc = __half2float(sh);
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (k0 + e < K) word |= q8(v[e], sc) << (8 * e);
+    if (k0 < K) packed[(k0 / 4) * N + n] = word;
+    if (lane == 0) gscales[g * N + n] = sh;
+  }
+}
+
 __global__ void quant_act_kernel(const __half* x, int64_t K, int8_t* q, float* scales) {
   const int64_t b = blockIdx.x;
   __shared__ float red[32];
@@ -286,12 +318,30 @@ __global__ void select_kernel(const __grid_constant__ SelectParams p) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int pos = *p.pos;
+  if (p.ipc_t > 1) {  // all-gather of the vocab shards' argmax keys over peer memory
+    for (int b = threadIdx.x; b < p.B; b += blockDim.x) {
+      const unsigned long long k = p.keys[p.ipc_rank * p.B + b];
+      for (int q = 0; q < p.ipc_t; ++q)
+        if (q != p.ipc_rank) p.ipc_keys[q][p.ipc_rank * p.B + b] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < p.ipc_t; ++q)
+        if (q != p.ipc_rank) atomicAdd_system(p.ipc_flag[q], 1ull);
+      const unsigned long long target =
+          (static_cast<unsigned long long>(*p.step_ctr) + 1ull) * static_cast<unsigned long long>(p.ipc_t - 1);
+      while (ptx::ld_acquire_sys(p.ipc_flag[p.ipc_rank]) < target) __nanosleep(32);
+    }
+    __syncthreads();
+  }
   for (int b = threadIdx.x; b < p.B; b += blockDim.x) {
     float bv = 0.f;
     int32_t bx = 0;
     if (p.keys != nullptr) {  // fused LM-head argmax: the max key is the max logit, lowest index
-      unsigned long long k = p.keys[b];
-      for (int s = 1; s < p.shards; ++s) k = max(k, p.keys[s * p.B + b]);
+      const volatile unsigned long long* keys = p.keys;  // peers' slots land over NVLink (IPC mode)
+      unsigned long long k = keys[b];
+      for (int s = 1; s < p.shards; ++s) k = max(k, keys[s * p.B + b]);
       bx = gemm::argmax_key_index(k);
     } else {
       bv = p.vals[b];
@@ -627,6 +677,14 @@ void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, 
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 
+void quantize_weights_i8_groups(const __half* w, int64_t N, int64_t K, int8_t* packed, __half* gscales,
+                                cudaStream_t s) {
+  const int64_t units = N * ((K + kI8Group - 1) / kI8Group);
+  quant_groups_i8_kernel<<<blocks_for(units, 8, 148 * 16), 256, 0, s>>>(w, N, K, reinterpret_cast<uint32_t*>(packed),
+                                                                        gscales);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
 void quantize_act_i8(const __half* x, int64_t B, int64_t K, int8_t* q, float* scales, cudaStream_t s) {
   quant_act_kernel<<<static_cast<unsigned>(B), 256, 0, s>>>(x, K, q, scales);
   DSINF_CUDA_CHECK(cudaGetLastError());
@@ -641,6 +699,8 @@ void argmax(const ArgmaxParams& p, cudaStream_t s, bool pdl) {
 }
 
 void select_token(const SelectParams& p, cudaStream_t s, bool pdl) {
+  if (p.ipc_t > 8) throw ConfigError("select_token: at most 8 IPC ranks");
+  if (p.ipc_t > 1 && (p.step_ctr == nullptr || p.keys == nullptr)) throw ConfigError("select_token: IPC needs keys and step_ctr");
   launch_pdl(select_kernel, dim3(1), dim3(32), 0, s, pdl, p);
 }
 

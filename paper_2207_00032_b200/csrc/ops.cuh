@@ -37,6 +37,11 @@ void init_rowmajor_f16(uint64_t base, float amp, int64_t rows, int64_t cols, __h
 void pack_f16(const void* w, bool src_f32, int64_t N, int64_t K, int pack_M, __half* out, cudaStream_t s);
 // Per-row int8 quantisation of a row-major fp16 matrix into the packed M=4 layout.
 void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, float* scales, cudaStream_t s);
+// K-group scales (kI8Group = 128 consecutive k per row share an fp16 scale; gscales [ceil(K/128)][N]),
+// packed like quantize_weights_i8; the W8A16 GEMM dequantises w = fp16(q * s) per group.
+constexpr int kI8Group = 128;
+void quantize_weights_i8_groups(const __half* w, int64_t N, int64_t K, int8_t* packed, __half* gscales,
+                                cudaStream_t s);
 // Per-token int8 quantisation of activations [B][K] (same formula as the GEMM prologue).
 void quantize_act_i8(const __half* x, int64_t B, int64_t K, int8_t* q, float* scales, cudaStream_t s);
 
@@ -130,6 +135,12 @@ struct SelectParams {
   int* pos;
   int32_t* hist;
   int max_ctx;
+  // DSINF_TP_IPC: this rank's keys ([rank][B] of `keys`) are first stored into every peer's key
+  // array over CUDA-IPC / NVLink and each peer's arrival counter bumped (system scope); the kernel
+  // then waits until its own counter shows the other t - 1 ranks' keys of this step.
+  int ipc_t = 0, ipc_rank = 0;
+  unsigned long long* ipc_keys[8] = {};  // every rank's key array [t][B] (index ipc_rank: ours)
+  unsigned long long* ipc_flag[8] = {};  // every rank's arrival counter
 };
 void select_token(const SelectParams& p, cudaStream_t s, bool pdl);
 

@@ -209,6 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     uint32_t phase = 0;
     if constexpr (kA16) {
       const int g = lane >> 2, t = lane & 3;
+      // K-group scales: stage i of this split is group row_begin / kRowsPerStage + i
+      const __half* gs = p.w_gscale == nullptr ? nullptr
+                                               : p.w_gscale + static_cast<size_t>(row_begin / kRowsPerStage) * p.N +
+                                                     n0 + cw * kWarpCols;
+      const int gs_valid = p.N - (n0 + cw * kWarpCols);
       if constexpr (kXS) {  // x word pair 2 * (4 kk + t) of batch row r in the stage's two boxes
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int st, int, int kk, int bt) {
           const int r = bt * 8 + g;
@@ -216,14 +221,14 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           const int w = 8 * kk + 2 * t, ww = w & 31;
           const uint8_t* xb = ring + st * kSB + kStageBytes + (w >> 5) * kXBoxBytes;
           return *reinterpret_cast<const uint2*>(xb + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) + (ww & 3) * 4);
-        });
+        }, 1, gs, p.N, gs_valid);
       } else {
         const int xrw = p.x_row_words;
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int, int it, int kk, int bt) {
           const int r = bt * 8 + g;
           if (r >= p.B) return make_uint2(0u, 0u);
           return *reinterpret_cast<const uint2*>(sx + r * xrw + it * 2 * kRowsPerStage + 8 * kk + 2 * t);
-        });
+        }, 1, gs, p.N, gs_valid);
       }
     } else if constexpr (kXS) {
       c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane);
@@ -273,8 +278,12 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       }
       float2 ws = make_float2(0.f, 0.f);
       if constexpr (kInt8) {
-        ws.x = __ldg(p.w_scale + n);
-        if (has1) ws.y = __ldg(p.w_scale + n + 1);
+        if (kA16 && p.w_gscale != nullptr) {  // K-group scales were applied in the main loop
+          ws = make_float2(1.f, 1.f);
+        } else {
+          ws.x = __ldg(p.w_scale + n);
+          if (has1) ws.y = __ldg(p.w_scale + n + 1);
+        }
       }
       const uint32_t off = static_cast<uint32_t>((b * kPartLd + c) * 4);
       // the ranks' partials in batches of 4 DSMEM loads in flight, summed in rank order

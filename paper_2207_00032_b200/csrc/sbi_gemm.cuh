@@ -75,6 +75,7 @@ struct Params {
   // or int8 quads); each stage loads one box of 32 words x B rows next to the weight boxes
   alignas(64) CUtensorMap xmap;
   const float* w_scale;  // int8: per-output-row scale [N]
+  const __half* w_gscale;  // W8A16 only, optional: K-group scales [ceil(K/128)][N] (then w_scale unused)
   int N, rows, K, B;
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
   int stages;

@@ -557,6 +557,9 @@ __device__ void fill_x_slice(const Params& p, uint32_t* sx, const Header& hd, in
   }
 }
 
+__device__ __forceinline__ __half2 bits_h2(uint32_t u) { return *reinterpret_cast<const __half2*>(&u); }
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+
 // int8 x4 (one packed weight word: 4 consecutive k) -> two fp16 pairs, exact:
 // bytes (s + 128) under a 0x64 exponent byte are 1024 + s + 128 in fp16; subtract 1152.
 __device__ __forceinline__ void i8x4_to_h2x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
@@ -603,11 +606,27 @@ struct Consumer {
   // W8A16 main loop; xword(it, kk, bt) returns the (b0, b1) x words of batch tile bt.
   // `step` > 1: this warp group consumes every step-th ring slot (the persistent step kernel's
   // interleaved consumer groups; stages % step == 0).
+  // K-group scales (gs != nullptr): one int8 stage is one 128-k group; gs points at the group of
+  // the first stage for this warp's 32 columns ([group][gs_ld] fp16, gs_valid columns readable),
+  // and the weights dequantise to w = fp16(q * s_group) before the MMA (the row scale is then 1).
   template <class XWord>
   __device__ __forceinline__ void run_a16(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
-                                          uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step = 1) {
+                                          uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step = 1,
+                                          const __half* gs = nullptr, int gs_ld = 0, int gs_valid = 0) {
     const uint8_t* wbox = ring + cw * kBoxBytes;
+    __half2 gsc[2][2], gsn[2][2];
+    auto load_gs = [&](int i, __half2 (&o)[2][2]) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 16 * j + 8 * h + g;
+          o[j][h] = __half2half2(c < gs_valid ? gs[static_cast<size_t>(i) * gs_ld + c] : __ushort_as_half(0));
+        }
+    };
+    if (gs != nullptr && n_iters > 0) load_gs(0, gsc);
     for (int it = 0; it < n_iters; ++it) {
+      if (gs != nullptr && it + 1 < n_iters) load_gs(it + 1, gsn);
       ptx::mbar_wait(&hd.full[s], phase);
       const uint8_t* sw = wbox + s * stage_bytes;
 #pragma unroll
@@ -621,6 +640,12 @@ struct Consumer {
           uint32_t a0, a1, a2, a3;
           i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][0][kk & 1]), a0, a2);
           i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][1][kk & 1]), a1, a3);
+          if (gs != nullptr) {
+            a0 = h2_bits(__hmul2(bits_h2(a0), gsc[j][0]));
+            a2 = h2_bits(__hmul2(bits_h2(a2), gsc[j][0]));
+            a1 = h2_bits(__hmul2(bits_h2(a1), gsc[j][1]));
+            a3 = h2_bits(__hmul2(bits_h2(a3), gsc[j][1]));
+          }
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt)
             if constexpr (kA16) ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, bx[bt].x, bx[bt].y);
@@ -631,6 +656,12 @@ struct Consumer {
       if ((s += step) >= stages) {
         s -= stages;
         phase ^= 1;
+      }
+      if (gs != nullptr) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) gsc[j][h] = gsn[j][h];
       }
     }
   }

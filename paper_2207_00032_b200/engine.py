@@ -41,7 +41,7 @@ class DecoderModel:
                  dtype_bytes: int = 2, batch: int = 1, max_ctx: int = 256, tp_size: int = 1, tp_rank: int = 0,
                  tp_mode: int = capi.TP_NONE, nccl_comm: Optional[int] = None, use_cuda_graph: bool = True,
                  use_pdl: bool = True, use_step_kernel: bool = False, seed: int = 20220701, ln_eps: float = 1e-5, rope_base: float = 10000.0,
-                 device: int = 0, int8_act: int = capi.INT8_W8A8):
+                 device: int = 0, int8_act: int = capi.INT8_W8A8, ipc_exchange=None):
         self.cfg = capi.ModelConfig(hidden, layers, heads, vocab, max_seq, dtype_bytes)
         self.rt = capi.RuntimeConfig(batch, tp_size, tp_rank, tp_mode, int(use_cuda_graph), int(use_pdl), max_ctx,
                                      seed, ln_eps, rope_base, device, int(use_step_kernel), int(int8_act))
@@ -50,6 +50,23 @@ class DecoderModel:
         self._h = C.c_void_p()
         capi.check(capi.lib.dsinf_model_create(C.byref(self.cfg), C.byref(self.rt), nccl_comm, C.byref(self._h)))
         self.info = self.get_info()
+        if tp_mode == capi.TP_IPC and tp_size > 1:
+            if ipc_exchange is None:
+                raise capi.ConfigError("TP_IPC needs ipc_exchange(bytes) -> list of every rank's bytes")
+            self.ipc_attach(ipc_exchange(self.ipc_handle()))
+
+    # -- DSINF_TP_IPC: CUDA-IPC handles, exchanged by the caller over any host channel
+    def ipc_handle(self) -> bytes:
+        n = C.c_int64()
+        capi.check(capi.lib.dsinf_model_ipc_handle(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        capi.check(capi.lib.dsinf_model_ipc_handle(self._h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def ipc_attach(self, blobs) -> None:
+        allb = b"".join(blobs)
+        buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
+        capi.check(capi.lib.dsinf_model_ipc_attach(self._h, buf, len(allb)))
 
     # -- lifecycle
     def close(self) -> None:
@@ -155,10 +172,11 @@ class DecoderModel:
 # ---------------------------------------------------------------- device operators on torch tensors
 
 def gemm(w_packed, x, N: int, K: int, *, w_scales=None, x_scales=None, bias=None, out=None, out_dtype=None,
-         gelu: bool = False, ksplit: int = 0, a16: bool = False, stream=None):
+         gelu: bool = False, ksplit: int = 0, a16: bool = False, w_group_scales=None, stream=None):
     """SBI-GeMM: out[B][N] = x[B][K] . W^T over the reference packed layout.
 
-    w_packed: fp16 tensor [ceil(K/2)*2*N] (pack_M = 2) or int8 [ceil(K/4)*4*N] (pack_M = 4)."""
+    w_packed: fp16 tensor [ceil(K/2)*2*N] (pack_M = 2) or int8 [ceil(K/4)*4*N] (pack_M = 4).
+    w_group_scales: fp16 [ceil(K/128)][N] K-group scales (quantize_weights_int8_groups; W8A16)."""
     B = x.shape[0]
     i8w = w_packed.dtype == torch.int8
     if out is None:
@@ -177,7 +195,10 @@ def gemm(w_packed, x, N: int, K: int, *, w_scales=None, x_scales=None, bias=None
     a.out_dtype = capi.DT_F32 if out.dtype == torch.float32 else capi.DT_F16
     a.epilogue = capi.EPI_GELU if gelu else capi.EPI_NONE
     a.ksplit = ksplit
-    a.int8_act = capi.INT8_W8A16 if a16 else capi.INT8_W8A8
+    a.int8_act = capi.INT8_W8A16 if a16 or w_group_scales is not None else capi.INT8_W8A8
+    if w_group_scales is not None:
+        a.w_group_scales = _dptr(w_group_scales)
+        a.group_size = 128
     capi.check(capi.lib.dsinf_gemm(C.byref(a), _stream_ptr(stream)))
     return out
 
@@ -228,6 +249,17 @@ def quantize_weights_int8(w, stream=None):
     s = torch.empty(N, dtype=torch.float32, device=w.device)
     capi.check(capi.lib.dsinf_quantize_weights_int8(_dptr(w.contiguous()), N, K, _dptr(q), _dptr(s),
                                                     _stream_ptr(stream)))
+    return q, s
+
+
+def quantize_weights_int8_groups(w, stream=None):
+    """Row-major fp16 [N][K] -> (packed int8 [ceil(K/4)*4*N], fp16 K-group scales [ceil(K/128)][N])."""
+    N, K = w.shape
+    kp = (K + 3) // 4 * 4
+    q = torch.zeros(N * kp, dtype=torch.int8, device=w.device)
+    s = torch.empty(((K + 127) // 128, N), dtype=torch.float16, device=w.device)
+    capi.check(capi.lib.dsinf_quantize_weights_int8_groups(_dptr(w.contiguous()), N, K, 128, _dptr(q), _dptr(s),
+                                                           _stream_ptr(stream)))
     return q, s
 
 

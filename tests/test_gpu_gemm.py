@@ -163,3 +163,38 @@ def test_int8_w8a16_every_split_agrees(ksplit):
     q_rm, s_rm = O.quant_rows(W.astype(np.float32))
     ref = (x.astype(np.float64) @ q_rm.astype(np.float64).T) * s_rm.astype(np.float64)
     assert np.allclose(out, ref, rtol=2e-3, atol=2e-2)
+
+
+@pytest.mark.parametrize("N,K", [(4096, 4096), (1000, 300), (12288, 4096), (640, 16384)])
+def test_int8_group_quantisation_bit_exact(N, K):
+    """K-group quantisation (128 k per fp16 scale): q and the scales are bit-identical to the oracle,
+    in the pack_M = 4 layout of the row mode (a heavy-tailed matrix, so the groups differ)."""
+    rng = np.random.default_rng(N + K)
+    W = (rng.standard_normal((N, K)) * 0.05 * np.exp(rng.standard_normal((N, K)))).astype(np.float16)
+    dev = torch.device("cuda")
+    wq, gs = E.quantize_weights_int8_groups(torch.from_numpy(W).to(dev))
+    oq, os_ = O.quant_groups(W.astype(np.float32))
+    assert np.array_equal(gs.cpu().numpy().view(np.uint16), os_.view(np.uint16))
+    packed_host = I.pack_weights(oq.astype(np.float64), I.GemmShape(N, K, 1, 1), 4).data
+    assert np.array_equal(wq.cpu().numpy().astype(np.float64), packed_host)
+
+
+@pytest.mark.parametrize("N,K,B,ksplit", [(4096, 4096, 1, 0), (12288, 4096, 1, 0), (4096, 16384, 1, 0),
+                                          (1000, 300, 3, 0), (4096, 4096, 8, 0), (16384, 4096, 16, 0),
+                                          (512, 4096, 2, 1), (512, 4096, 2, 4), (512, 4096, 2, 16)])
+def test_int8_group_w8a16_gemm(N, K, B, ksplit):
+    """W8A16 with K-group scales: y = sum_k fp16(q s_group) x_k, fp32 accumulation -- within
+    2e-3 * sum|w_eff x| + 1e-3 of the oracle's fp64 sum over the same fp16 effective weights, for
+    every split (a split boundary is a group boundary) and both x plans."""
+    rng = np.random.default_rng(N * 7 + K + B)
+    W = (rng.standard_normal((N, K)) * 0.05 * np.exp(rng.standard_normal((N, K)))).astype(np.float16)
+    x = rng.standard_normal((B, K)).astype(np.float16)
+    dev = torch.device("cuda")
+    wq, gs = E.quantize_weights_int8_groups(torch.from_numpy(W).to(dev))
+    out = E.gemm(wq, torch.from_numpy(x).to(dev), N, K, w_group_scales=gs, ksplit=ksplit).cpu().numpy()
+    oq, os_ = O.quant_groups(W.astype(np.float32))
+    ref = O.gemm_a16_groups(oq, os_, x).astype(np.float64)
+    weff = O.dequant_groups(oq, os_).astype(np.float64)
+    bound = np.abs(x.astype(np.float64)) @ np.abs(weff).T
+    err = np.abs(out - ref)
+    assert np.all(err <= 2e-3 * bound + 1e-3), float((err / (bound + 1e-9)).max())

@@ -279,23 +279,28 @@ def test_prefill_tensor_parallel_matches_oracle(dtype_bytes, tp):
 
 @pytest.mark.parametrize("dtype_bytes", [2, 1])
 @pytest.mark.parametrize("tp,batch", [(2, 1), (4, 3), (8, 2)])
-def test_fused_allreduce_tp_matches_oracle(dtype_bytes, tp, batch, monkeypatch):
+@pytest.mark.parametrize("xs", ["0", "1"])
+def test_fused_allreduce_tp_matches_oracle(dtype_bytes, tp, batch, xs, monkeypatch):
     """Tensor parallelism with the fused all-reduce (row-parallel epilogues push their partials into
     every rank's slots and bump a counter; the next LayerNorm prologue waits and sums the slots in
     rank order) against the TP-aware oracle, graph-replayed over several steps."""
     monkeypatch.setenv("DSINF_FUSED_AR", "1")
-    monkeypatch.setenv("DSINF_XS", "0")  # the fused slots are summed by the per-CTA LayerNorm prologues
+    # the fused slots are summed by the per-CTA LayerNorm prologues (slice plan, DSINF_XS=0) or by
+    # the row_prep launches of the x-streaming plan (DSINF_XS=1)
+    monkeypatch.setenv("DSINF_XS", xs)
     run_parity(512, 3, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, tp=tp, step_kernel=False, prompt_len=5, gen=4)
 
 
-def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
-    """Same TP=4 model with the fused all-reduce and with explicit on-device all-reduce launches:
-    identical greedy tokens, logits within fp32 summation-order noise."""
+@pytest.mark.parametrize("xs", ["0", "1"])
+def test_fused_allreduce_equals_explicit_allreduce(monkeypatch, xs):
+    """Same TP=4 model and plan with the fused all-reduce and with explicit on-device all-reduce
+    launches: identical greedy tokens, logits within fp32 summation-order noise, and exactly the
+    all-reduce launches (2 per layer) fewer."""
     rng = np.random.default_rng(5)
     prompt = rng.integers(0, 1000, (2, 6)).astype(np.int32)
     outs, launches = [], []
+    monkeypatch.setenv("DSINF_XS", xs)
     for fused in ("1", "0"):
-        # no DSINF_XS here: the fused request itself selects the slice plan it needs
         monkeypatch.setenv("DSINF_FUSED_AR", fused)
         m = DecoderModel(512, 2, 8, 1000, batch=2, max_ctx=24, tp_size=4, tp_mode=capi.TP_LOCAL, seed=SEED)
         m.set_prompt(prompt)
@@ -306,7 +311,7 @@ def test_fused_allreduce_equals_explicit_allreduce(monkeypatch):
         launches.append(info.kernels_per_step)
         assert info.fused_allreduce == (1 if fused == "1" else 0)
         m.close()
-    assert launches[0] < launches[1], launches  # the fused path has no all-reduce / row_prep launches
+    assert launches[1] - launches[0] == 2 * 2, launches  # 2 layers x (attn-out, MLP-down) all-reduces
     (la, ha), (lb, hb) = outs
     assert np.array_equal(ha, hb)
     assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(lb).max()) + 1e-4
