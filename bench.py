@@ -391,7 +391,8 @@ def tp_slice_sweep(E, capi, torch, args, stream, peak_gbs):
 
 def kernel_roofline(E, torch, preset, tp, batch, dtype, peak_gbs, stream):
     """Times each SBI-GeMM shape of one layer (+ LM head) alone with CUDA events on the launching
-    stream; 4 rotating weight copies (> L2) per shape.  Returns the per-kernel list and the byte-weighted
+    stream (20 drop-in dsinf_gemm calls captured in a CUDA graph and replayed); 4 rotating weight
+    copies (> L2) per shape.  Returns the per-kernel list and the byte-weighted
     aggregate for the dominant kernel family (sbi_gemm_kernel)."""
     layer, lm = gemm_shapes(preset, tp)
     dev = torch.device("cuda")
@@ -412,14 +413,22 @@ def kernel_roofline(E, torch, preset, tp, batch, dtype, peak_gbs, stream):
         for i in range(3):
             wq, ws = copies[i % 4]
             E.gemm(wq, x, N, K, w_scales=ws, out=out, stream=stream)
+        # the n calls captured once into a CUDA graph and replayed: device time of the launches,
+        # not the host's ctypes / launch overhead between back-to-back small calls
         n = 20
-        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        graph = torch.cuda.CUDAGraph()
         torch.cuda.synchronize()
-        st.record(stream)
-        for i in range(n):
-            wq, ws = copies[i % 4]
-            E.gemm(wq, x, N, K, w_scales=ws, out=out, stream=stream)
-        en.record(stream)
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(n):
+                wq, ws = copies[i % 4]
+                E.gemm(wq, x, N, K, w_scales=ws, out=out, stream=stream)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):  # replay() launches on the current stream
+            graph.replay()
+            torch.cuda.synchronize()
+            st.record(stream)
+            graph.replay()
+            en.record(stream)
         en.synchronize()
         ms = st.elapsed_time(en) / n
         algo = gemm_algo_bytes(N, K, batch, int8)

@@ -2,6 +2,8 @@
 // attention, and the exec_reference drop-in (gemm.hpp:147-202) executed on the GPU.
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <vector>
 
@@ -16,6 +18,37 @@ using namespace dsinf;
 namespace {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Per-(device, stream) scratch for the once-per-launch activation quantisation: calls on one stream
+// are ordered, so its buffer is reused without synchronisation (grown, after a stream sync, when a
+// larger call arrives).  Under graph capture a stream-ordered allocation is used instead.
+void* stream_scratch(cudaStream_t s, size_t bytes, bool* async_alloc) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DSINF_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) {
+    void* p = nullptr;
+    DSINF_CUDA_CHECK(cudaMallocAsync(&p, bytes, s));
+    *async_alloc = true;
+    return p;
+  }
+  *async_alloc = false;
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> cache;
+  int dev = 0;
+  DSINF_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = cache[{dev, s}];
+  if (e.second < bytes) {
+    if (e.first != nullptr) {
+      DSINF_CUDA_CHECK(cudaStreamSynchronize(s));
+      DSINF_CUDA_CHECK(cudaFree(e.first));
+    }
+    e.first = nullptr;
+    DSINF_CUDA_CHECK(cudaMalloc(&e.first, bytes));
+    e.second = bytes;
+  }
+  return e.first;
+}
 
 void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
   require(a.w_packed && a.x && a.out, "null pointer argument");
@@ -48,7 +81,8 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
                           (reinterpret_cast<uintptr_t>(a.x) & 7) == 0;
   void* xq_scratch = nullptr;
   const int64_t bmax = std::min<int64_t>(gemm::kMaxB, a.B);
-  if (quant_once) DSINF_CUDA_CHECK(cudaMallocAsync(&xq_scratch, static_cast<size_t>(bmax) * (K + 4) + 256, s));
+  bool scratch_async = false;
+  if (quant_once) xq_scratch = stream_scratch(s, static_cast<size_t>(bmax) * (K + 4) + 256, &scratch_async);
   for (int64_t b0 = 0; b0 < a.B; b0 += gemm::kMaxB) {
     const int nb = static_cast<int>(std::min<int64_t>(gemm::kMaxB, a.B - b0));
     int xes = a.x_dtype == DSINF_DT_I8 ? 1 : 2;
@@ -65,6 +99,8 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
       pp.out_scale = sc;
       pp.B = nb;
       pp.K = K;
+      // standalone: no GEMM to overlap, so spread long rows over the widest cluster (>= 512 k per CTA)
+      pp.split = K >= 8 * 512 ? 8 : (K >= 4 * 512 ? 4 : (K >= 2 * 512 ? 2 : 1));
       ops::row_prep(pp, s, false);
       xb = xq;
       xsc = sc;
@@ -98,7 +134,7 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
                                         : (a.epilogue == DSINF_EPI_GELU ? gemm::EPI_GELU_F16 : gemm::EPI_F16);
     gemm::launch(p, plan, i8w, s, false);
   }
-  if (xq_scratch) DSINF_CUDA_CHECK(cudaFreeAsync(xq_scratch, s));
+  if (xq_scratch && scratch_async) DSINF_CUDA_CHECK(cudaFreeAsync(xq_scratch, s));
 }
 
 struct DeviceBuffer {

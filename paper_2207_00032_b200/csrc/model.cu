@@ -97,6 +97,11 @@ struct Shard {
   gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
   PrefillBufs pf;
   bool rm_ready = false;
+  // prefill weights when the row-major copies of every layer do not fit (or DSINF_PREFILL_REPACK=1):
+  // ONE layer's four row-major tensors, re-filled from the packed decode weights before each
+  // layer's GEMMs (packed_to_rowmajor), so the model keeps a single resident weight copy
+  bool rm_per_layer = false;
+  void* rm_scratch[4] = {nullptr, nullptr, nullptr, nullptr};
   // fused tensor-parallel all-reduce: [2 points][t source ranks][B*h] partial slots written by every
   // rank's attn-out (point 0) / MLP-down (point 1) epilogue, and their arrival counters [2][L]
   float* red = nullptr;
@@ -353,6 +358,32 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
 void build_rowmajor(Model& m, Shard& sh, cudaStream_t s) {
   const int r = sh.rank;
   const int64_t h = m.h;
+  {
+    const int64_t eb = m.int8 ? 1 : 2;
+    const int64_t layer_bytes = (3 * m.Hl * m.d * h + h * m.Hl * m.d + 2 * m.Fl * h) * eb;
+    size_t free_b = 0, total_b = 0;
+    DSINF_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const char* rp = std::getenv("DSINF_PREFILL_REPACK");
+    const int64_t shards_left = static_cast<int64_t>(m.shards.size());  // copies still to build (worst case)
+    const bool fits = static_cast<double>(layer_bytes) * m.L * shards_left + (4LL << 30) < static_cast<double>(free_b);
+    sh.rm_per_layer = rp ? std::atoi(rp) != 0 : !fits;
+    if (sh.rm_per_layer) {
+      const int64_t qkv = 3 * m.Hl * m.d * h, o = h * m.Hl * m.d, f = m.Fl * h;
+      sh.rm_scratch[0] = m.alloc(static_cast<size_t>(qkv * eb));
+      sh.rm_scratch[1] = m.alloc(static_cast<size_t>(o * eb));
+      sh.rm_scratch[2] = m.alloc(static_cast<size_t>(f * eb));
+      sh.rm_scratch[3] = m.alloc(static_cast<size_t>(f * eb));
+      for (int l = 0; l < m.L; ++l) {
+        LayerW& w = sh.layers[l];
+        w.rqkv = sh.rm_scratch[0];
+        w.ro = sh.rm_scratch[1];
+        w.rup = sh.rm_scratch[2];
+        w.rdown = sh.rm_scratch[3];
+      }
+      sh.rm_ready = true;
+      return;
+    }
+  }
   for (int l = 0; l < m.L; ++l) {
     LayerW& w = sh.layers[l];
     auto make = [&](int tensor, const float* scales) -> void* {
@@ -944,6 +975,16 @@ struct Enqueuer {
     };
     const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
     for (int l = 0; l < m.L; ++l) {
+      for (Shard& sh : m.shards) {
+        if (!sh.rm_per_layer) continue;
+        const LayerW& w = sh.layers[l];
+        const int64_t pm = m.int8 ? 4 : 2, h64 = m.h;
+        ops::packed_to_rowmajor(w.wqkv, h64 / pm, 3 * m.Hl * m.d, static_cast<uint32_t*>(w.rqkv), s);
+        ops::packed_to_rowmajor(w.wo, m.Hl * m.d / pm, h64, static_cast<uint32_t*>(w.ro), s);
+        ops::packed_to_rowmajor(w.wup, h64 / pm, m.Fl, static_cast<uint32_t*>(w.rup), s);
+        ops::packed_to_rowmajor(w.wdown, m.Fl / pm, h64, static_cast<uint32_t*>(w.rdown), s);
+        launches += 4;
+      }
       for (Shard& sh : m.shards) {
         const LayerW& w = sh.layers[l];
         PrefillBufs& pf = sh.pf;

@@ -618,6 +618,8 @@ void row_prep(const PrepParams& p_in, cudaStream_t s, bool pdl) {
   int S = 1;
   if (forced > 0) {
     S = forced;
+  } else if (p.split > 0) {
+    S = p.split;
   } else {
     S = 8;
     while (S > 2 && p.B * S > 16) S >>= 1;
@@ -674,6 +676,28 @@ void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, 
   DSINF_CUDA_CHECK(cudaGetLastError());
   const int64_t total = (K + 3) / 4 * N;
   quant_pack_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(w, N, K, scales, reinterpret_cast<uint32_t*>(packed));
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void word_transpose_kernel(const uint32_t* __restrict__ in, int64_t rows, int64_t N,
+                                      uint32_t* __restrict__ out) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && n < N) ? __ldcs(in + r * N + n) : 0u;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t n = n0 + i, r = r0 + threadIdx.x;
+    if (n < N && r < rows) out[n * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s) {
+  if (rows >= (1LL << 31) / 32 * 32 || N >= (1LL << 31) / 32 * 32) throw ConfigError("packed_to_rowmajor: too large");
+  const dim3 grid(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  word_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(packed, rows, N, out);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 

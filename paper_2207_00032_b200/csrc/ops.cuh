@@ -27,6 +27,10 @@ void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStre
 // Row-major [N_local][K_local] copy of the same tensor for the tensor-core path: fp16, or int8
 // quantised with the given (packed-layout) row scales.
 void init_rowmajor_map_f16(const ShardMap& m, __half* out, cudaStream_t s);
+// Packed decode weights -> the row-major [N][K] operand of the tensor-core prefill: both layouts
+// are 32-bit words (pack_M consecutive k of one output row), so this is the word transpose
+// [rows][N] -> [N][rows] (rows = K / pack_M, K % pack_M == 0), smem-tiled, coalesced both ways.
+void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s);
 void init_rowmajor_map_i8(const ShardMap& m, const float* scales, int8_t* out, cudaStream_t s);
 // 1-D tensor (bias / LN) of length n_local: value = offset + unit(flat = row(n)) * amp.
 void init_vector_f16(const ShardMap& m, float offset, __half* out, cudaStream_t s);
@@ -96,6 +100,7 @@ struct PrepParams {
   float* out_scale;            // int8: [B]
   int B, K;
   unsigned long long* trace;
+  int split;  // CTAs (cluster) per row: 0 = the measured in-model rule, else 1, 2, 4 or 8
 };
 void row_prep(const PrepParams& p, cudaStream_t s, bool pdl);
 

@@ -384,3 +384,27 @@ def test_generate_fills_max_ctx_and_rejects_beyond():
     with pytest.raises(capi.InfeasibleError):
         m.generate(prompt, 9)
     m.close()
+
+
+@pytest.mark.parametrize("dtype_bytes", [2, 1])
+def test_prefill_single_weight_copy_identical(dtype_bytes, monkeypatch):
+    """DSINF_PREFILL_REPACK=1 (chosen automatically when the row-major prefill copies of every layer
+    do not fit): the tensor-core prefill re-fills ONE layer's row-major operands from the packed
+    decode weights before each layer, so the model holds a single resident weight copy.  Same GEMM
+    operands, so the prefill logits and the following decode are bit-identical to the copy mode."""
+    rng = np.random.default_rng(17)
+    prompt = rng.integers(0, 1000, (2, 40)).astype(np.int32)
+    outs = []
+    for rp in ("0", "1"):
+        monkeypatch.setenv("DSINF_PREFILL_REPACK", rp)
+        m = DecoderModel(512, 2, 8, 1000, dtype_bytes=dtype_bytes, batch=2, max_ctx=48, seed=SEED)
+        m.set_prompt(prompt)
+        m.prefill()
+        torch.cuda.synchronize()
+        lg = m.full_logits()
+        m.step(3)
+        torch.cuda.synchronize()
+        outs.append((lg, m.full_logits(), m.read_tokens()[1]))
+        m.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
