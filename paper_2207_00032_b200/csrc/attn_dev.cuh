@@ -36,9 +36,11 @@ __host__ __device__ constexpr size_t attn_scratch_floats(int d) {
 // Computes the partial of positions [j0, j1) into co[0..d) (output, unnormalised) and
 // cst[0] = max, cst[1] = sum.  Called by kAttnThreads threads (tid in [0, 128)); `bar` is the
 // barrier among them.  Loads use ld.global.cg: q / K / V may have been written by other CTAs.
+// kv_pre (optional): K rows then V rows of positions [j0, j_pre) already in shared memory
+// ([rows_cap][d] halves each; staged before the kernel's dependency wait), read instead of global.
 template <int TPP, class Bar>
 __device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1, int tid, float* scratch,
-                           Bar bar) {
+                           Bar bar, const __half* kv_pre = nullptr, int j_pre = 0, int rows_cap = 0) {
   constexpr int PPR = kAttnThreads / TPP;
   const int d = p.d;
   float* so = scratch;       // [PPR][d]
@@ -76,8 +78,14 @@ __device__ void attn_chunk(const AttnParams& p, int b, int head, int j0, int j1,
     for (int u = 0; u < kAttnUnroll; ++u) {
       const int j = j0 + (r0 + u) * PPR + slot;
       if (r0 < rounds && j < j1 && has_dims) {
-        kk[u] = __ldcg(reinterpret_cast<const uint4*>(kb + static_cast<size_t>(j) * d));
-        vv[u] = __ldcg(reinterpret_cast<const uint4*>(vb + static_cast<size_t>(j) * d));
+        if (j < j_pre) {
+          const __half* ks = kv_pre + static_cast<size_t>(j - j0) * d + dim0;
+          kk[u] = *reinterpret_cast<const uint4*>(ks);
+          vv[u] = *reinterpret_cast<const uint4*>(ks + static_cast<size_t>(rows_cap) * d);
+        } else {
+          kk[u] = __ldcg(reinterpret_cast<const uint4*>(kb + static_cast<size_t>(j) * d));
+          vv[u] = __ldcg(reinterpret_cast<const uint4*>(vb + static_cast<size_t>(j) * d));
+        }
       } else {
         kk[u] = make_uint4(0, 0, 0, 0);
         vv[u] = make_uint4(0, 0, 0, 0);

@@ -60,6 +60,10 @@ struct AttnParams {
   float scale;
   unsigned* amax_out;         // row max |out| stripes for the int8 attn-out prologue, or null
   unsigned long long* trace;  // launch timeline slot or null
+  // > 0: K/V rows of the earlier positions of a CTA's chunk (at most kv_rows_cap) are copied into
+  // shared memory BEFORE the dependency wait (they were written by earlier steps); only q and the
+  // new position's K/V row are read after it.  Set by ops::attention.
+  int kv_rows_cap;
 };
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
