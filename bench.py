@@ -313,6 +313,7 @@ def workload_config(args, preset, world):
            "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
     if args.dtype == "int8":
         cfg["int8_act"] = auto_act(args.batch, world) if args.int8_act == "auto" else args.int8_act
+        cfg["int8_scales"] = "K-group 128 (fp16)" if args.int8_group else "per output row (fp32)"
     return cfg
 
 
@@ -528,7 +529,8 @@ def run_ours(args, preset, rank, world, local_rank):
                            batch=args.batch, max_ctx=max_ctx, tp_size=world, tp_rank=rank,
                            tp_mode=capi.TP_NCCL if world > 1 else capi.TP_NONE, nccl_comm=comm,
                            use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank,
-                           int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16, "auto": capi.INT8_AUTO}[args.int8_act])
+                           int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16, "auto": capi.INT8_AUTO}[args.int8_act],
+                           int8_group=args.int8_group if args.dtype == "int8" else 0)
     rng = np.random.default_rng(SEED)
     prompt = rng.integers(0, preset.vocab, (args.batch, args.prompt)).astype(np.int32)
 
@@ -540,7 +542,7 @@ def run_ours(args, preset, rank, world, local_rank):
 
     # ---- prompt prefill: the large-batch (tcgen05) path at TP = 1, else the prompt tokens through
     # the decode step graph
-    use_tc_prefill = world == 1 and not args.token_prefill
+    use_tc_prefill = world == 1 and not args.token_prefill and not (args.dtype == "int8" and args.int8_group)
 
     def do_prefill():
         model.set_prompt(prompt, stream=stream)
@@ -743,6 +745,9 @@ def main():
     ap.add_argument("--int8-act", choices=["w8a8", "w8a16", "auto"], default="auto",
                     help="int8 decode GEMMs: per-token int8 activations (int32 accumulate), weight-only, or the "
                          "measured per-batch choice (W8A16 for batch <= 8, W8A8 above)")
+    ap.add_argument("--int8-group", type=int, choices=[0, 128], default=0,
+                    help="int8: 128 = K-group weight scales (weight-only GEMMs, per-group dequant; the prompt goes "
+                         "through the decode step)")
     ap.add_argument("--no-tp-slices", action="store_true", help="skip the per-rank TP slice measurements")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for cpu_baseline")

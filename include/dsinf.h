@@ -241,6 +241,8 @@ typedef struct dsinf_runtime_config {
   int32_t use_step_kernel; /* TP = 1: run each decode step as ONE persistent kernel */
   int32_t int8_act;     /* dtype_bytes 1: DSINF_INT8_W8A8 (default), DSINF_INT8_W8A16 or DSINF_INT8_AUTO
                            (decode GEMMs; the tensor-core prefill stays W8A8) */
+  int32_t int8_group;   /* dtype_bytes 1: 0 = per-output-row scales; 128 = K-group scales (fp16 per
+                           128 k of a row; decode GEMMs W8A16 with per-group dequant; no prefill) */
 } dsinf_runtime_config;
 
 typedef struct dsinf_model dsinf_model;

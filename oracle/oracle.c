@@ -281,6 +281,7 @@ void or_gemm_i8(const int8_t* wq, const float* ws, const int8_t* xq, const float
 typedef struct {
   float *wqkv, *wo, *wup, *wdown, *wlm;       /* fp16 path: row-major local shards */
   int8_t *qqkv, *qo, *qup, *qdown;             /* int8 path */
+  float *gqkv, *go, *gup, *gdown;              /* int8 K-group scales [Kl/128][Nl] (fp16 values), or NULL */
   float *sqkv, *so, *sup, *sdown;              /* int8 row scales (global-row) */
 } or_rank_w;
 
@@ -346,6 +347,30 @@ static void gen_shard_i8(int8_t* q, float* scales, int64_t Nl, int64_t Kl, int64
     const float s = q_scale(mx);
     scales[n] = s;
     for (int64_t k = 0; k < Kl; ++k) q[n * Kl + k] = q_one(gval(base, gr, col_off + k, Kg), s);
+  }
+}
+
+/* K-group variant (or_config.int8_group = 128; ops.cu init_packed_i8_groups_kernel): per (global row,
+ * 128-k group of the global k index) s = fp16(max|w| / 127), q = clamp(rint(w / s)); the local
+ * k range starts at col_off (a multiple of 128).  gs [Kl/128][Nl] holds the fp16 scales as floats. */
+static void gen_shard_i8_groups(int8_t* q, float* gs, int64_t Nl, int64_t Kl, int64_t Kg, int64_t sec_l,
+                                int64_t sec_g, int64_t row_off, int64_t col_off, uint64_t base) {
+  const int64_t G = Kl / 128;
+#pragma omp parallel for schedule(static)
+  for (int64_t n = 0; n < Nl; ++n) {
+    const int64_t gr = (n / sec_l) * sec_g + row_off + n % sec_l;
+    for (int64_t g = 0; g < G; ++g) {
+      float mx = 0.0f;
+      for (int64_t k = g * 128; k < g * 128 + 128; ++k) {
+        const float a = fabsf(gval(base, gr, col_off + k, Kg));
+        if (a > mx) mx = a;
+      }
+      uint16_t sh = or_f32_to_f16(q_scale(mx));
+      if (or_f16_to_f32(sh) == 0.0f) sh = or_f32_to_f16(1.0f);
+      const float sc = or_f16_to_f32(sh);
+      gs[g * Nl + n] = sc;
+      for (int64_t k = g * 128; k < g * 128 + 128; ++k) q[n * Kl + k] = q_one(gval(base, gr, col_off + k, Kg), sc);
+    }
   }
 }
 
@@ -420,6 +445,16 @@ or_model* or_model_create(const or_config* cfg) {
         w->qdown = (int8_t*)malloc((size_t)(h * Fl));
         w->sdown = falloc(h);
         gen_shard_i8(w->qdown, w->sdown, h, Fl, m->F, h, h, 0, r * Fl, bd);
+        if (m->c.int8_group == 128) {  /* K-group weights replace the row-scaled ones */
+          w->gqkv = falloc(3 * Hl * d * (h / 128));
+          gen_shard_i8_groups(w->qqkv, w->gqkv, 3 * Hl * d, h, h, Hl * d, h, r * Hl * d, 0, bq);
+          w->go = falloc(h * (Hl * d / 128));
+          gen_shard_i8_groups(w->qo, w->go, h, Hl * d, h, h, h, 0, r * Hl * d, bo);
+          w->gup = falloc(Fl * (h / 128));
+          gen_shard_i8_groups(w->qup, w->gup, Fl, h, h, Fl, m->F, r * Fl, 0, bu);
+          w->gdown = falloc(h * (Fl / 128));
+          gen_shard_i8_groups(w->qdown, w->gdown, h, Fl, m->F, h, h, 0, r * Fl, bd);
+        }
       }
     }
     ly->bqkv = falloc(3 * h);
@@ -477,6 +512,7 @@ void or_model_destroy(or_model* m) {
       free(w->wqkv); free(w->wo); free(w->wup); free(w->wdown);
       free(w->qqkv); free(w->qo); free(w->qup); free(w->qdown);
       free(w->sqkv); free(w->so); free(w->sup); free(w->sdown);
+      free(w->gqkv); free(w->go); free(w->gup); free(w->gdown);
     }
     free(ly->ranks);
     free(ly->bqkv); free(ly->bo); free(ly->bup); free(ly->bdown);
@@ -535,7 +571,17 @@ static int act_of(int int8_act, int g) { return (int8_act & 0x100) ? (int8_act >
 /* int8 path GEMM on fp16 activations: per-token quantisation, exact int32, fp32 dequant
  * (int8_act 1: weight-only, fp16 activations) */
 static void gemm8(int int8_act, const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B,
-                  float* y) {
+                  float* y, const float* gs) {
+  if (gs != NULL) { /* K-group weight-only: y = sum_k fp16(q s_group) x_k (fp64 sum; the GPU: fp32) */
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n)
+      for (int64_t b = 0; b < B; ++b) {
+        double a = 0.0;
+        for (int64_t k = 0; k < K; ++k) a += (double)f16r((float)W[n * K + k] * gs[(k / 128) * N + n]) * (double)x16[b * K + k];
+        y[b * N + n] = (float)a;
+      }
+    return;
+  }
   if (int8_act == 1) {
     gemm8_a16(W, ws, N, K, x16, B, y);
     return;
@@ -588,7 +634,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
       const int64_t Nq = 3 * Hl * d;
       /* K1: QKV + bias + RoPE + KV append */
       if (!i8) gemm16(w->wqkv, Nq, h, sm, xln, B, yd);
-      else gemm8(act_of(m->c.int8_act, 0), w->qqkv, w->sqkv, Nq, h, xln, B, yf);
+      else gemm8(act_of(m->c.int8_act, 0), w->qqkv, w->sqkv, Nq, h, xln, B, yf, w->gqkv);
       for (int64_t b = 0; b < B; ++b)
         for (int64_t n = 0; n < Nq; n += 2) {
           const int64_t sec = n / (Hl * d), rem = n % (Hl * d), hh = rem / d, i = rem % d;
@@ -666,7 +712,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wo, h, Hl * d, sm, xa, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(act_of(m->c.int8_act, 1), w->qo, w->so, h, Hl * d, xa, B, yf);
+        gemm8(act_of(m->c.int8_act, 1), w->qo, w->so, h, Hl * d, xa, B, yf, w->go);
       }
       for (int64_t i = 0; i < B * h; ++i) dsum[i] = rk == 0 ? yf[i] : dsum[i] + yf[i];
       free(xa);
@@ -688,7 +734,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
           for (int64_t n = 0; n < Fl; ++n)
             u16[b * Fl + n] = f16r((float)gelu_tanh(yd[b * Fl + n] + ly->bup[rk * Fl + n]));
       } else {
-        gemm8(act_of(m->c.int8_act, 2), w->qup, w->sup, Fl, h, xln, B, yf);
+        gemm8(act_of(m->c.int8_act, 2), w->qup, w->sup, Fl, h, xln, B, yf, w->gup);
         for (int64_t b = 0; b < B; ++b)
           for (int64_t n = 0; n < Fl; ++n) {
             const float y = yf[b * Fl + n] + ly->bup[rk * Fl + n];
@@ -700,7 +746,7 @@ int or_model_step(or_model* m, const int32_t* tokens, int64_t pos, float* logits
         gemm16(w->wdown, h, Fl, sm, u16, B, yd);
         for (int64_t i = 0; i < B * h; ++i) yf[i] = (float)yd[i];
       } else {
-        gemm8(act_of(m->c.int8_act, 3), w->qdown, w->sdown, h, Fl, u16, B, yf);
+        gemm8(act_of(m->c.int8_act, 3), w->qdown, w->sdown, h, Fl, u16, B, yf, w->gdown);
       }
       for (int64_t i = 0; i < B * h; ++i) dm[i] = rk == 0 ? yf[i] : dm[i] + yf[i];
     }

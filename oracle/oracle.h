@@ -81,6 +81,7 @@ typedef struct or_config {
   float ln_eps, rope_base;
   int32_t int8_act;    /* int8 weights: 0 = W8A8 (per-token int8 x, int32 accumulate), 1 = W8A16 (fp16 x),
                           0x100 | mask = per GEMM (bit 0 QKV, 1 attn-out, 2 MLP-up, 3 MLP-down set = W8A16) */
+  int32_t int8_group;  /* 0 = per-row weight scales; 128 = K-group fp16 scales (weight-only GEMMs) */
 } or_config;
 
 typedef struct or_model or_model;

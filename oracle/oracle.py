@@ -28,7 +28,7 @@ class Config(C.Structure):
     _fields_ = [("hidden", C.c_int64), ("layers", C.c_int64), ("heads", C.c_int64), ("vocab", C.c_int64),
                 ("max_ctx", C.c_int64), ("dtype_bytes", C.c_int32), ("tp", C.c_int32), ("batch", C.c_int32),
                 ("sm_count", C.c_int32), ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float),
-                ("int8_act", C.c_int32)]
+                ("int8_act", C.c_int32), ("int8_group", C.c_int32)]
 
 
 def _load(path):
@@ -219,9 +219,9 @@ class OracleModel:
     """CPU decoder with the GPU path's storage points (fp16 / fp32) and exec_reference GEMM order."""
 
     def __init__(self, hidden, layers, heads, vocab=50257, *, dtype_bytes=2, tp=1, batch=1, max_ctx=256,
-                 seed=20220701, ln_eps=1e-5, rope_base=10000.0, sm_count=148, int8_act=0):
+                 seed=20220701, ln_eps=1e-5, rope_base=10000.0, sm_count=148, int8_act=0, int8_group=0):
         self.cfg = Config(hidden, layers, heads, vocab, max_ctx, dtype_bytes, tp, batch, sm_count, seed, ln_eps,
-                          rope_base, int8_act)
+                          rope_base, int8_act, int8_group)
         self.batch, self.vocab, self.hidden = batch, vocab, hidden
         self._h = oracle_lib().or_model_create(C.byref(self.cfg))
 

@@ -117,7 +117,7 @@ class RuntimeConfig(C.Structure):
     _fields_ = [("batch", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32), ("tp_mode", C.c_int32),
                 ("use_cuda_graph", C.c_int32), ("use_pdl", C.c_int32), ("max_ctx", C.c_int64),
                 ("seed", C.c_uint64), ("ln_eps", C.c_float), ("rope_base", C.c_float), ("device", C.c_int32),
-                ("use_step_kernel", C.c_int32), ("int8_act", C.c_int32)]
+                ("use_step_kernel", C.c_int32), ("int8_act", C.c_int32), ("int8_group", C.c_int32)]
 
 
 class ModelInfo(C.Structure):

@@ -56,6 +56,8 @@ struct LayerW {
   uint32_t* wdown = nullptr;
   float* sdown = nullptr;
   __half* bdown = nullptr;
+  // int8 K-group scales (dsinf_runtime_config.int8_group = 128): fp16 [K_local/128][N_local]
+  __half *gqkv = nullptr, *go = nullptr, *gup = nullptr, *gdown = nullptr;
   // row-major [N][K] copies for the tensor-core prefill (fp16, or int8 with the scales above);
   // generated on the first dsinf_model_prefill
   void *rqkv = nullptr, *ro = nullptr, *rup = nullptr, *rdown = nullptr;
@@ -254,12 +256,18 @@ ops::ShardMap tensor_map(int64_t h, int64_t H, int64_t V, int t, int r, uint64_t
 }
 
 // Allocates and generates one GEMM weight in the packed layout (fp16 M=2 or int8 M=4).
-uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaStream_t s) {
+uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaStream_t s, __half** gscales = nullptr) {
   const int M = m.int8 ? 4 : 2;
   const int64_t words = (map.K_local + M - 1) / M * map.N_local;
   uint32_t* w = m.alloc_n<uint32_t>(words);
   m.weight_bytes += words * 4;
-  if (m.int8) {
+  if (m.int8 && m.rt.int8_group != 0) {  // K-group scales: the W8A16 GEMMs dequantise per group
+    const int64_t ng = map.K_local / ops::kI8Group * map.N_local;
+    *gscales = m.alloc_n<__half>(ng);
+    m.weight_bytes += ng * 2;
+    *scales = nullptr;
+    ops::init_packed_i8_groups(map, w, *gscales, s);
+  } else if (m.int8) {
     *scales = m.alloc_n<float>(map.N_local);
     m.weight_bytes += map.N_local * 4;
     ops::init_packed_i8(map, w, *scales, s);
@@ -289,13 +297,13 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
       tensor_amp(tensor, &off);
       return make_vec(m, map(tensor), off, s);
     };
-    w.wqkv = make_weight(m, map(DSINF_T_QKV), &w.sqkv, s);
+    w.wqkv = make_weight(m, map(DSINF_T_QKV), &w.sqkv, s, &w.gqkv);
     w.bqkv = vec(DSINF_T_QKV_BIAS);
-    w.wo = make_weight(m, map(DSINF_T_O), &w.so, s);
+    w.wo = make_weight(m, map(DSINF_T_O), &w.so, s, &w.go);
     w.bo = vec(DSINF_T_O_BIAS);
-    w.wup = make_weight(m, map(DSINF_T_UP), &w.sup, s);
+    w.wup = make_weight(m, map(DSINF_T_UP), &w.sup, s, &w.gup);
     w.bup = vec(DSINF_T_UP_BIAS);
-    w.wdown = make_weight(m, map(DSINF_T_DOWN), &w.sdown, s);
+    w.wdown = make_weight(m, map(DSINF_T_DOWN), &w.sdown, s, &w.gdown);
     w.bdown = vec(DSINF_T_DOWN_BIAS);
     w.ln1g = vec(DSINF_T_LN1_G);
     w.ln1b = vec(DSINF_T_LN1_B);
@@ -423,11 +431,13 @@ void ensure_prefill_bufs(Model& m, Shard& sh, int64_t M) {
   pf.cap = M;
 }
 
-gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w) {
+gemm::Params base_params(const Model& m, const uint32_t* w, const float* ws, int N, int K, bool int8_w,
+                         const __half* gs = nullptr) {
   gemm::Params p{};
   p.rows = int8_w ? (K + 3) / 4 : (K + 1) / 2;
   gemm::make_weight_map(&p.tmap, w, N, p.rows);
   p.w_scale = ws;
+  p.w_gscale = int8_w ? gs : nullptr;
   p.N = N;
   p.K = K;
   p.B = m.B;
@@ -687,7 +697,7 @@ struct Enqueuer {
   void k1_qkv(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     const int N = static_cast<int>(3 * m.Hl * m.d);
-    gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8);
+    gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8, w.gqkv);
     if (m.xs_ln) {
       RedIn red;  // fused all-reduce: row_prep sums the ranks' MLP-down slots of layer l - 1
       const bool use_slots = m.fused_ar && l > 0;
@@ -744,7 +754,7 @@ struct Enqueuer {
 
   void k3_attn_out(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
-    gemm::Params p = base_params(m, w.wo, w.so, static_cast<int>(m.h), static_cast<int>(m.Hl * m.d), m.int8);
+    gemm::Params p = base_params(m, w.wo, w.so, static_cast<int>(m.h), static_cast<int>(m.Hl * m.d), m.int8, w.go);
     p.pro = m.q8g(1) ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.a;
     p.x_ld = static_cast<int>(m.Hl * m.d);
@@ -771,7 +781,7 @@ struct Enqueuer {
 
   void k4_up(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
-    gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8);
+    gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8, w.gup);
     if (m.xs_ln) {
       if (m.fuse_ln)
         ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8g(2));
@@ -805,7 +815,7 @@ struct Enqueuer {
 
   void k5_down(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
-    gemm::Params p = base_params(m, w.wdown, w.sdown, static_cast<int>(m.h), static_cast<int>(m.Fl), m.int8);
+    gemm::Params p = base_params(m, w.wdown, w.sdown, static_cast<int>(m.h), static_cast<int>(m.Fl), m.int8, w.gdown);
     p.pro = m.q8g(3) ? gemm::PRO_QUANT : gemm::PRO_F16;
     p.x = sh.u;
     p.x_ld = static_cast<int>(m.Fl);
@@ -1232,6 +1242,11 @@ void validate_configs(const dsinf_model_config& c, const dsinf_runtime_config& r
   if (r.tp_mode == DSINF_TP_NCCL || r.tp_mode == DSINF_TP_SLICE || r.tp_mode == DSINF_TP_IPC)
     require(r.tp_rank >= 0 && r.tp_rank < r.tp_size, "bad tp_rank");
   if (r.tp_mode == DSINF_TP_IPC) require(r.use_step_kernel == 0, "the persistent step kernel is TP = 1 only");
+  require(r.int8_group == 0 || r.int8_group == 128, "int8_group must be 0 (row scales) or 128");
+  if (r.int8_group != 0) {
+    require(c.dtype_bytes == 1, "int8_group needs int8 weights (dtype_bytes 1)");
+    require(r.use_step_kernel == 0, "int8_group: the persistent step kernel takes row scales only");
+  }
 }
 
 void build_rope(Model& m, cudaStream_t s) {
@@ -1326,6 +1341,8 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       if (const char* am = std::getenv("DSINF_A16_MASK")) m->a16_mask = static_cast<int>(std::strtol(am, nullptr, 0)) & 0xf;
     }
     m->a16 = m->a16_mask != 0;
+    if (m->int8 && rt->int8_group != 0)  // K-group scales are dequantised by the W8A16 main loop
+      require(m->a16_mask == 0xf, "int8_group: every decode GEMM must be W8A16 (int8_act W8A16, or AUTO at batch <= 8)");
     if (rt->use_step_kernel && m->int8) {  // the persistent step kernel runs INT8 weight-only
       require(rt->int8_act != DSINF_INT8_W8A8, "the persistent step kernel runs INT8 as W8A16 (weight-only)");
       m->a16_mask = 0xf;
@@ -1521,6 +1538,7 @@ int dsinf_model_prefill(dsinf_model* m, void* stream) {
     require(m->host_pos == 0, "prefill must start at position 0 (call dsinf_model_set_prompt first)");
     require(m->rt.tp_mode != DSINF_TP_IPC || m->t == 1,
             "prefill: DSINF_TP_IPC has no all-reduce for the large-batch GEMMs (use decode steps)");
+    require(m->rt.int8_group == 0, "prefill: the tensor-core prefill takes per-row INT8 scales (int8_group = 0)");
     require(m->d % 32 == 0 && m->d <= 256, "prefill attention needs head_dim % 32 == 0 and <= 256");
     require(m->h % 16 == 0 && (m->Hl * m->d) % 16 == 0 && m->Fl % 16 == 0,
             "prefill needs 16-byte TMA rows (hidden, per-rank head and MLP widths % 16 == 0)");

@@ -85,6 +85,37 @@ __global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t*
   }
 }
 
+// The same synthetic tensor quantised per (global output row, 128-k group) (K_local and col_off
+// multiples of 128, so a group never straddles TP shards): fp16 scale s = fp16(max|w| / 127), q =
+// clamp(rint(w / s)); one warp per (row, group), lane l owns packed word l of the group.
+__global__ void init_packed_i8_groups_kernel(ShardMap m, uint32_t* packed, __half* gscales) {
+  const int64_t G = m.K_local / kI8Group;
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(warps) + (threadIdx.x >> 5); u < m.N_local * G;
+       u += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t n = u / G, g = u - n * G;
+    const int64_t grow = global_row(m, n);
+    const int64_t k0 = g * kI8Group + 4 * lane;
+    float v[4];
+    float mx = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[e] = synth_value(m, grow, m.col_off + k0 + e);
+      mx = fmaxf(mx, fabsf(v[e]));
+    }
+    mx = ptx::warp_max(mx);
+    __half sh = __float2half_rn(mx > 0.f ? __fdiv_rn(mx, 127.0f) : 1.0f);
+    if (__half2float(sh) == 0.f) sh = __float2half_rn(1.0f);
+    const float sc = __half2float(sh);
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) word |= q8(v[e], sc) << (8 * e);
+    packed[(k0 / 4) * m.N_local + n] = word;
+    if (lane == 0) gscales[g * m.N_local + n] = sh;
+  }
+}
+
 // Row-major [N_local][K_local] copies of the same synthetic tensor for the tensor-core
 // (large-batch) path: fp16 values, or int8 quantised with the packed layout's row scales (so both
 // layouts hold identical int8 weights).
@@ -642,6 +673,14 @@ void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStre
   DSINF_CUDA_CHECK(cudaGetLastError());
   const int64_t total = (m.K_local + 3) / 4 * m.N_local;
   init_packed_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, scales, packed);
+  DSINF_CUDA_CHECK(cudaGetLastError());
+}
+
+void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s) {
+  if (m.K_local % kI8Group != 0 || m.col_off % kI8Group != 0)
+    throw ConfigError("K-group INT8 weights need per-rank in_dim (and shard offsets) multiples of 128");
+  const int64_t units = m.N_local * (m.K_local / kI8Group);
+  init_packed_i8_groups_kernel<<<blocks_for(units, 8, 148 * 16), 256, 0, s>>>(m, packed, gscales);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 

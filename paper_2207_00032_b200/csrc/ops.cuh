@@ -11,6 +11,8 @@ namespace ops {
 // Logical (un-sharded) position of a local weight element under Megatron TP sharding.
 //   global row = (n / sec_local) * sec_global + row_off + n % sec_local
 //   global col = col_off + k;  flat = row * K_global + col
+constexpr int kI8Group = 128;  // INT8 K-group size (128 consecutive k share an fp16 scale)
+
 struct ShardMap {
   int64_t N_local, K_local;
   int64_t N_global, K_global;
@@ -24,6 +26,8 @@ struct ShardMap {
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s);
 // Same tensor quantised per global output row to int8 (pack_M = 4) + fp32 row scales.
 void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s);
+// Same tensor quantised per (global row, 128-k group): fp16 scales [K_local/128][N_local].
+void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s);
 // Row-major [N_local][K_local] copy of the same tensor for the tensor-core path: fp16, or int8
 // quantised with the given (packed-layout) row scales.
 void init_rowmajor_map_f16(const ShardMap& m, __half* out, cudaStream_t s);
@@ -43,7 +47,6 @@ void pack_f16(const void* w, bool src_f32, int64_t N, int64_t K, int pack_M, __h
 void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, float* scales, cudaStream_t s);
 // K-group scales (kI8Group = 128 consecutive k per row share an fp16 scale; gscales [ceil(K/128)][N]),
 // packed like quantize_weights_i8; the W8A16 GEMM dequantises w = fp16(q * s) per group.
-constexpr int kI8Group = 128;
 void quantize_weights_i8_groups(const __half* w, int64_t N, int64_t K, int8_t* packed, __half* gscales,
                                 cudaStream_t s);
 // Per-token int8 quantisation of activations [B][K] (same formula as the GEMM prologue).

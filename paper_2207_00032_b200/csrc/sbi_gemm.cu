@@ -596,6 +596,8 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
   p.a16 = plan.a16;
+  if (p.w_gscale != nullptr && !(int8_weights && plan.a16))
+    throw ConfigError("sbi_gemm: K-group scales need int8 weights on the W8A16 plan");
   p.x_row_words = (plan.a16 ? 2 : 1) * plan.rows_per_split + 8;
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");

@@ -41,10 +41,11 @@ class DecoderModel:
                  dtype_bytes: int = 2, batch: int = 1, max_ctx: int = 256, tp_size: int = 1, tp_rank: int = 0,
                  tp_mode: int = capi.TP_NONE, nccl_comm: Optional[int] = None, use_cuda_graph: bool = True,
                  use_pdl: bool = True, use_step_kernel: bool = False, seed: int = 20220701, ln_eps: float = 1e-5, rope_base: float = 10000.0,
-                 device: int = 0, int8_act: int = capi.INT8_W8A8, ipc_exchange=None):
+                 device: int = 0, int8_act: int = capi.INT8_W8A8, ipc_exchange=None, int8_group: int = 0):
         self.cfg = capi.ModelConfig(hidden, layers, heads, vocab, max_seq, dtype_bytes)
         self.rt = capi.RuntimeConfig(batch, tp_size, tp_rank, tp_mode, int(use_cuda_graph), int(use_pdl), max_ctx,
-                                     seed, ln_eps, rope_base, device, int(use_step_kernel), int(int8_act))
+                                     seed, ln_eps, rope_base, device, int(use_step_kernel), int(int8_act),
+                                     int(int8_group))
         self.batch, self.vocab, self.max_ctx = batch, vocab, max_ctx
         self.hidden, self.layers, self.heads = hidden, layers, heads
         self._h = C.c_void_p()

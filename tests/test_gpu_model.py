@@ -22,7 +22,8 @@ SEED = 20220701
 
 
 def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, prompt_len=6, gen=4,
-               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=False, int8_act=0, oracle_int8_act=None):
+               use_graph=True, use_pdl=True, max_ctx=32, step_kernel=False, int8_act=0, oracle_int8_act=None,
+               int8_group=0):
     tol_rel, tol_abs = (0.03, 0.01) if dtype_bytes == 2 else (0.06, 0.02)
     if step_kernel and dtype_bytes == 1 and int8_act == capi.INT8_W8A8:
         int8_act = capi.INT8_W8A16  # the persistent step kernel runs INT8 weight-only
@@ -31,9 +32,10 @@ def run_parity(hidden, layers, heads, vocab, *, batch=1, dtype_bytes=2, tp=1, pr
     mode = capi.TP_LOCAL if tp > 1 else capi.TP_NONE
     gpu = DecoderModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, batch=batch, max_ctx=max_ctx,
                        tp_size=tp, tp_mode=mode, use_cuda_graph=use_graph, use_pdl=use_pdl, seed=SEED,
-                       use_step_kernel=step_kernel, int8_act=int8_act)
+                       use_step_kernel=step_kernel, int8_act=int8_act, int8_group=int8_group)
     ora = O.OracleModel(hidden, layers, heads, vocab, dtype_bytes=dtype_bytes, tp=tp, batch=batch, max_ctx=max_ctx,
-                        seed=SEED, int8_act=int8_act if oracle_int8_act is None else oracle_int8_act)
+                        seed=SEED, int8_act=int8_act if oracle_int8_act is None else oracle_int8_act,
+                        int8_group=int8_group)
     gpu.set_prompt(prompt)
     worst = 0.0
     margins = []
@@ -408,3 +410,17 @@ def test_prefill_single_weight_copy_identical(dtype_bytes, monkeypatch):
         m.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("tp,batch", [(1, 1), (1, 5), (2, 3), (4, 2)])
+def test_int8_k_group_decode_matches_oracle(tp, batch):
+    """INT8 decode with K-group weight scales (int8_group = 128, "per-group
+    dequant"): every layer GEMM weight-only with the per-group dequant in the SBI-GeMM main loop,
+    against the oracle's K-group restatement (same q and fp16 scales, fp64 sums), TP shards on one
+    device included (a group never straddles a shard)."""
+    run_parity(512, 2, 8, 1000, batch=batch, dtype_bytes=1, tp=tp, int8_act=capi.INT8_W8A16, int8_group=128)
+
+
+def test_int8_k_group_rejects_w8a8():
+    with pytest.raises(capi.ConfigError):
+        DecoderModel(256, 1, 4, 1000, dtype_bytes=1, batch=1, max_ctx=16, int8_act=capi.INT8_W8A8, int8_group=128)

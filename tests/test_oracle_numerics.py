@@ -181,3 +181,20 @@ def test_int8_group_scales_reduce_quantisation_error():
     ey_grp = np.abs(x @ wg.T - y).max()
     print(f"weight rms error: per-row {e_row:.3e}, K-group {e_grp:.3e}; max |dy|: {ey_row:.3e} vs {ey_grp:.3e}")
     assert e_grp < 0.7 * e_row and ey_grp < ey_row
+
+
+def test_oracle_k_group_model_runs_and_differs_from_row_scales():
+    """The oracle decoder with K-group INT8 weights (int8_group = 128, W8A16) differs from the
+    per-row one (different quantised weights) but stays close to the fp16 model."""
+    kw = dict(batch=2, max_ctx=8, seed=5)
+    toks = np.array([3, 7], dtype=np.int32)
+    outs = {}
+    for name, args in {"fp16": dict(dtype_bytes=2), "row": dict(dtype_bytes=1, int8_act=1),
+                       "group": dict(dtype_bytes=1, int8_act=1, int8_group=128)}.items():
+        m = O.OracleModel(256, 2, 4, 500, **kw, **args)
+        outs[name] = m.step(toks, 0)[0]
+        m.close()
+    assert not np.array_equal(outs["row"], outs["group"])
+    e_row = np.abs(outs["row"] - outs["fp16"]).max()
+    e_grp = np.abs(outs["group"] - outs["fp16"]).max()
+    assert e_grp < 0.1 * np.abs(outs["fp16"]).max() and e_row < 0.1 * np.abs(outs["fp16"]).max()
