@@ -613,6 +613,16 @@ struct Consumer {
   __device__ __forceinline__ void run_a16(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
                                           uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step = 1,
                                           const __half* gs = nullptr, int gs_ld = 0, int gs_valid = 0) {
+    // two instantiations of the loop: the row-scale loop carries no group-scale registers
+    if (gs == nullptr)
+      run_a16_loop<false>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid);
+    else
+      run_a16_loop<true>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid);
+  }
+  template <bool kGroups, class XWord>
+  __device__ __forceinline__ void run_a16_loop(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
+                                               uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step,
+                                               const __half* gs, int gs_ld, int gs_valid) {
     const uint8_t* wbox = ring + cw * kBoxBytes;
     __half2 gsc[2][2], gsn[2][2];
     auto load_gs = [&](int i, __half2 (&o)[2][2]) {
@@ -624,9 +634,13 @@ struct Consumer {
           o[j][h] = __half2half2(c < gs_valid ? gs[static_cast<size_t>(i) * gs_ld + c] : __ushort_as_half(0));
         }
     };
-    if (gs != nullptr && n_iters > 0) load_gs(0, gsc);
+    if constexpr (kGroups) {
+      if (n_iters > 0) load_gs(0, gsc);
+    }
     for (int it = 0; it < n_iters; ++it) {
-      if (gs != nullptr && it + 1 < n_iters) load_gs(it + 1, gsn);
+      if constexpr (kGroups) {
+        if (it + 1 < n_iters) load_gs(it + 1, gsn);
+      }
       ptx::mbar_wait(&hd.full[s], phase);
       const uint8_t* sw = wbox + s * stage_bytes;
 #pragma unroll
@@ -640,7 +654,7 @@ struct Consumer {
           uint32_t a0, a1, a2, a3;
           i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][0][kk & 1]), a0, a2);
           i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][1][kk & 1]), a1, a3);
-          if (gs != nullptr) {
+          if constexpr (kGroups) {
             a0 = h2_bits(__hmul2(bits_h2(a0), gsc[j][0]));
             a2 = h2_bits(__hmul2(bits_h2(a2), gsc[j][0]));
             a1 = h2_bits(__hmul2(bits_h2(a1), gsc[j][1]));
@@ -657,7 +671,7 @@ struct Consumer {
         s -= stages;
         phase ^= 1;
       }
-      if (gs != nullptr) {
+      if constexpr (kGroups) {
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll

@@ -604,7 +604,11 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
   const int kps = kRowsPerStage * f.kpr;  // k per stage
   // LayerNorm phases: the whole normalised row is the same for every segment -- built once per
   // phase when it fits the slice (fp16 words: K / 2 per row)
-  const bool full_x = gp.pro == gemm::PRO_LN && gp.K / 2 <= P.x_cap;
+  // (the whole-row slice covers every stage of the phase: K/2 words rounded up to whole stages,
+  // zero past K -- the weights of a partial last stage are zero-filled by TMA, but 0 x stale smem
+  // could be NaN)
+  const int full_words = f.spt * kRowsPerStage * f.xw;
+  const bool full_x = gp.pro == gemm::PRO_LN && full_words <= P.x_cap;
   if (grp == 0) {
     if (f.dep == DEP_FULL) {
       const unsigned t = (epoch + 1u) * f.dep_target;
@@ -614,7 +618,7 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
       });
     }
     if (lead) trace_rec(P, cta, p, 1);
-    if (full_x) fill_x_ln_fast(gp, sx, hd, 0, gp.K / 2, P.xrw, ctid);
+    if (full_x) fill_x_ln_fast(gp, sx, hd, 0, full_words, P.xrw, ctid);
   }
   if (full_x) all_bar();
   if (full_x && lead) trace_rec(P, cta, p, 5);

@@ -96,6 +96,14 @@ def test_gpt2_shape_two_layers(step_kernel):
     run_parity(1600, 2, 25, 50257, prompt_len=4, gen=3, max_ctx=16, step_kernel=step_kernel)
 
 
+@PATHS
+def test_gpt2_shape_int8_partial_stage(step_kernel):
+    """INT8 at GPT-2 widths: K = 1600 ends in a partial 128-k weight stage (zero-filled by TMA), whose
+    x words must be zero too (the persistent kernel's whole-row LayerNorm slice)."""
+    run_parity(1600, 2, 25, 50257, dtype_bytes=1, prompt_len=4, gen=3, max_ctx=16, step_kernel=step_kernel,
+               int8_act=capi.INT8_W8A16)
+
+
 def test_step_kernel_matches_per_kernel_path():
     """Both TP=1 paths give the same greedy tokens and logits within fp32 split-K reordering."""
     prompt = np.random.default_rng(3).integers(0, 2000, (4, 9)).astype(np.int32)
