@@ -273,7 +273,9 @@ int dsinf_model_set_prompt_device(dsinf_model* m, const int32_t* prompt_dev, int
  * Needs a prompt set at position 0.  Every TP mode is supported: TP_NONE, TP_LOCAL and TP_NCCL
  * give the model's outputs (column-/row-parallel GEMMs, the row-parallel partials all-reduced,
  * vocab-parallel LM head with the argmax keys gathered); TP_SLICE runs rank tp_rank's shard alone
- * and its outputs are for timing only.  First call generates row-major weight copies. */
+ * and its outputs are for timing only; TP_IPC and int8_group = 128 are rejected (ConfigError).
+ * First call generates row-major weight copies, or -- when they would not fit -- one layer's
+ * operands refilled from the packed weights before each layer (one resident weight copy). */
 int dsinf_model_prefill(dsinf_model* m, void* stream);
 int dsinf_decode_step(dsinf_model* m, void* stream);
 /* Enqueue `steps` decode steps back to back. */
