@@ -586,23 +586,25 @@ template <bool kInt8, int kNB8, bool kA16 = false>
 struct Consumer {
   using Acc = typename std::conditional<kInt8 && !kA16, int, float>::type;
   Acc acc[2][kNB8][4];
-  uint32_t aoff[2][2][2];  // [j][h][par]  (kA16: par = parity of the 16-k step)
+  // MMA row m of block j (A-fragment rows g and g + 8 of lane (g, t)) is output column
+  // col(j, m) = 4 (m mod 8) + 2 j + (m >= 8) of the warp's 32: a lane's four A words of one packed
+  // row are the 16 contiguous bytes of columns 4g .. 4g+3 -- ONE 128-bit shared load instead of
+  // four 32-bit ones (the 128B swizzle moves whole 16-byte chunks; the 32 lanes of a load cover
+  // 4 rows x 128 B, the minimum 4 wavefronts).  Word 2j + h of the chunk = block j, row g + 8h.
+  uint32_t aoff4[2];  // [par] byte offset of the lane's chunk (kA16: par = parity of the 16-k step)
   int g, t;
 
   __device__ __forceinline__ void init(int lane) {
     g = lane >> 2;
     t = lane & 3;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int par = 0; par < 2; ++par) {
-          const int r = kA16 ? 4 * par + t : 2 * t + par;
-          const int c = 16 * j + 8 * h + g;
-          aoff[j][h][par] = r * 128 + (((c >> 2) ^ r) << 4) + (c & 3) * 4;
-        }
+    for (int par = 0; par < 2; ++par) {
+      const int r = kA16 ? 4 * par + t : 2 * t + par;
+      aoff4[par] = r * 128 + ((g ^ r) << 4);
+    }
   }
+  // output column (within the warp's 32) of accumulator element q of block j
+  __device__ __forceinline__ int acc_col(int j, int q) const { return 4 * g + 2 * j + (q >= 2 ? 1 : 0); }
   // W8A16 main loop; xword(it, kk, bt) returns the (b0, b1) x words of batch tile bt.
   // `step` > 1: this warp group consumes every step-th ring slot (the persistent step kernel's
   // interleaved consumer groups; stages % step == 0).
@@ -630,7 +632,7 @@ struct Consumer {
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int c = 16 * j + 8 * h + g;
+          const int c = 4 * g + 2 * j + h;
           o[j][h] = __half2half2(c < gs_valid ? gs[static_cast<size_t>(i) * gs_ld + c] : __ushort_as_half(0));
         }
     };
@@ -649,11 +651,13 @@ struct Consumer {
 #pragma unroll
         for (int bt = 0; bt < kNB8; ++bt) bx[bt] = xword(s, it, kk, bt);
         const uint8_t* a = sw + (kk >> 1) * 8 * 128;
+        const uint4 w4 = *reinterpret_cast<const uint4*>(a + aoff4[kk & 1]);
+        const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t a0, a1, a2, a3;
-          i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][0][kk & 1]), a0, a2);
-          i8x4_to_h2x2(*reinterpret_cast<const uint32_t*>(a + aoff[j][1][kk & 1]), a1, a3);
+          i8x4_to_h2x2(wq[2 * j], a0, a2);
+          i8x4_to_h2x2(wq[2 * j + 1], a1, a3);
           if constexpr (kGroups) {
             a0 = h2_bits(__hmul2(bits_h2(a0), gsc[j][0]));
             a2 = h2_bits(__hmul2(bits_h2(a2), gsc[j][0]));
@@ -712,12 +716,14 @@ struct Consumer {
           b1[bt] = v.y;
         }
         const uint8_t* a = sw + ks * 8 * 128;
+        const uint4 w0 = *reinterpret_cast<const uint4*>(a + aoff4[0]);  // packed row 2t
+        const uint4 w1 = *reinterpret_cast<const uint4*>(a + aoff4[1]);  // packed row 2t + 1
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][0]);
-          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][0]);
-          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][1]);
-          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
+          const uint32_t a0 = j == 0 ? w0.x : w0.z;
+          const uint32_t a1 = j == 0 ? w0.y : w0.w;
+          const uint32_t a2 = j == 0 ? w1.x : w1.z;
+          const uint32_t a3 = j == 0 ? w1.y : w1.w;
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt) {
             if constexpr (kInt8 && !kA16)
@@ -765,12 +771,14 @@ struct Consumer {
           b1[bt] = v.y;
         }
         const uint8_t* a = sw + ks * 8 * 128;
+        const uint4 w0 = *reinterpret_cast<const uint4*>(a + aoff4[0]);  // packed row 2t
+        const uint4 w1 = *reinterpret_cast<const uint4*>(a + aoff4[1]);  // packed row 2t + 1
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const uint32_t a0 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][0]);
-          const uint32_t a1 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][0]);
-          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(a + aoff[j][0][1]);
-          const uint32_t a3 = *reinterpret_cast<const uint32_t*>(a + aoff[j][1][1]);
+          const uint32_t a0 = j == 0 ? w0.x : w0.z;
+          const uint32_t a1 = j == 0 ? w0.y : w0.w;
+          const uint32_t a2 = j == 0 ? w1.x : w1.z;
+          const uint32_t a3 = j == 0 ? w1.y : w1.w;
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt) {
             if constexpr (kInt8 && !kA16)
@@ -794,15 +802,15 @@ struct Consumer {
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int bt = 0; bt < kNB8; ++bt) {
-        const int n = cw * kWarpCols + j * 16 + g;
+        const int n = cw * kWarpCols + acc_col(j, 0);  // elements 2, 3: column n + 1
         const int b = bt * 8 + 2 * t;
         if (b < B) {
           part[b * ld + n] = acc[j][bt][0];
-          part[b * ld + n + 8] = acc[j][bt][2];
+          part[b * ld + n + 1] = acc[j][bt][2];
         }
         if (b + 1 < B) {
           part[(b + 1) * ld + n] = acc[j][bt][1];
-          part[(b + 1) * ld + n + 8] = acc[j][bt][3];
+          part[(b + 1) * ld + n + 1] = acc[j][bt][3];
         }
       }
   }

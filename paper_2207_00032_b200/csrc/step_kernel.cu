@@ -682,7 +682,7 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
       for (int bt = 0; bt < kNB8; ++bt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int col = cw * gemm::kWarpCols + j * 16 + c.g + (q >= 2 ? 8 : 0);
+          const int col = cw * gemm::kWarpCols + c.acc_col(j, q);
           const int b = bt * 8 + 2 * c.t + (q & 1);
           if (b < B) red_add(acc + static_cast<size_t>(b) * kColTile + col, __float2ll_rn(c.acc[j][bt][q] * kFix));
         }
