@@ -21,44 +21,11 @@ namespace {
 
 using dev::kAttnThreads;
 
-template <int TPP>
-__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_constant__ AttnParams p) {
-  constexpr int PPR = kAttnThreads / TPP;
-  extern __shared__ __align__(16) float asmem[];
+// Merge the C chunk partials of (b, head) across the cluster through DSMEM and write the output
+// row (and the int8 row max).  co / cst: this CTA's partial (unnormalised output, max, sum).
+__device__ __forceinline__ void merge_chunks_and_store(const AttnParams& p, float* co, float* cst, int head, int b,
+                                                       int c, int C, int tid) {
   const int d = p.d;
-  float* co = asmem + PPR * d + 2 * PPR;  // layout of attn_chunk's scratch
-  float* cst = co + d;
-  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
-  const int tid = threadIdx.x;
-  ptx::trace_begin(p.trace);
-  ptx::pdl_trigger();
-  // the position counter and the K/V rows of earlier positions were written by earlier steps (the
-  // previous graph launch has completed): they are read before the wait on this step's QKV GEMM
-  const int pos = *reinterpret_cast<const volatile int*>(p.pos);
-  const int ctx = pos + 1;
-  const int chunk = (ctx + C - 1) / C;
-  const int j0 = c * chunk;
-  const int j1 = min(ctx, j0 + chunk);
-  const int j_pre = p.kv_rows_cap > 0 ? max(j0, min(j1, pos)) : 0;
-  __half* kv = reinterpret_cast<__half*>(asmem + dev::attn_scratch_floats<TPP>(d));
-  if (j_pre > j0) {  // cp.async 16-byte pieces of rows [j0, j_pre) of K and V
-    const int per_row = d / 8, n = (j_pre - j0) * per_row;
-    const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
-    for (int i = tid; i < 2 * n; i += kAttnThreads) {
-      const int v = i >= n, ii = v ? i - n : i;
-      const int r = ii / per_row, q = ii - r * per_row;
-      const __half* src = (v ? p.vc : p.kc) + kv_base + static_cast<size_t>(j0 + r) * d + q * 8;
-      __half* dst = kv + (static_cast<size_t>(v) * p.kv_rows_cap + r) * d + q * 8;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst)), "l"(src) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  ptx::pdl_wait();
-  if (j_pre > j0) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-  }
-  dev::attn_chunk<TPP>(p, b, head, j0, j1, tid, asmem, [] { __syncthreads(); }, kv, j_pre, p.kv_rows_cap);
   // merge the C chunks of this (b, head) across the cluster
   if (C > 1)
     ptx::cluster_sync();
@@ -114,6 +81,204 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
   ptx::trace_end(p.trace);
 }
 
+template <int TPP>
+__global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int PPR = kAttnThreads / TPP;
+  extern __shared__ __align__(16) float asmem[];
+  const int d = p.d;
+  float* co = asmem + PPR * d + 2 * PPR;  // layout of attn_chunk's scratch
+  float* cst = co + d;
+  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
+  const int tid = threadIdx.x;
+  ptx::trace_begin(p.trace);
+  ptx::pdl_trigger();
+  // the position counter and the K/V rows of earlier positions were written by earlier steps (the
+  // previous graph launch has completed): they are read before the wait on this step's QKV GEMM
+  const int pos = *reinterpret_cast<const volatile int*>(p.pos);
+  const int ctx = pos + 1;
+  const int chunk = (ctx + C - 1) / C;
+  const int j0 = c * chunk;
+  const int j1 = min(ctx, j0 + chunk);
+  const int j_pre = p.kv_rows_cap > 0 ? max(j0, min(j1, pos)) : 0;
+  __half* kv = reinterpret_cast<__half*>(asmem + dev::attn_scratch_floats<TPP>(d));
+  if (j_pre > j0) {  // cp.async 16-byte pieces of rows [j0, j_pre) of K and V
+    const int per_row = d / 8, n = (j_pre - j0) * per_row;
+    const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
+    for (int i = tid; i < 2 * n; i += kAttnThreads) {
+      const int v = i >= n, ii = v ? i - n : i;
+      const int r = ii / per_row, q = ii - r * per_row;
+      const __half* src = (v ? p.vc : p.kc) + kv_base + static_cast<size_t>(j0 + r) * d + q * 8;
+      __half* dst = kv + (static_cast<size_t>(v) * p.kv_rows_cap + r) * d + q * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(dst)), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  ptx::pdl_wait();
+  if (j_pre > j0) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+  dev::attn_chunk<TPP>(p, b, head, j0, j1, tid, asmem, [] { __syncthreads(); }, kv, j_pre, p.kv_rows_cap);
+  merge_chunks_and_store(p, co, cst, head, b, c, C, tid);
+}
+
+// Bulk-copy (TMA, 1-D) variant: the chunk's K and V rows are contiguous in the cache
+// ([B][H][max_seq][d]), so one elected thread streams them into a 2-stage shared-memory ring of
+// kTmaRows positions (two cp.async.bulk per stage, completion as mbarrier transaction bytes) while
+// the CTA scores the previous stage from shared memory: a handful of large DMA requests per CTA
+// instead of 16-byte loads on every thread's dependency chain.  Same online softmax and merge
+// as attn_chunk / attention_kernel.
+constexpr int kTmaRows = 32;
+
+template <int TPP>
+__host__ __device__ constexpr size_t tma_ring_bytes(int d) {
+  return static_cast<size_t>(2) * 2 * kTmaRows * d * 2;
+}
+
+template <int TPP>
+__global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int PPR = kAttnThreads / TPP;  // positions scored in parallel
+  constexpr int kU = kTmaRows / PPR;       // positions per thread per stage
+  extern __shared__ __align__(128) uint8_t araw[];
+  const int d = p.d;
+  const size_t stage_halves = static_cast<size_t>(2) * kTmaRows * d;  // K rows then V rows
+  __half* ring = reinterpret_cast<__half*>(araw);
+  float* scratch = reinterpret_cast<float*>(araw + tma_ring_bytes<TPP>(d));
+  float* so = scratch;       // [PPR][d]
+  float* sm = so + PPR * d;  // [PPR]
+  float* sl = sm + PPR;      // [PPR]
+  float* co = sl + PPR;      // [d]
+  float* cst = co + d;       // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      araw + tma_ring_bytes<TPP>(d) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8);
+  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
+  const int tid = threadIdx.x;
+  ptx::trace_begin(p.trace);
+  ptx::pdl_trigger();
+  if (tid == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::pdl_wait();
+  const int ctx = *p.pos + 1;
+  const int chunk = (ctx + C - 1) / C;
+  const int j0 = c * chunk;
+  const int j1 = min(ctx, j0 + chunk);
+  const int n = max(0, j1 - j0);
+  const int nst = (n + kTmaRows - 1) / kTmaRows;
+  const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
+  const uint64_t pol = ptx::policy_evict_first();
+  auto issue = [&](int st) {
+    const int rows = min(kTmaRows, n - st * kTmaRows);
+    const uint32_t bytes = static_cast<uint32_t>(rows) * d * 2;
+    __half* dst = ring + (st & 1) * stage_halves;
+    const size_t src = kv_base + static_cast<size_t>(j0 + st * kTmaRows) * d;
+    ptx::mbar_arrive_expect_tx(&bars[st & 1], 2 * bytes);
+    ptx::bulk_g2s(dst, p.kc + src, bytes, &bars[st & 1], pol);
+    ptx::bulk_g2s(dst + static_cast<size_t>(kTmaRows) * d, p.vc + src, bytes, &bars[st & 1], pol);
+  };
+  __syncthreads();  // barrier init visible
+  if (tid == 0) {
+    if (nst > 0) issue(0);
+    if (nst > 1) issue(1);
+  }
+  const int slot = tid / TPP, lane_in = tid % TPP;
+  const int dim0 = lane_in * 8;
+  const bool has_dims = dim0 < d;
+  float q[8];
+  if (has_dims) {
+    const uint4 qu = __ldcg(reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(b) * p.H * d + head * d + dim0));
+    dev::h8_to_f(qu, q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] *= p.scale;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = 0.f;
+  for (int st = 0; st < nst; ++st) {
+    ptx::mbar_wait(&bars[st & 1], static_cast<uint32_t>((st >> 1) & 1));
+    const __half* ks = ring + (st & 1) * stage_halves;
+    const __half* vs = ks + static_cast<size_t>(kTmaRows) * d;
+    const int rows = min(kTmaRows, n - st * kTmaRows);
+    float sc[kU];
+    float mt = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int r = u * PPR + slot;
+      float sdot = 0.f;
+      if (r < rows && has_dims) {
+        float kf[8];
+        dev::h8_to_f(*reinterpret_cast<const uint4*>(ks + static_cast<size_t>(r) * d + dim0), kf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sdot = fmaf(q[i], kf[i], sdot);
+      }
+#pragma unroll
+      for (int off = TPP / 2; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+      sc[u] = r < rows ? sdot : -INFINITY;
+      mt = fmaxf(mt, sc[u]);
+    }
+    if (mt != -INFINITY) {
+      const float mn = fmaxf(m, mt);
+      const float corr = expf(m - mn);
+      l *= corr;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] *= corr;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (sc[u] == -INFINITY) continue;
+        const float pj = expf(sc[u] - mn);
+        l += pj;
+        if (has_dims) {
+          float vf[8];
+          dev::h8_to_f(*reinterpret_cast<const uint4*>(vs + static_cast<size_t>(u * PPR + slot) * d + dim0), vf);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i]);
+        }
+      }
+      m = mn;
+    }
+    __syncthreads();  // every thread is done with this ring slot
+    if (tid == 0 && st + 2 < nst) issue(st + 2);
+  }
+  // merge the PPR position slots of this CTA (attn_chunk's tail)
+  if (has_dims) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) so[slot * d + dim0 + i] = o[i];
+  }
+  if (lane_in == 0) {
+    sm[slot] = m;
+    sl[slot] = l;
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int sidx = 0; sidx < PPR; ++sidx) M = fmaxf(M, sm[sidx]);
+  for (int i = tid; i < d; i += kAttnThreads) {
+    float acc = 0.f;
+    for (int sidx = 0; sidx < PPR; ++sidx) {
+      const float w = sm[sidx] == -INFINITY ? 0.f : expf(sm[sidx] - M);
+      acc = fmaf(w, so[sidx * d + i], acc);
+    }
+    co[i] = acc;
+  }
+  if (tid == 0) {
+    float L = 0.f;
+    for (int sidx = 0; sidx < PPR; ++sidx) L += sm[sidx] == -INFINITY ? 0.f : sl[sidx] * expf(sm[sidx] - M);
+    cst[0] = M;
+    cst[1] = L;
+  }
+  __syncthreads();
+  merge_chunks_and_store(p, co, cst, head, b, c, C, tid);
+}
+
+template <int TPP>
+size_t tma_smem_bytes(int d) {
+  return tma_ring_bytes<TPP>(d) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8 + 16;
+}
+
 }  // namespace
 
 int attention_chunks(int B, int H) {
@@ -132,6 +297,17 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  if (carveout_max()) {
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
   // the K/V staging area (<= 48 KB) on top of the softmax scratch
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -149,10 +325,24 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
   if (p.d % 8 != 0 || p.d > 256) throw ConfigError("attention: head dim must be a multiple of 8 and <= 256");
   if (chunks < 1 || chunks > 16) throw ConfigError("attention: bad chunk count");
   const dim3 grid(p.H, p.B, chunks), block(kAttnThreads), cluster(1, 1, chunks);
+  // DSINF_ATTN_TMA=1: the bulk-copy K/V ring variant (16-byte aligned rows: d % 8 == 0).  Parity-
+  // tested; measured equal or slightly slower in the step (GPT-J in-step attention int8 B=16
+  // 11.7 -> 12.2 us, fp16 B=1 step 2.678 -> 2.713 ms), so the per-thread pipelined loads stay default
+  const int tma = [] { const char* v = std::getenv("DSINF_ATTN_TMA"); return v ? std::atoi(v) : 0; }();  // read per enqueue
+  if (tma && (reinterpret_cast<uintptr_t>(p.kc) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.vc) & 15) == 0) {
+    p.kv_rows_cap = 0;
+    if (p.d <= 64)
+      launch_pdl(attention_tma_kernel<8>, grid, block, tma_smem_bytes<8>(p.d), s, pdl, p, cluster);
+    else if (p.d <= 128)
+      launch_pdl(attention_tma_kernel<16>, grid, block, tma_smem_bytes<16>(p.d), s, pdl, p, cluster);
+    else
+      launch_pdl(attention_tma_kernel<32>, grid, block, tma_smem_bytes<32>(p.d), s, pdl, p, cluster);
+    return;
+  }
   // DSINF_ATTN_PREFETCH=1: K/V staging before the dependency wait (a chunk's rows at the largest
   // context must fit a 48 KB budget).  Measured slower and off by default: GPT-J B=1 int8 2.062 ->
   // 2.100 ms, fp16 2.671 -> 2.706; with attention PDL-launched (DSINF_PDL_MASK=0x8f) 2.150 / 2.691
-  static const int pre = [] { const char* v = std::getenv("DSINF_ATTN_PREFETCH"); return v ? std::atoi(v) : 0; }();
+  const int pre = [] { const char* v = std::getenv("DSINF_ATTN_PREFETCH"); return v ? std::atoi(v) : 0; }();
   const int rows_cap = (p.max_seq + chunks - 1) / chunks;
   const size_t kv_bytes = static_cast<size_t>(2) * rows_cap * p.d * 2;
   p.kv_rows_cap = pre && kv_bytes <= 48 * 1024 ? rows_cap : 0;

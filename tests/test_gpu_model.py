@@ -432,3 +432,12 @@ def test_int8_k_group_decode_matches_oracle(tp, batch):
 def test_int8_k_group_rejects_w8a8():
     with pytest.raises(capi.ConfigError):
         DecoderModel(256, 1, 4, 1000, dtype_bytes=1, batch=1, max_ctx=16, int8_act=capi.INT8_W8A8, int8_group=128)
+
+
+@pytest.mark.parametrize("batch,d_heads", [(1, 4), (5, 8), (16, 4)])
+def test_attention_bulk_copy_variant(batch, d_heads, monkeypatch):
+    """DSINF_ATTN_TMA=1: decode attention streaming each chunk's contiguous K/V rows through a
+    2-stage shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier) -- against the oracle,
+    head dims 128 and 64, contexts longer than one 32-row stage."""
+    monkeypatch.setenv("DSINF_ATTN_TMA", "1")
+    run_parity(512, 2, d_heads, 1000, batch=batch, prompt_len=40, gen=4, max_ctx=48)
