@@ -166,6 +166,11 @@ struct dsinf_model {
   // weights instead of a per-CTA smem slice.  xs_ln: the LayerNorm GEMMs (QKV, MLP-up, LM head)
   // take x from a row_prep launch; xs_od: attn-out / MLP-down (int8: after a quantise prep).
   bool xs_ln = false, xs_od = false, xs_lm = false;
+  // LayerNorm-streaming (gemm::Plan::ln_stream; TP = 1 with producer-fused statistics): the
+  // LayerNorm GEMMs stream the fp32 residual and normalise it per stage -- no row_prep launch.
+  // Not for W8A8 GEMMs (their per-token scale needs the whole normalised row).  DSINF_LN_STREAM=0: off
+  bool ln_stream = false;
+  bool ln_use(int g) const { return ln_stream && !q8g(g); }  // g: 0 QKV, 2 MLP-up, 4 LM head (fp16)
   unsigned long long* ltrace = nullptr;
   std::vector<int> ltrace_kinds;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
   int64_t ltrace_n = 0;
@@ -354,11 +359,13 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   }
   if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
   const bool i8 = m.int8;
-  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0));
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
+                                m.ln_use(0));
   sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1));
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2));
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2));
   sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3));
-  sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm);
+  sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm, false,
+                               m.ln_stream && m.xs_lm);
 }
 
 // Row-major copies of the layer GEMM weights for the tensor-core prefill (same synthetic values;
@@ -698,7 +705,13 @@ struct Enqueuer {
     const LayerW& w = sh.layers[l];
     const int N = static_cast<int>(3 * m.Hl * m.d);
     gemm::Params p = base_params(m, w.wqkv, w.sqkv, N, static_cast<int>(m.h), m.int8, w.gqkv);
-    if (m.xs_ln) {
+    if (m.ln_use(0)) {  // the residual streamed and LayerNorm'd per stage (Deep-Fusion region 1)
+      p.pro = gemm::PRO_LN;
+      p.res_in = sh.res[0];
+      p.ln_stats_in = lnslot(sh, 2 * l);
+      p.ln_g = w.ln1g;
+      p.ln_b = w.ln1b;
+    } else if (m.xs_ln) {
       RedIn red;  // fused all-reduce: row_prep sums the ranks' MLP-down slots of layer l - 1
       const bool use_slots = m.fused_ar && l > 0;
       if (use_slots) red = red_in(sh, 1, l - 1);
@@ -782,7 +795,13 @@ struct Enqueuer {
   void k4_up(Shard& sh, int l) {
     const LayerW& w = sh.layers[l];
     gemm::Params p = base_params(m, w.wup, w.sup, static_cast<int>(m.Fl), static_cast<int>(m.h), m.int8, w.gup);
-    if (m.xs_ln) {
+    if (m.ln_use(2)) {  // Deep-Fusion region 3: LayerNorm per streamed stage, no row_prep
+      p.pro = gemm::PRO_LN;
+      p.res_in = sh.res[0];
+      p.ln_stats_in = lnslot(sh, 2 * l + 1);
+      p.ln_g = w.ln2g;
+      p.ln_b = w.ln2b;
+    } else if (m.xs_ln) {
       if (m.fuse_ln)
         ln_x(sh, p, sh.res[0], lnslot(sh, 2 * l + 1), nullptr, nullptr, nullptr, w.ln2g, w.ln2b, m.q8g(2));
       else if (m.fused_ar) {
@@ -848,7 +867,13 @@ struct Enqueuer {
     RedIn red;
     const bool fold_red = fold && m.fused_ar;
     if (fold_red) red = red_in(sh, 1, static_cast<int>(m.L) - 1);
-    if (m.xs_lm) {
+    if (m.ln_stream && m.xs_lm) {
+      p.pro = gemm::PRO_LN;
+      p.res_in = sh.res[0];
+      p.ln_stats_in = lnslot(sh, 2 * static_cast<int>(m.L));
+      p.ln_g = sh.lnfg;
+      p.ln_b = sh.lnfb;
+    } else if (m.xs_lm) {
       ln_x(sh, p, sh.res[0], m.fuse_ln ? lnslot(sh, 2 * static_cast<int>(m.L)) : nullptr, fold ? sh.d_mlp : nullptr,
            fold ? sh.layers[m.L - 1].bdown : nullptr, nullptr, sh.lnfg, sh.lnfb, false, fold_red ? &red : nullptr);
     } else {
@@ -1375,6 +1400,8 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
       const char* lm = std::getenv("DSINF_XS_LM");
       m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
+      const char* lsv = std::getenv("DSINF_LN_STREAM");
+      m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : true);
       // fused all-reduce: on-device shards (DSINF_TP_LOCAL) or CUDA-IPC peer mappings across
       // processes; the per-CTA LayerNorm prologue path (slice plan) consumes the slots, the row_prep
       // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every

@@ -42,14 +42,22 @@ using dev::Header;
 // kXS (x-streaming, large batch): stages are 18 KB (weights + the x box), no x slice.
 // kA16 (int8 weights only): W8A16 -- x stays fp16 (slice of fp16 pairs, or two x boxes per
 // 128-k stage when streamed), weights widened in registers, fp32 accumulate, y = acc * w_scale.
-template <bool kInt8, int kNB8, bool kXS, bool kA16>
+// kXS: 0 smem x slice, 1 x-streaming, 2 LayerNorm-streaming (fp32 residual boxes per stage,
+// normalised by the consumers into the stage's fp16 x boxes; fp16 or W8A16 weights).
+template <bool kInt8, int kNB8, int kXS, bool kA16>
 __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
   static_assert(!kA16 || kInt8, "W8A16 needs int8 weights");
+  constexpr bool kLN = kXS == 2;
+  static_assert(!kLN || !kInt8 || kA16, "LayerNorm-streaming takes fp16 or W8A16 weights");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
-  constexpr int kSB = kXS ? (kA16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes;
-  constexpr int kXBoxes = kA16 ? 2 : 1;  // x boxes per streamed stage
+  constexpr int kSB = kLN ? (kA16 ? kStageBytesLN16 : kStageBytesLN)
+                          : (kXS ? (kA16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes);
+  constexpr int kXBoxes = kA16 ? 2 : 1;           // fp16 x boxes per streamed stage
+  constexpr int kRBoxes = kLN ? 2 * kXBoxes : 0;  // fp32 residual boxes per stage (LayerNorm-streaming)
+  constexpr int kXOff = kStageBytes + kRBoxes * kXBoxBytes;  // the x boxes within a stage
+  constexpr int kKPerRow = kInt8 ? 4 : 2;        // k per packed weight row
   uint8_t* ring = smem;
   Header& hd = *reinterpret_cast<Header*>(smem + stages * kSB);
   uint32_t* sx = reinterpret_cast<uint32_t*>(smem + stages * kSB + kHeaderBytes);
@@ -94,7 +102,22 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       // weights of the first `stages` stages before the dependency, their x boxes after it
       const uint64_t policy = ptx::policy_evict_first();
       const uint64_t xpolicy = ptx::policy_evict_last();  // x is re-read by every column tile
-      const uint32_t tx = kStageBytes + kXBoxes * p.B * 128;
+      const uint32_t tx = kStageBytes + (kLN ? kRBoxes : kXBoxes) * p.B * 128;
+      // the stage's activation boxes: GEMM-ready x words, or (kLN) the fp32 residual of its k range
+      auto load_x = [&](int it, uint8_t* st) {
+        const int r0 = row_begin + it * kRowsPerStage;
+        if constexpr (kLN) {
+#pragma unroll
+          for (int rb = 0; rb < kRBoxes; ++rb)
+            ptx::tma_load_2d(st + kStageBytes + rb * kXBoxBytes, &p.xmap, kKPerRow * r0 + rb * 32, 0,
+                             &hd.full[it % stages], xpolicy);
+        } else {
+#pragma unroll
+          for (int xb = 0; xb < kXBoxes; ++xb)
+            ptx::tma_load_2d(st + kStageBytes + xb * kXBoxBytes, &p.xmap, kXBoxes * r0 + xb * kRowsPerStage, 0,
+                             &hd.full[it % stages], xpolicy);
+        }
+      };
       const int pre = min(stages, n_iters);
       for (int it = 0; it < pre; ++it) {
         ptx::mbar_arrive_expect_tx(&hd.full[it], tx);
@@ -104,11 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           ptx::tma_load_2d(ring + it * kSB + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[it], policy);
       }
       ptx::pdl_wait();
-      for (int it = 0; it < pre; ++it)
-#pragma unroll
-        for (int xb = 0; xb < kXBoxes; ++xb)
-          ptx::tma_load_2d(ring + it * kSB + kStageBytes + xb * kXBoxBytes, &p.xmap,
-                           kXBoxes * (row_begin + it * kRowsPerStage) + xb * kRowsPerStage, 0, &hd.full[it], xpolicy);
+      for (int it = 0; it < pre; ++it) load_x(it, ring + it * kSB);
       int s = pre % stages;
       uint32_t phase = pre == stages ? 1u : 0u;
       for (int it = pre; it < n_iters; ++it) {
@@ -119,10 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w)
           ptx::tma_load_2d(dst + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[s], policy);
-#pragma unroll
-        for (int xb = 0; xb < kXBoxes; ++xb)
-          ptx::tma_load_2d(dst + kStageBytes + xb * kXBoxBytes, &p.xmap, kXBoxes * r0 + xb * kRowsPerStage, 0,
-                           &hd.full[s], xpolicy);
+        load_x(it, dst);
         if (++s == stages) {
           s = 0;
           phase ^= 1;
@@ -157,6 +173,22 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     // ================= consumers
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
+    // LayerNorm-streaming: gamma / beta of this split's k range into smem (weights: before the wait)
+    __half* sg = reinterpret_cast<__half*>(sx);
+    __half* sb = sg + p.rows_per_split * kKPerRow;
+    if constexpr (kLN) {
+      const int k0 = row_begin * kKPerRow, nk = p.rows_per_split * kKPerRow;  // nk % 64 == 0
+      for (int i = ctid; i < nk / 8; i += 128) {
+        const int k = k0 + 8 * i;
+        uint4 g = make_uint4(0u, 0u, 0u, 0u), b = make_uint4(0u, 0u, 0u, 0u);
+        if (k < p.K) {  // K % 8 == 0 on this plan
+          g = __ldg(reinterpret_cast<const uint4*>(p.ln_g + k));
+          b = __ldg(reinterpret_cast<const uint4*>(p.ln_b + k));
+        }
+        reinterpret_cast<uint4*>(sg)[i] = g;
+        reinterpret_cast<uint4*>(sb)[i] = b;
+      }
+    }
     ptx::pdl_wait();
 #ifdef DSINF_DIAG
     const unsigned long long t_rel = ptx::trace_release(p.trace, 32);
@@ -169,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       if (ctid == 0) ptx::wait_flag(p.red_flag, p.step_ctr, p.red_per_step);
       dev::consumer_bar();
     }
-    if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
+    if (kLN) {  // the residual arrives with the weights; the row statistics come from the producer
+      if (ctid < p.B) dev::ln_from_sums(p.ln_stats_in, ctid, p.ln_inv_k, p.ln_eps, hd.mean[ctid], hd.rstd[ctid]);
+    } else if (kXS) {  // x arrives with the weights; only the per-token int8 scales are needed
       if (kInt8 && !kA16 && ctid < p.B) hd.xscale[ctid] = p.x_scale[ctid];
     } else if (kA16) {  // fp16 x slice, in units of fp16 pairs: twice the packed int8 rows
       if (p.pro == PRO_LN && p.ln_stats_in != nullptr) {
@@ -207,6 +241,30 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     c.zero();
     int s = 0;
     uint32_t phase = 0;
+    // LayerNorm-streaming: the 128 consumer threads turn stage st's fp32 residual boxes into its fp16
+    // x boxes ((v - mean) rstd g + b, row_prep's expression), then a consumer barrier
+    auto ln_pre = [&](int st, int it) {
+      if constexpr (kLN) {
+        uint8_t* stg = ring + st * kSB;
+        const int kl0 = it * kRowsPerStage * kKPerRow;  // k offset of the stage within the split
+        constexpr int W = kXBoxes * 32;               // fp16 x words per row per stage
+        for (int i = ctid; i < p.B * W; i += 128) {
+          const int r = i / W, w = i - r * W;
+          const int e = 2 * w, rb = e >> 5, ee = e & 31;
+          const float2 v = *reinterpret_cast<const float2*>(stg + kStageBytes + rb * kXBoxBytes + r * 128 +
+                                                            (((ee >> 2) ^ (r & 7)) << 4) + (ee & 3) * 4);
+          const __half2 g2 = *reinterpret_cast<const __half2*>(sg + kl0 + e);
+          const __half2 b2 = *reinterpret_cast<const __half2*>(sb + kl0 + e);
+          const float mean = hd.mean[r], rstd = hd.rstd[r];
+          const uint32_t word = dev::pack_h2((v.x - mean) * rstd * __low2float(g2) + __low2float(b2),
+                                             (v.y - mean) * rstd * __high2float(g2) + __high2float(b2));
+          const int xb = w >> 5, ww = w & 31;
+          *reinterpret_cast<uint32_t*>(stg + kXOff + xb * kXBoxBytes + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) +
+                                       (ww & 3) * 4) = word;
+        }
+        dev::consumer_bar();
+      }
+    };
     if constexpr (kA16) {
       const int g = lane >> 2, t = lane & 3;
       // K-group scales: stage i of this split is group row_begin / kRowsPerStage + i
@@ -219,9 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           const int r = bt * 8 + g;
           if (r >= p.B) return make_uint2(0u, 0u);
           const int w = 8 * kk + 2 * t, ww = w & 31;
-          const uint8_t* xb = ring + st * kSB + kStageBytes + (w >> 5) * kXBoxBytes;
+          const uint8_t* xb = ring + st * kSB + kXOff + (w >> 5) * kXBoxBytes;
           return *reinterpret_cast<const uint2*>(xb + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) + (ww & 3) * 4);
-        }, 1, gs, p.N, gs_valid);
+        }, 1, gs, p.N, gs_valid, ln_pre);
       } else {
         const int xrw = p.x_row_words;
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int, int it, int kk, int bt) {
@@ -231,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         }, 1, gs, p.N, gs_valid);
       }
     } else if constexpr (kXS) {
-      c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane);
+      c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane, kSB, kXOff, ln_pre);
     } else {
       c.run(ring, hd, stages, s, phase, n_iters, sx, p.x_row_words, p.B, cw, lane);
     }
@@ -364,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (clog && threadIdx.x == 0) clog[5] = ptx::gtimer();
 }
 
-template <bool kInt8, int kNB8, bool kXS, bool kA16 = false>
+template <bool kInt8, int kNB8, int kXS, bool kA16 = false>
 void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pdl) {
   auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   cudaLaunchConfig_t cfg{};
@@ -389,7 +447,7 @@ void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pd
   DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
 }
 
-template <bool kInt8, int kNB8, bool kXS, bool kA16 = false>
+template <bool kInt8, int kNB8, int kXS, bool kA16 = false>
 void configure_one() {
   auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -417,7 +475,13 @@ int env_int(const char* name, int dflt) {
 }
 
 // Co-resident clusters of `split` CTAs for this kernel / smem (cached; 0 when unknown).
-const void* kernel_ptr(bool int8_weights, int nb8, bool xs, bool a16) {
+const void* kernel_ptr(bool int8_weights, int nb8, bool xs, bool a16, bool ln = false) {
+  if (ln) {
+    if (a16) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, 2, true>)
+                             : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, 2, true>);
+    return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<false, 1, 2, false>)
+                    : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, 2, false>);
+  }
   if (a16) {
     if (xs) return nb8 == 1 ? reinterpret_cast<const void*>(sbi_gemm_kernel<true, 1, true, true>)
                             : reinterpret_cast<const void*>(sbi_gemm_kernel<true, 2, true, true>);
@@ -436,14 +500,14 @@ const void* kernel_ptr(bool int8_weights, int nb8, bool xs, bool a16) {
                   : reinterpret_cast<const void*>(sbi_gemm_kernel<false, 2, false, false>);
 }
 
-int resident_clusters(bool int8_weights, int nb8, bool xs, bool a16, int split, size_t smem) {
+int resident_clusters(bool int8_weights, int nb8, bool xs, bool a16, int split, size_t smem, bool ln = false) {
   static std::mutex mu;
-  static std::map<std::tuple<bool, int, bool, bool, int, size_t>, int> cache;
-  const auto key = std::make_tuple(int8_weights, nb8, xs, a16, split, smem);
+  static std::map<std::tuple<bool, int, bool, bool, int, size_t, bool>, int> cache;
+  const auto key = std::make_tuple(int8_weights, nb8, xs, a16, split, smem, ln);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const void* kern = kernel_ptr(int8_weights, nb8, xs, a16);
+  const void* kern = kernel_ptr(int8_weights, nb8, xs, a16, ln);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1, split, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -492,6 +556,10 @@ void configure() {
   configure_one<true, 2, false, true>();
   configure_one<true, 1, true, true>();
   configure_one<true, 2, true, true>();
+  configure_one<false, 1, 2>();
+  configure_one<false, 2, 2>();
+  configure_one<true, 1, 2, true>();
+  configure_one<true, 2, 2, true>();
 }
 
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words) {
@@ -523,25 +591,33 @@ bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
 // splits K only when the output tiles alone cannot occupy the machine, but it sizes the split
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16) {
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16, bool ln_stream) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   if (a16 && !int8_weights) throw ConfigError("sbi_gemm: W8A16 needs int8 weights");
+  if (ln_stream && (!x_stream || (int8_weights && !a16)))
+    throw ConfigError("sbi_gemm: LayerNorm-streaming needs the x-streaming plan with fp16 or W8A16 weights");
   const int m = int8_weights ? 4 : 2;
   const int rows = (K + m - 1) / m;
   const int xw = a16 ? 2 : 1;  // x-slice words per packed row
   Plan pl{};
   pl.x_stream = x_stream ? 1 : 0;
+  pl.ln_stream = ln_stream ? 1 : 0;
   pl.a16 = a16 ? 1 : 0;
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
   const size_t x_budget = 64 * 1024;
-  const size_t stage_bytes = x_stream ? (a16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes;
+  const size_t stage_bytes = ln_stream ? (a16 ? kStageBytesLN16 : kStageBytesLN)
+                                       : (x_stream ? (a16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes);
   auto rps_for = [&](int s) {
     int r = (rows + s - 1) / s;
     return (r + kRowsPerStage - 1) / kRowsPerStage * kRowsPerStage;
   };
   // smem x slice of the non-streaming mode (the streaming mode keeps x in the ring stages)
-  auto x_bytes = [&](int rps) { return x_stream ? size_t{0} : static_cast<size_t>(B) * (xw * rps + 8) * 4; };
+  // (LayerNorm-streaming: the split's gamma and beta, fp16, in place of the slice)
+  auto x_bytes = [&](int rps) {
+    if (ln_stream) return static_cast<size_t>(2) * rps * m * 2;
+    return x_stream ? size_t{0} : static_cast<size_t>(B) * (xw * rps + 8) * 4;
+  };
   auto valid = [&](int s) {
     const int rps = rps_for(s);
     if ((rows + rps - 1) / rps != s) return false;  // no empty split
@@ -572,7 +648,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
     for (int s = 1; s <= 16; s <<= 1) {
       if (!valid(s)) continue;
       const int units = pl.col_tiles * s;
-      const int clusters = resident_clusters(int8_weights, pl.nb8, x_stream, a16, s, smem_for(s, nullptr));
+      const int clusters = resident_clusters(int8_weights, pl.nb8, x_stream, a16, s, smem_for(s, nullptr), ln_stream);
       int capacity = clusters > 0 ? clusters * s : 2 * 148;
       if (cap_per_sm > 0) capacity = std::min(capacity, cap_per_sm * 148);  // leave room for PDL overlap
       if (units <= capacity && units > best_units) {
@@ -609,7 +685,15 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   const bool xs = plan.x_stream != 0;
   const bool i8x = int8_weights && !plan.a16;  // int8 activations
   if (plan.a16 && p.pro != PRO_F16 && p.pro != PRO_LN) throw ConfigError("sbi_gemm: W8A16 takes fp16 x (PRO_F16 / PRO_LN)");
-  if (xs) {
+  if (plan.ln_stream) {
+    if (p.pro != PRO_LN || p.ln_stats_in == nullptr || p.res_in == nullptr || p.ln_g == nullptr || p.ln_b == nullptr)
+      throw ConfigError("sbi_gemm: LayerNorm-streaming needs PRO_LN with the producer's row sums");
+    if (p.K % 8 != 0 || p.res_delta != nullptr || p.res_out != nullptr)
+      throw ConfigError("sbi_gemm: LayerNorm-streaming takes a final residual row (K % 8 == 0)");
+    if ((reinterpret_cast<uintptr_t>(p.ln_g) & 15) != 0 || (reinterpret_cast<uintptr_t>(p.ln_b) & 15) != 0)
+      throw ConfigError("sbi_gemm: LayerNorm-streaming needs 16-byte aligned gamma / beta");
+    make_x_map(&p.xmap, p.res_in, p.K, p.B, p.K);  // fp32 residual [B][K] as 32-bit words
+  } else if (xs) {
     if (p.pro != (i8x ? PRO_I8 : PRO_F16))
       throw ConfigError("sbi_gemm: the x-streaming plan needs GEMM-ready x (fp16, or int8 for W8A8)");
     if (!x_streamable(p.x, p.x_ld, p.K, i8x)) throw ConfigError("sbi_gemm: x cannot be streamed (alignment)");
@@ -617,7 +701,13 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
     make_x_map(&p.xmap, p.x, plan.a16 ? 2 * p.rows : p.rows, p.B, p.x_ld / (i8x ? 4 : 2));
   }
 #define DSINF_LAUNCH(I8, NB, XS, A16) launch_impl<I8, NB, XS, A16>(p, plan, stream, pdl)
-  if (plan.a16) {
+  if (plan.ln_stream) {
+    if (plan.a16) {
+      if (plan.nb8 == 1) DSINF_LAUNCH(true, 1, 2, true); else DSINF_LAUNCH(true, 2, 2, true);
+    } else {
+      if (plan.nb8 == 1) DSINF_LAUNCH(false, 1, 2, false); else DSINF_LAUNCH(false, 2, 2, false);
+    }
+  } else if (plan.a16) {
     if (plan.nb8 == 1) {
       if (xs) DSINF_LAUNCH(true, 1, true, true); else DSINF_LAUNCH(true, 1, false, true);
     } else {

@@ -29,6 +29,12 @@ constexpr int kXBoxBytes = kMaxB * 128;                    // 2 KB (B rows x 128
 constexpr int kStageBytesXS = kStageBytes + kXBoxBytes;    // 18 KB, multiple of 1024
 // W8A16 x-streaming: int8 weight stages cover 128 k, i.e. two 32-word boxes of fp16 x pairs
 constexpr int kStageBytesXS16 = kStageBytes + 2 * kXBoxBytes;  // 20 KB
+// LayerNorm-streaming (Plan::ln_stream, TP = 1): each stage carries the fp32 RESIDUAL boxes of its k
+// range (32 floats x B rows per box: 2 for a 64-k fp16 stage, 4 for a 128-k int8 stage) and the
+// consumers normalise them into the fp16 x boxes of the same stage with the producer's row sums:
+// no row_prep launch between the residual-producing GEMM and the LayerNorm GEMM.
+constexpr int kStageBytesLN = kStageBytes + 2 * kXBoxBytes + kXBoxBytes;        // 22 KB
+constexpr int kStageBytesLN16 = kStageBytes + 4 * kXBoxBytes + 2 * kXBoxBytes;  // 28 KB
 
 // Row statistics handed from a producing epilogue to the next kernel's prologue (TP = 1 path):
 //   LayerNorm: per row, sum(y) and sum(y*y) in fixed point (int64; y * 2^32 and y^2 * 2^28,
@@ -134,6 +140,7 @@ struct Params {
 
 struct Plan {
   int x_stream;  // 1: x streamed per stage by TMA (PRO_F16 / PRO_I8 only), no smem x slice
+  int ln_stream;  // 1 (with x_stream): the residual is streamed and LayerNorm'd per stage (PRO_LN)
   int a16;       // W8A16 plan (int8 weights, fp16 x)
   int col_tiles;
   int ksplit;
@@ -148,7 +155,8 @@ struct Plan {
 void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 // Sets kernel attributes for every instantiation; call before graph capture.
 void configure();
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false, bool a16 = false);
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false, bool a16 = false,
+               bool ln_stream = false);
 // TMA descriptor of x for the x-streaming mode: `words` 32-bit words per row, `B` rows, row
 // stride ld_words (ld_words * 4 must be a multiple of 16 and x 16-byte aligned).
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words);

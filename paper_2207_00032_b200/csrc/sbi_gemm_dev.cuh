@@ -611,20 +611,27 @@ struct Consumer {
   // K-group scales (gs != nullptr): one int8 stage is one 128-k group; gs points at the group of
   // the first stage for this warp's 32 columns ([group][gs_ld] fp16, gs_valid columns readable),
   // and the weights dequantise to w = fp16(q * s_group) before the MMA (the row scale is then 1).
-  template <class XWord>
+  // `pre(s, it)` (optional) runs on every consumer thread right after stage s arrived, before its
+  // MMAs (the LayerNorm-streaming plan normalises the stage's residual boxes there).
+  struct NoPre {
+    __device__ __forceinline__ void operator()(int, int) const {}
+  };
+  template <class XWord, class Pre = NoPre>
   __device__ __forceinline__ void run_a16(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
                                           uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step = 1,
-                                          const __half* gs = nullptr, int gs_ld = 0, int gs_valid = 0) {
+                                          const __half* gs = nullptr, int gs_ld = 0, int gs_valid = 0, Pre pre = Pre()) {
     // two instantiations of the loop: the row-scale loop carries no group-scale registers
     if (gs == nullptr)
-      run_a16_loop<false>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid);
+      run_a16_loop<false>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid,
+                          pre);
     else
-      run_a16_loop<true>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid);
+      run_a16_loop<true>(ring, stage_bytes, hd, stages, s, phase, n_iters, cw, lane, xword, step, gs, gs_ld, gs_valid,
+                         pre);
   }
-  template <bool kGroups, class XWord>
+  template <bool kGroups, class XWord, class Pre>
   __device__ __forceinline__ void run_a16_loop(const uint8_t* ring, int stage_bytes, Header& hd, int stages, int& s,
                                                uint32_t& phase, int n_iters, int cw, int lane, XWord xword, int step,
-                                               const __half* gs, int gs_ld, int gs_valid) {
+                                               const __half* gs, int gs_ld, int gs_valid, Pre pre) {
     const uint8_t* wbox = ring + cw * kBoxBytes;
     __half2 gsc[2][2], gsn[2][2];
     auto load_gs = [&](int i, __half2 (&o)[2][2]) {
@@ -644,6 +651,7 @@ struct Consumer {
         if (it + 1 < n_iters) load_gs(it + 1, gsn);
       }
       ptx::mbar_wait(&hd.full[s], phase);
+      pre(s, it);
       const uint8_t* sw = wbox + s * stage_bytes;
 #pragma unroll
       for (int kk = 0; kk < kRowsPerStage / 4; ++kk) {
@@ -743,8 +751,10 @@ struct Consumer {
   }
   // x-streaming variant: stage s holds the 4 weight boxes then the x box (B rows x 128 B,
   // 128B-swizzled: 16-byte chunk c of row r sits at chunk c ^ (r & 7)).
+  template <class Pre = NoPre>
   __device__ __forceinline__ void run_xs(const uint8_t* ring, Header& hd, int stages, int& s, uint32_t& phase,
-                                         int n_iters, int B, int cw, int lane) {
+                                         int n_iters, int B, int cw, int lane, int stage_bytes = kStageBytesXS,
+                                         int x_off = kStageBytes, Pre pre = Pre()) {
     bool xvalid[kNB8];
     uint32_t xoff[kNB8][kRowsPerStage / 8];
 #pragma unroll
@@ -753,13 +763,14 @@ struct Consumer {
       xvalid[bt] = r < B;
 #pragma unroll
       for (int ks = 0; ks < kRowsPerStage / 8; ++ks)
-        xoff[bt][ks] = kStageBytes + r * 128 + (((2 * ks + (t >> 1)) ^ (r & 7)) << 4) + ((t & 1) << 3);
+        xoff[bt][ks] = x_off + r * 128 + (((2 * ks + (t >> 1)) ^ (r & 7)) << 4) + ((t & 1) << 3);
     }
     const uint8_t* wbox = ring + cw * kBoxBytes;
     for (int it = 0; it < n_iters; ++it) {
       ptx::mbar_wait(&hd.full[s], phase);
-      const uint8_t* stage = ring + s * kStageBytesXS;
-      const uint8_t* sw = wbox + s * kStageBytesXS;
+      pre(s, it);
+      const uint8_t* stage = ring + s * stage_bytes;
+      const uint8_t* sw = wbox + s * stage_bytes;
 #pragma unroll
       for (int ks = 0; ks < kRowsPerStage / 8; ++ks) {
         uint32_t b0[kNB8], b1[kNB8];

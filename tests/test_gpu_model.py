@@ -441,3 +441,34 @@ def test_attention_bulk_copy_variant(batch, d_heads, monkeypatch):
     head dims 128 and 64, contexts longer than one 32-row stage."""
     monkeypatch.setenv("DSINF_ATTN_TMA", "1")
     run_parity(512, 2, d_heads, 1000, batch=batch, prompt_len=40, gen=4, max_ctx=48)
+
+
+@pytest.mark.parametrize("dtype_bytes,batch,int8_act", [(2, 1, 0), (2, 16, 0), (1, 1, capi.INT8_W8A16),
+                                                         (1, 16, capi.INT8_AUTO)])
+def test_layernorm_streaming_plan(dtype_bytes, batch, int8_act, monkeypatch):
+    """LayerNorm-streaming (TP = 1): the LayerNorm GEMMs stream the fp32 residual with their weights
+    and normalise each stage in shared memory with the producer's row sums -- the row_prep launches
+    of Deep-Fusion regions 1 and 3 (and the LM head's) disappear.  Same LayerNorm expression as
+    row_prep: identical greedy tokens, logits equal to fp32 rounding, 2L + 1 fewer launches (fewer at
+    AUTO B=16, whose W8A8 QKV keeps its quantising row_prep); and against the oracle."""
+    rng = np.random.default_rng(31)
+    prompt = rng.integers(0, 1000, (batch, 6)).astype(np.int32)
+    outs, launches = [], []
+    for ls in ("0", "1"):
+        monkeypatch.setenv("DSINF_LN_STREAM", ls)
+        m = DecoderModel(512, 3, 8, 1000, dtype_bytes=dtype_bytes, batch=batch, max_ctx=24, seed=SEED,
+                         int8_act=int8_act)
+        m.set_prompt(prompt)
+        m.step(9)
+        torch.cuda.synchronize()
+        outs.append((m.full_logits(), m.read_tokens()[1]))
+        launches.append(m.get_info().kernels_per_step)
+        m.close()
+    (la, ha), (lb, hb) = outs
+    assert np.array_equal(ha, hb)
+    assert float(np.abs(la - lb).max()) <= 1e-3 * float(np.abs(la).max()) + 1e-4
+    fewer = 2 * 3 + 1 if not (dtype_bytes == 1 and batch == 16) else 3 + 1
+    assert launches[0] - launches[1] == fewer, launches
+    monkeypatch.setenv("DSINF_LN_STREAM", "1")
+    run_parity(512, 2, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, int8_act=int8_act,
+               oracle_int8_act=None if int8_act != capi.INT8_AUTO else (0x10f if batch <= 8 else 0x10e))
