@@ -1400,8 +1400,13 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       m->xs_od = rows16 && (m->q8() ? (od_v < 0 ? m->xs_ln : od_v != 0) : (od_v < 0 ? true : od_v != 0));
       const char* lm = std::getenv("DSINF_XS_LM");
       m->xs_lm = m->h % 8 == 0 && (lm ? std::atoi(lm) != 0 : true);
+      // default by batch (GPT-J, ms/token without -> with): fp16 B=1 2.678 -> 2.571, B=4 2.789 -> 2.647,
+      // B=8 2.893 -> 2.804, B=16 3.155 -> 3.496 (every column tile re-normalises the fp32 rows);
+      // W8A16 B=1 1.976 -> 1.910, B=4 2.083 -> 2.092, B=8 2.220 -> 2.417 (its consumers are the busier);
+      // GPT-2 B=1 fp16 1.797 -> 1.649, int8 1.658 -> 1.521.  DSINF_LN_STREAM=0/1 forces it.
       const char* lsv = std::getenv("DSINF_LN_STREAM");
-      m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : true);
+      const bool ls_default = m->int8 ? m->B <= 2 : m->B <= 8;
+      m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : ls_default);
       // fused all-reduce: on-device shards (DSINF_TP_LOCAL) or CUDA-IPC peer mappings across
       // processes; the per-CTA LayerNorm prologue path (slice plan) consumes the slots, the row_prep
       // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
