@@ -52,11 +52,14 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = p.stages;
-  constexpr int kSB = kLN ? (kA16 ? kStageBytesLN16 : kStageBytesLN)
-                          : (kXS ? (kA16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes);
   constexpr int kXBoxes = kA16 ? 2 : 1;           // fp16 x boxes per streamed stage
   constexpr int kRBoxes = kLN ? 2 * kXBoxes : 0;  // fp32 residual boxes per stage (LayerNorm-streaming)
-  constexpr int kXOff = kStageBytes + kRBoxes * kXBoxBytes;  // the x boxes within a stage
+  // activation box slot: kXBoxBytes (16 rows), or for LayerNorm-streaming 1 KB when B <= 8 (one
+  // 128B-swizzle atom), so the small-batch ring keeps 4 stages (p.box_bytes, set by launch)
+  const int kBoxSlot = kLN ? p.box_bytes : kXBoxBytes;
+  const int kSB = kLN ? kStageBytes + (kRBoxes + kXBoxes) * kBoxSlot
+                      : (kXS ? (kA16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes);
+  const int kXOff = kStageBytes + kRBoxes * kBoxSlot;  // the x boxes within a stage
   constexpr int kKPerRow = kInt8 ? 4 : 2;        // k per packed weight row
   uint8_t* ring = smem;
   Header& hd = *reinterpret_cast<Header*>(smem + stages * kSB);
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         if constexpr (kLN) {
 #pragma unroll
           for (int rb = 0; rb < kRBoxes; ++rb)
-            ptx::tma_load_2d(st + kStageBytes + rb * kXBoxBytes, &p.xmap, kKPerRow * r0 + rb * 32, 0,
+            ptx::tma_load_2d(st + kStageBytes + rb * kBoxSlot, &p.xmap, kKPerRow * r0 + rb * 32, 0,
                              &hd.full[it % stages], xpolicy);
         } else {
 #pragma unroll
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         for (int i = ctid; i < p.B * W; i += 128) {
           const int r = i / W, w = i - r * W;
           const int e = 2 * w, rb = e >> 5, ee = e & 31;
-          const float2 v = *reinterpret_cast<const float2*>(stg + kStageBytes + rb * kXBoxBytes + r * 128 +
+          const float2 v = *reinterpret_cast<const float2*>(stg + kStageBytes + rb * kBoxSlot + r * 128 +
                                                             (((ee >> 2) ^ (r & 7)) << 4) + (ee & 3) * 4);
           const __half2 g2 = *reinterpret_cast<const __half2*>(sg + kl0 + e);
           const __half2 b2 = *reinterpret_cast<const __half2*>(sb + kl0 + e);
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           const uint32_t word = dev::pack_h2((v.x - mean) * rstd * __low2float(g2) + __low2float(b2),
                                              (v.y - mean) * rstd * __high2float(g2) + __high2float(b2));
           const int xb = w >> 5, ww = w & 31;
-          *reinterpret_cast<uint32_t*>(stg + kXOff + xb * kXBoxBytes + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) +
+          *reinterpret_cast<uint32_t*>(stg + kXOff + xb * kBoxSlot + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) +
                                        (ww & 3) * 4) = word;
         }
         dev::consumer_bar();
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           const int r = bt * 8 + g;
           if (r >= p.B) return make_uint2(0u, 0u);
           const int w = 8 * kk + 2 * t, ww = w & 31;
-          const uint8_t* xb = ring + st * kSB + kXOff + (w >> 5) * kXBoxBytes;
+          const uint8_t* xb = ring + st * kSB + kXOff + (w >> 5) * kBoxSlot;
           return *reinterpret_cast<const uint2*>(xb + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) + (ww & 3) * 4);
         }, 1, gs, p.N, gs_valid, ln_pre);
       } else {
@@ -606,7 +609,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
   const size_t x_budget = 64 * 1024;
-  const size_t stage_bytes = ln_stream ? (a16 ? kStageBytesLN16 : kStageBytesLN)
+  const size_t stage_bytes = ln_stream ? kStageBytes + (a16 ? 6 : 3) * ln_box_bytes(B)
                                        : (x_stream ? (a16 ? kStageBytesXS16 : kStageBytesXS) : kStageBytes);
   auto rps_for = [&](int s) {
     int r = (rows + s - 1) / s;
@@ -693,6 +696,7 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
     if ((reinterpret_cast<uintptr_t>(p.ln_g) & 15) != 0 || (reinterpret_cast<uintptr_t>(p.ln_b) & 15) != 0)
       throw ConfigError("sbi_gemm: LayerNorm-streaming needs 16-byte aligned gamma / beta");
     make_x_map(&p.xmap, p.res_in, p.K, p.B, p.K);  // fp32 residual [B][K] as 32-bit words
+    p.box_bytes = ln_box_bytes(p.B);
   } else if (xs) {
     if (p.pro != (i8x ? PRO_I8 : PRO_F16))
       throw ConfigError("sbi_gemm: the x-streaming plan needs GEMM-ready x (fp16, or int8 for W8A8)");

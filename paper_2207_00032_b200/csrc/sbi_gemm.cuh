@@ -33,8 +33,9 @@ constexpr int kStageBytesXS16 = kStageBytes + 2 * kXBoxBytes;  // 20 KB
 // range (32 floats x B rows per box: 2 for a 64-k fp16 stage, 4 for a 128-k int8 stage) and the
 // consumers normalise them into the fp16 x boxes of the same stage with the producer's row sums:
 // no row_prep launch between the residual-producing GEMM and the LayerNorm GEMM.
-constexpr int kStageBytesLN = kStageBytes + 2 * kXBoxBytes + kXBoxBytes;        // 22 KB
-constexpr int kStageBytesLN16 = kStageBytes + 4 * kXBoxBytes + 2 * kXBoxBytes;  // 28 KB
+// Box slots: 1 KB (one 128B-swizzle atom) for B <= 8, else kXBoxBytes; stage = 16 KB + 3 slots
+// (fp16: 2 residual + 1 x) or 6 slots (W8A16: 4 + 2).
+inline int ln_box_bytes(int B) { return B <= 8 ? 1024 : kXBoxBytes; }
 
 // Row statistics handed from a producing epilogue to the next kernel's prologue (TP = 1 path):
 //   LayerNorm: per row, sum(y) and sum(y*y) in fixed point (int64; y * 2^32 and y^2 * 2^28,
@@ -86,6 +87,7 @@ struct Params {
   int rows_per_split;    // multiple of kRowsPerStage; split s covers [s*rps, (s+1)*rps)
   int stages;
   int x_row_words;       // smem stride of one x row (== 8 mod 32)
+  int box_bytes;         // LayerNorm-streaming: smem slot of one activation box (set by launch)
   // prologue
   int pro;
   int a16;               // int8 weights with fp16 x (W8A16, weight-only): fp32 accumulate, y = acc * w_scale
