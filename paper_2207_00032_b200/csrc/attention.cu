@@ -3,6 +3,7 @@
 //
 // One thread-block cluster per (batch row, head); its `C` CTAs split the context into chunks
 // (attn_dev.cuh) and merge their (max, sum, output) partials through distributed shared memory.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -283,13 +284,17 @@ size_t tma_smem_bytes(int d) {
 
 int attention_chunks(int B, int H) {
   // enough CTAs for the KV stream's memory parallelism: (batch, head) pairs x chunks >= target
-  static const int target = [] {
+  const int target = [] {  // read per model (DSINF_ATTN_CTAS)
     const char* v = std::getenv("DSINF_ATTN_CTAS");
     return v ? std::atoi(v) : 2 * 148;
   }();
+  const int max_c = [] {
+    const char* v = std::getenv("DSINF_ATTN_MAXC");
+    return v ? std::max(1, std::min(16, std::atoi(v))) : 8;
+  }();
   const int pairs = B * H;
   int c = 1;
-  while (c < 8 && pairs * c < target) c <<= 1;
+  while (c < max_c && pairs * c < target) c <<= 1;
   return c;
 }
 
@@ -325,10 +330,10 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
   if (p.d % 8 != 0 || p.d > 256) throw ConfigError("attention: head dim must be a multiple of 8 and <= 256");
   if (chunks < 1 || chunks > 16) throw ConfigError("attention: bad chunk count");
   const dim3 grid(p.H, p.B, chunks), block(kAttnThreads), cluster(1, 1, chunks);
-  // DSINF_ATTN_TMA=1: the bulk-copy K/V ring variant (16-byte aligned rows: d % 8 == 0).  Parity-
-  // tested; measured equal or slightly slower in the step (GPT-J in-step attention int8 B=16
-  // 11.7 -> 12.2 us, fp16 B=1 step 2.678 -> 2.713 ms), so the per-thread pipelined loads stay default
-  const int tma = [] { const char* v = std::getenv("DSINF_ATTN_TMA"); return v ? std::atoi(v) : 0; }();  // read per enqueue
+  // the bulk-copy K/V ring variant (16-byte aligned rows: d % 8 == 0), default; DSINF_ATTN_TMA=0 selects
+  // the per-thread pipelined loads.  GPT-J ms/token (per-thread -> bulk): int8 B=1 1.893 -> 1.867,
+  // B=8 2.209 -> 2.190; fp16 B=1 2.564 -> 2.554, B=16 3.137 -> 3.123; GPT-2 B=1 fp16 1.650 -> 1.626
+  const int tma = [] { const char* v = std::getenv("DSINF_ATTN_TMA"); return v ? std::atoi(v) : 1; }();  // read per enqueue
   if (tma && (reinterpret_cast<uintptr_t>(p.kc) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.vc) & 15) == 0) {
     p.kv_rows_cap = 0;
     if (p.d <= 64)
@@ -339,9 +344,9 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
       launch_pdl(attention_tma_kernel<32>, grid, block, tma_smem_bytes<32>(p.d), s, pdl, p, cluster);
     return;
   }
-  // DSINF_ATTN_PREFETCH=1: K/V staging before the dependency wait (a chunk's rows at the largest
-  // context must fit a 48 KB budget).  Measured slower and off by default: GPT-J B=1 int8 2.062 ->
-  // 2.100 ms, fp16 2.671 -> 2.706; with attention PDL-launched (DSINF_PDL_MASK=0x8f) 2.150 / 2.691
+  // DSINF_ATTN_PREFETCH=1 (with DSINF_ATTN_TMA=0): K/V staging before the dependency wait (a chunk's
+  // rows at the largest context must fit a 48 KB budget).  Measured slower and off by default: GPT-J
+  // B=1 int8 1.929 -> 1.944 ms, fp16 2.564 -> 2.589
   const int pre = [] { const char* v = std::getenv("DSINF_ATTN_PREFETCH"); return v ? std::atoi(v) : 0; }();
   const int rows_cap = (p.max_seq + chunks - 1) / chunks;
   const size_t kv_bytes = static_cast<size_t>(2) * rows_cap * p.d * 2;
