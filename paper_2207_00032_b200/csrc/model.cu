@@ -261,7 +261,9 @@ ops::ShardMap tensor_map(int64_t h, int64_t H, int64_t V, int t, int r, uint64_t
 }
 
 // Allocates and generates one GEMM weight in the packed layout (fp16 M=2 or int8 M=4).
-uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaStream_t s, __half** gscales = nullptr) {
+// biased: int8 bytes stored as s + 128 for the W8A16 GEMMs (gemm::Plan::a16 == 2)
+uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaStream_t s, __half** gscales = nullptr,
+                      bool biased = false) {
   const int M = m.int8 ? 4 : 2;
   const int64_t words = (map.K_local + M - 1) / M * map.N_local;
   uint32_t* w = m.alloc_n<uint32_t>(words);
@@ -271,11 +273,11 @@ uint32_t* make_weight(Model& m, const ops::ShardMap& map, float** scales, cudaSt
     *gscales = m.alloc_n<__half>(ng);
     m.weight_bytes += ng * 2;
     *scales = nullptr;
-    ops::init_packed_i8_groups(map, w, *gscales, s);
+    ops::init_packed_i8_groups(map, w, *gscales, s, biased);
   } else if (m.int8) {
     *scales = m.alloc_n<float>(map.N_local);
     m.weight_bytes += map.N_local * 4;
-    ops::init_packed_i8(map, w, *scales, s);
+    ops::init_packed_i8(map, w, *scales, s, biased);
   } else {
     *scales = nullptr;
     ops::init_packed_f16(map, w, s);
@@ -302,13 +304,13 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
       tensor_amp(tensor, &off);
       return make_vec(m, map(tensor), off, s);
     };
-    w.wqkv = make_weight(m, map(DSINF_T_QKV), &w.sqkv, s, &w.gqkv);
+    w.wqkv = make_weight(m, map(DSINF_T_QKV), &w.sqkv, s, &w.gqkv, m.a16g(0));
     w.bqkv = vec(DSINF_T_QKV_BIAS);
-    w.wo = make_weight(m, map(DSINF_T_O), &w.so, s, &w.go);
+    w.wo = make_weight(m, map(DSINF_T_O), &w.so, s, &w.go, m.a16g(1));
     w.bo = vec(DSINF_T_O_BIAS);
-    w.wup = make_weight(m, map(DSINF_T_UP), &w.sup, s, &w.gup);
+    w.wup = make_weight(m, map(DSINF_T_UP), &w.sup, s, &w.gup, m.a16g(2));
     w.bup = vec(DSINF_T_UP_BIAS);
-    w.wdown = make_weight(m, map(DSINF_T_DOWN), &w.sdown, s, &w.gdown);
+    w.wdown = make_weight(m, map(DSINF_T_DOWN), &w.sdown, s, &w.gdown, m.a16g(3));
     w.bdown = vec(DSINF_T_DOWN_BIAS);
     w.ln1g = vec(DSINF_T_LN1_G);
     w.ln1b = vec(DSINF_T_LN1_B);
@@ -360,10 +362,13 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
   const bool i8 = m.int8;
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
-                                m.ln_use(0));
-  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1));
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2));
-  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3));
+                                m.ln_use(0), m.a16g(0));
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1), false,
+                              m.a16g(1));
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2),
+                               m.a16g(2));
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3), false,
+                                 m.a16g(3));
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm, false,
                                m.ln_stream && m.xs_lm);
 }
@@ -1014,10 +1019,11 @@ struct Enqueuer {
         if (!sh.rm_per_layer) continue;
         const LayerW& w = sh.layers[l];
         const int64_t pm = m.int8 ? 4 : 2, h64 = m.h;
-        ops::packed_to_rowmajor(w.wqkv, h64 / pm, 3 * m.Hl * m.d, static_cast<uint32_t*>(w.rqkv), s);
-        ops::packed_to_rowmajor(w.wo, m.Hl * m.d / pm, h64, static_cast<uint32_t*>(w.ro), s);
-        ops::packed_to_rowmajor(w.wup, h64 / pm, m.Fl, static_cast<uint32_t*>(w.rup), s);
-        ops::packed_to_rowmajor(w.wdown, m.Fl / pm, h64, static_cast<uint32_t*>(w.rdown), s);
+        auto unbias = [&](int g) { return m.a16g(g) ? 0x80808080u : 0u; };  // W8A16 weights are stored biased
+        ops::packed_to_rowmajor(w.wqkv, h64 / pm, 3 * m.Hl * m.d, static_cast<uint32_t*>(w.rqkv), s, unbias(0));
+        ops::packed_to_rowmajor(w.wo, m.Hl * m.d / pm, h64, static_cast<uint32_t*>(w.ro), s, unbias(1));
+        ops::packed_to_rowmajor(w.wup, h64 / pm, m.Fl, static_cast<uint32_t*>(w.rup), s, unbias(2));
+        ops::packed_to_rowmajor(w.wdown, m.Fl / pm, h64, static_cast<uint32_t*>(w.rdown), s, unbias(3));
         launches += 4;
       }
       for (Shard& sh : m.shards) {

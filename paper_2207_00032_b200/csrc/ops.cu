@@ -68,7 +68,7 @@ __device__ __forceinline__ uint32_t q8(float x, float scale) {
   return static_cast<uint32_t>(q) & 0xffu;
 }
 
-__global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t* packed) {
+__global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t* packed, uint32_t bias) {
   const int64_t rows = (m.K_local + 3) / 4;
   const int64_t total = rows * m.N_local;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -81,14 +81,14 @@ __global__ void init_packed_i8_kernel(ShardMap m, const float* scales, uint32_t*
       const int64_t k = 4 * r + e;
       if (k < m.K_local) word |= q8(synth_value(m, grow, m.col_off + k), s) << (8 * e);
     }
-    packed[i] = word;
+    packed[i] = word ^ bias;
   }
 }
 
 // The same synthetic tensor quantised per (global output row, 128-k group) (K_local and col_off
 // multiples of 128, so a group never straddles TP shards): fp16 scale s = fp16(max|w| / 127), q =
 // clamp(rint(w / s)); one warp per (row, group), lane l owns packed word l of the group.
-__global__ void init_packed_i8_groups_kernel(ShardMap m, uint32_t* packed, __half* gscales) {
+__global__ void init_packed_i8_groups_kernel(ShardMap m, uint32_t* packed, __half* gscales, uint32_t bias) {
   const int64_t G = m.K_local / kI8Group;
   const int warps = blockDim.x / 32;
   const int lane = threadIdx.x & 31;
@@ -111,7 +111,7 @@ __global__ void init_packed_i8_groups_kernel(ShardMap m, uint32_t* packed, __hal
     uint32_t word = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) word |= q8(v[e], sc) << (8 * e);
-    packed[(k0 / 4) * m.N_local + n] = word;
+    packed[(k0 / 4) * m.N_local + n] = word ^ bias;
     if (lane == 0) gscales[g * m.N_local + n] = sh;
   }
 }
@@ -668,19 +668,20 @@ void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s) {
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 
-void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s) {
+void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s, bool biased) {
   init_row_scale_kernel<<<blocks_for(m.N_local, 8, 148 * 8), 256, 0, s>>>(m, scales);
   DSINF_CUDA_CHECK(cudaGetLastError());
   const int64_t total = (m.K_local + 3) / 4 * m.N_local;
-  init_packed_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, scales, packed);
+  init_packed_i8_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, scales, packed, biased ? 0x80808080u : 0u);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 
-void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s) {
+void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s, bool biased) {
   if (m.K_local % kI8Group != 0 || m.col_off % kI8Group != 0)
     throw ConfigError("K-group INT8 weights need per-rank in_dim (and shard offsets) multiples of 128");
   const int64_t units = m.N_local * (m.K_local / kI8Group);
-  init_packed_i8_groups_kernel<<<blocks_for(units, 8, 148 * 16), 256, 0, s>>>(m, packed, gscales);
+  init_packed_i8_groups_kernel<<<blocks_for(units, 8, 148 * 16), 256, 0, s>>>(m, packed, gscales,
+                                                                            biased ? 0x80808080u : 0u);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -719,7 +720,7 @@ void quantize_weights_i8(const __half* w, int64_t N, int64_t K, int8_t* packed, 
 }
 
 __global__ void word_transpose_kernel(const uint32_t* __restrict__ in, int64_t rows, int64_t N,
-                                      uint32_t* __restrict__ out) {
+                                      uint32_t* __restrict__ out, uint32_t xor_mask) {
   __shared__ uint32_t tile[32][33];
   const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -729,14 +730,15 @@ __global__ void word_transpose_kernel(const uint32_t* __restrict__ in, int64_t r
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t n = n0 + i, r = r0 + threadIdx.x;
-    if (n < N && r < rows) out[n * rows + r] = tile[threadIdx.x][i];
+    if (n < N && r < rows) out[n * rows + r] = tile[threadIdx.x][i] ^ xor_mask;
   }
 }
 
-void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s) {
+void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s,
+                        uint32_t xor_mask) {
   if (rows >= (1LL << 31) / 32 * 32 || N >= (1LL << 31) / 32 * 32) throw ConfigError("packed_to_rowmajor: too large");
   const dim3 grid(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
-  word_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(packed, rows, N, out);
+  word_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(packed, rows, N, out, xor_mask);
   DSINF_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -25,16 +25,19 @@ struct ShardMap {
 // Synthetic weight tensor written in the reference packed layout, fp16, pack_M = 2.
 void init_packed_f16(const ShardMap& m, uint32_t* packed, cudaStream_t s);
 // Same tensor quantised per global output row to int8 (pack_M = 4) + fp32 row scales.
-void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s);
+// biased: bytes stored as s + 128 (XOR 0x80), the W8A16 decode GEMMs' layout (no XOR when widening)
+void init_packed_i8(const ShardMap& m, uint32_t* packed, float* scales, cudaStream_t s, bool biased = false);
 // Same tensor quantised per (global row, 128-k group): fp16 scales [K_local/128][N_local].
-void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s);
+void init_packed_i8_groups(const ShardMap& m, uint32_t* packed, __half* gscales, cudaStream_t s, bool biased = false);
 // Row-major [N_local][K_local] copy of the same tensor for the tensor-core path: fp16, or int8
 // quantised with the given (packed-layout) row scales.
 void init_rowmajor_map_f16(const ShardMap& m, __half* out, cudaStream_t s);
 // Packed decode weights -> the row-major [N][K] operand of the tensor-core prefill: both layouts
 // are 32-bit words (pack_M consecutive k of one output row), so this is the word transpose
 // [rows][N] -> [N][rows] (rows = K / pack_M, K % pack_M == 0), smem-tiled, coalesced both ways.
-void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s);
+// xor_mask 0x80808080 un-biases W8A16-biased int8 words.
+void packed_to_rowmajor(const uint32_t* packed, int64_t rows, int64_t N, uint32_t* out, cudaStream_t s,
+                        uint32_t xor_mask = 0);
 void init_rowmajor_map_i8(const ShardMap& m, const float* scales, int8_t* out, cudaStream_t s);
 // 1-D tensor (bias / LN) of length n_local: value = offset + unit(flat = row(n)) * amp.
 void init_vector_f16(const ShardMap& m, float offset, __half* out, cudaStream_t s);

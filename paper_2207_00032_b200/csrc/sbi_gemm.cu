@@ -44,7 +44,7 @@ using dev::Header;
 // 128-k stage when streamed), weights widened in registers, fp32 accumulate, y = acc * w_scale.
 // kXS: 0 smem x slice, 1 x-streaming, 2 LayerNorm-streaming (fp32 residual boxes per stage,
 // normalised by the consumers into the stage's fp16 x boxes; fp16 or W8A16 weights).
-template <bool kInt8, int kNB8, int kXS, bool kA16>
+template <bool kInt8, int kNB8, int kXS, int kA16>
 __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
   static_assert(!kA16 || kInt8, "W8A16 needs int8 weights");
   constexpr bool kLN = kXS == 2;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (clog && threadIdx.x == 0) clog[5] = ptx::gtimer();
 }
 
-template <bool kInt8, int kNB8, int kXS, bool kA16 = false>
+template <bool kInt8, int kNB8, int kXS, int kA16 = 0>
 void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pdl) {
   auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   cudaLaunchConfig_t cfg{};
@@ -450,7 +450,7 @@ void launch_impl(const Params& p, const Plan& plan, cudaStream_t stream, bool pd
   DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
 }
 
-template <bool kInt8, int kNB8, int kXS, bool kA16 = false>
+template <bool kInt8, int kNB8, int kXS, int kA16 = 0>
 void configure_one() {
   auto kern = sbi_gemm_kernel<kInt8, kNB8, kXS, kA16>;
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -563,6 +563,13 @@ void configure() {
   configure_one<false, 2, 2>();
   configure_one<true, 1, 2, true>();
   configure_one<true, 2, 2, true>();
+  // biased-weight W8A16 (the decode model's weights)
+  configure_one<true, 1, 0, 2>();
+  configure_one<true, 2, 0, 2>();
+  configure_one<true, 1, 1, 2>();
+  configure_one<true, 2, 1, 2>();
+  configure_one<true, 1, 2, 2>();
+  configure_one<true, 2, 2, 2>();
 }
 
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words) {
@@ -594,7 +601,8 @@ bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
 // splits K only when the output tiles alone cannot occupy the machine, but it sizes the split
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
-Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16, bool ln_stream) {
+Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16, bool ln_stream,
+               bool a16_biased) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   if (a16 && !int8_weights) throw ConfigError("sbi_gemm: W8A16 needs int8 weights");
   if (ln_stream && (!x_stream || (int8_weights && !a16)))
@@ -605,7 +613,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   Plan pl{};
   pl.x_stream = x_stream ? 1 : 0;
   pl.ln_stream = ln_stream ? 1 : 0;
-  pl.a16 = a16 ? 1 : 0;
+  pl.a16 = a16 ? (a16_biased ? 2 : 1) : 0;
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
   const size_t x_budget = 64 * 1024;
@@ -707,7 +715,14 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
     make_x_map(&p.xmap, p.x, plan.a16 ? 2 * p.rows : p.rows, p.B, p.x_ld / (i8x ? 4 : 2));
   }
 #define DSINF_LAUNCH(I8, NB, XS, A16) launch_impl<I8, NB, XS, A16>(p, plan, stream, pdl)
-  if (plan.ln_stream) {
+  if (plan.a16 == 2) {  // biased-weight W8A16
+    const int x = plan.ln_stream ? 2 : (xs ? 1 : 0);
+    if (plan.nb8 == 1) {
+      if (x == 2) DSINF_LAUNCH(true, 1, 2, 2); else if (x == 1) DSINF_LAUNCH(true, 1, 1, 2); else DSINF_LAUNCH(true, 1, 0, 2);
+    } else {
+      if (x == 2) DSINF_LAUNCH(true, 2, 2, 2); else if (x == 1) DSINF_LAUNCH(true, 2, 1, 2); else DSINF_LAUNCH(true, 2, 0, 2);
+    }
+  } else if (plan.ln_stream) {
     if (plan.a16) {
       if (plan.nb8 == 1) DSINF_LAUNCH(true, 1, 2, true); else DSINF_LAUNCH(true, 2, 2, true);
     } else {

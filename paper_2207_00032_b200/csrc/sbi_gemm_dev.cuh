@@ -562,8 +562,11 @@ __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cas
 
 // int8 x4 (one packed weight word: 4 consecutive k) -> two fp16 pairs, exact:
 // bytes (s + 128) under a 0x64 exponent byte are 1024 + s + 128 in fp16; subtract 1152.
+// kBiased: the word already holds the biased bytes s + 128 (the decode model's W8A16 weights are
+// stored that way, packed_weights_bias), which saves the XOR -- one of five widening instructions.
+template <bool kBiased = false>
 __device__ __forceinline__ void i8x4_to_h2x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
-  const uint32_t u = w ^ 0x80808080u;
+  const uint32_t u = kBiased ? w : (w ^ 0x80808080u);
   const uint32_t l = __byte_perm(u, 0x64646464u, 0x4140);
   const uint32_t h = __byte_perm(u, 0x64646464u, 0x4342);
   const __half2 bias = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
@@ -582,7 +585,8 @@ __device__ __forceinline__ void i8x4_to_h2x2(uint32_t w, uint32_t& lo, uint32_t&
 // multiplied by fp16 x with mma.m16n8k16 (fp32 accumulate).  Per 16-k step thread t owns packed
 // row 4*kk + t (4 consecutive k): weight word -> (a0, a2) / (a1, a3), x word pair 2*(4kk + t)
 // -> (b0, b1), the same k assignment on both operands.
-template <bool kInt8, int kNB8, bool kA16 = false>
+// kA16: 0 = not W8A16; 1 = W8A16 over signed int8 words; 2 = W8A16 over biased (s + 128) words.
+template <bool kInt8, int kNB8, int kA16 = 0>
 struct Consumer {
   using Acc = typename std::conditional<kInt8 && !kA16, int, float>::type;
   Acc acc[2][kNB8][4];
@@ -664,8 +668,8 @@ struct Consumer {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           uint32_t a0, a1, a2, a3;
-          i8x4_to_h2x2(wq[2 * j], a0, a2);
-          i8x4_to_h2x2(wq[2 * j + 1], a1, a3);
+          i8x4_to_h2x2<kA16 == 2>(wq[2 * j], a0, a2);
+          i8x4_to_h2x2<kA16 == 2>(wq[2 * j + 1], a1, a3);
           if constexpr (kGroups) {
             a0 = h2_bits(__hmul2(bits_h2(a0), gsc[j][0]));
             a2 = h2_bits(__hmul2(bits_h2(a2), gsc[j][0]));

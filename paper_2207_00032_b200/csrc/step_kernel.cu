@@ -623,7 +623,7 @@ __device__ void gemm_phase(const Prog& P, const Phase& f, int p, unsigned epoch,
   if (full_x) all_bar();
   if (full_x && lead) trace_rec(P, cta, p, 5);
   const int cap = full_x ? f.spt : P.x_cap / (kRowsPerStage * f.xw);  // stages per x chunk
-  using Cons = gemm::dev::Consumer<kA16, kNB8, kA16>;
+  using Cons = gemm::dev::Consumer<kA16, kNB8, kA16 ? 2 : 0>;  // the model's W8A16 weights are biased
   Cons c;
   c.init(lane);
   for (int i = a; i < e;) {
