@@ -311,6 +311,9 @@ def workload_config(args, preset, world):
     cfg = {"workload": f"{preset.name} {args.dtype} greedy decode, batch {args.batch}, {args.prompt}-token prompt, "
                        f"TP={world}", "model": args.config, "global_batch": args.batch, "seq_len": args.prompt,
            "parallelism": f"tp{world}", "l2": "weights per step (GB) >> 126 MB L2; no flush needed"}
+    if world > 1:
+        cfg["collectives"] = ("all-reduces fused into the row-parallel GEMM epilogues over CUDA-IPC peer memory "
+                              "(DSINF_TP_IPC)" if args.tp_mode == "ipc" else "NCCL all-reduce / all-gather launches")
     if args.dtype == "int8":
         cfg["int8_act"] = auto_act(args.batch, world) if args.int8_act == "auto" else args.int8_act
         cfg["int8_scales"] = "K-group 128 (fp16)" if args.int8_group else "per output row (fp32)"
@@ -505,16 +508,30 @@ def run_ours(args, preset, rank, world, local_rank):
     from paper_2207_00032_b200 import _capi as capi
     from paper_2207_00032_b200 import engine as E
 
+    local_rank = local_rank % max(1, torch.cuda.device_count())  # ranks may share a GPU (functional runs)
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.Stream()
     peak_gbs, peak_kind = measured_peaks()
     dtype_bytes = 1 if args.dtype == "int8" else 2
     comm = None
-    if world > 1:
+    ipc_exchange = None
+    tp_mode = capi.TP_NONE
+    if world > 1 and args.tp_mode == "ipc":
+        # the fused all-reduce over CUDA-IPC peer memory (DSINF_TP_IPC): handles all-gathered over gloo
+        import torch.distributed as dist
+
+        def ipc_exchange(blob):
+            lst = [None] * world
+            dist.all_gather_object(lst, blob)
+            return lst
+
+        tp_mode = capi.TP_IPC
+    elif world > 1:
         import ctypes as C
 
         import torch.distributed as dist
 
+        tp_mode = capi.TP_NCCL
         uid = (C.c_uint8 * 128)()
         if rank == 0:
             capi.check(capi.lib.dsinf_nccl_get_unique_id(uid))
@@ -527,7 +544,7 @@ def run_ours(args, preset, rank, world, local_rank):
     max_ctx = args.prompt + 2 * (args.warmup + args.steps) + 8
     model = E.DecoderModel(preset.hidden, preset.layers, preset.heads, preset.vocab, dtype_bytes=dtype_bytes,
                            batch=args.batch, max_ctx=max_ctx, tp_size=world, tp_rank=rank,
-                           tp_mode=capi.TP_NCCL if world > 1 else capi.TP_NONE, nccl_comm=comm,
+                           tp_mode=tp_mode, nccl_comm=comm, ipc_exchange=ipc_exchange,
                            use_cuda_graph=not args.no_graph, use_pdl=not args.no_pdl, seed=SEED, device=local_rank,
                            int8_act={"w8a8": capi.INT8_W8A8, "w8a16": capi.INT8_W8A16, "auto": capi.INT8_AUTO}[args.int8_act],
                            int8_group=args.int8_group if args.dtype == "int8" else 0)
@@ -748,6 +765,9 @@ def main():
     ap.add_argument("--int8-group", type=int, choices=[0, 128], default=0,
                     help="int8: 128 = K-group weight scales (weight-only GEMMs, per-group dequant; the prompt goes "
                          "through the decode step)")
+    ap.add_argument("--tp-mode", choices=["ipc", "nccl"], default="ipc",
+                    help="N > 1: all-reduces fused into the GEMM epilogues over CUDA-IPC peer memory (default), "
+                         "or NCCL all-reduce launches between the GEMMs")
     ap.add_argument("--no-tp-slices", action="store_true", help="skip the per-rank TP slice measurements")
     ap.add_argument("--token-prefill", action="store_true", help="prefill the prompt through the decode step graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for cpu_baseline")
