@@ -56,6 +56,7 @@ struct LayerW {
   uint32_t* wdown = nullptr;
   float* sdown = nullptr;
   __half* bdown = nullptr;
+  unsigned* up_flags = nullptr;  // DSINF_DOWN_FLAGS: [L][MLP-up column tiles] completion counters (monotonic)
   // int8 K-group scales (dsinf_runtime_config.int8_group = 128): fp16 [K_local/128][N_local]
   __half *gqkv = nullptr, *go = nullptr, *gup = nullptr, *gdown = nullptr;
   // row-major [N][K] copies for the tensor-core prefill (fp16, or int8 with the scales above);
@@ -170,6 +171,10 @@ struct dsinf_model {
   // LayerNorm GEMMs stream the fp32 residual and normalise it per stage -- no row_prep launch.
   // Not for W8A8 GEMMs (their per-token scale needs the whole normalised row).  DSINF_LN_STREAM=0: off
   bool ln_stream = false;
+  // DSINF_DOWN_FLAGS=1 (TP = 1, x-streamed fp16 / W8A16 MLP-down): MLP-down is PDL-launched and its
+  // producer waits only for the MLP-up column tiles of its k range (per-tile counters) instead of
+  // the whole MLP-up grid; its epilogue still waits for the grid
+  bool down_flags = false;
   bool ln_use(int g) const { return ln_stream && !q8g(g); }  // g: 0 QKV, 2 MLP-up, 4 LM head (fp16)
   unsigned long long* ltrace = nullptr;
   std::vector<int> ltrace_kinds;  // DSINF_LAUNCH_TRACE: [2][ptx::kTraceEnd] start / end stamps
@@ -369,6 +374,12 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
                                m.a16g(2));
   sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3), false,
                                  m.a16g(3));
+  if (m.down_flags) {
+    for (LayerW& w : sh.layers) {
+      w.up_flags = m.alloc_n<unsigned>(sh.plan_up.col_tiles);
+      DSINF_CUDA_CHECK(cudaMemsetAsync(w.up_flags, 0, sizeof(unsigned) * sh.plan_up.col_tiles, s));
+    }
+  }
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm, false,
                                m.ln_stream && m.xs_lm);
 }
@@ -696,13 +707,14 @@ struct Enqueuer {
   long long* lnslot(Shard& sh, int i) const { return sh.lnstats ? sh.lnstats + static_cast<int64_t>(i) * gemm::kLnSlotWords : nullptr; }
   unsigned* amslot(Shard& sh, int i) const { return sh.amax ? sh.amax + static_cast<int64_t>(i) * gemm::kAmaxSlotWords : nullptr; }
 
-  void gemm_launch(const gemm::Params& p_in, const gemm::Plan& plan, bool int8_w, int bit) {
+  void gemm_launch(const gemm::Params& p_in, const gemm::Plan& plan, bool int8_w, int bit, bool force_pdl = false) {
     gemm::Params p = p_in;
     p.trace = tslot(bit == 0 ? DSINF_LK_QKV : bit == 2 ? DSINF_LK_O : bit == 3 ? DSINF_LK_UP : bit == 4 ? DSINF_LK_DOWN
                                                                                                   : DSINF_LK_LM);
     if (m.cta_log && gemm_index++ == m.cta_log_launch) p.cta_log = m.cta_log;
-    pdl_launches += P(bit);
-    gemm::launch(p, plan, int8_w, s, P(bit));
+    const bool pl = P(bit) || (force_pdl && pdl);
+    pdl_launches += pl;
+    gemm::launch(p, plan, int8_w, s, pl);
     ++launches;
   }
 
@@ -833,6 +845,7 @@ struct Enqueuer {
     p.epi = gemm::EPI_GELU_F16;
     p.bias = w.bup;
     p.out = sh.u;
+    p.out_flags = w.up_flags;
     p.amax_out = amslot(sh, 2 * l + 1);
     gemm_launch(p, sh.plan_up, m.int8, 3);
   }
@@ -861,7 +874,14 @@ struct Enqueuer {
       p.out = sh.d_mlp;
       if (m.fused_ar) push_to_all(sh, p, 1, l);
     }
-    gemm_launch(p, sh.plan_down, m.int8, 4);
+    if (w.up_flags != nullptr) {
+      p.dep_flags = w.up_flags;
+      p.dep_per_step = static_cast<unsigned>(sh.plan_up.ksplit);
+      p.dep_step = m.step_ctr;
+      gemm_launch(p, sh.plan_down, m.int8, 4, /*force_pdl=*/true);
+    } else {
+      gemm_launch(p, sh.plan_down, m.int8, 4);
+    }
   }
 
   // complete_res: res[0] already holds the final residual (prefill); else the decode step's last
@@ -1411,6 +1431,8 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // W8A16 B=1 1.976 -> 1.910, B=4 2.083 -> 2.092, B=8 2.220 -> 2.417 (its consumers are the busier);
       // GPT-2 B=1 fp16 1.797 -> 1.649, int8 1.658 -> 1.521.  DSINF_LN_STREAM=0/1 forces it.
       const char* lsv = std::getenv("DSINF_LN_STREAM");
+      const char* dfv = std::getenv("DSINF_DOWN_FLAGS");
+      m->down_flags = m->t == 1 && m->xs_od && !m->q8g(3) && dfv != nullptr && std::atoi(dfv) != 0;
       const bool ls_default = m->int8 ? m->B <= 2 : m->B <= 8;
       m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : ls_default);
       // fused all-reduce: on-device shards (DSINF_TP_LOCAL) or CUDA-IPC peer mappings across

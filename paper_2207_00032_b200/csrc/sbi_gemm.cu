@@ -129,7 +129,20 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         for (int w = 0; w < kConsumerWarps; ++w)
           ptx::tma_load_2d(ring + it * kSB + w * kBoxBytes, &p.tmap, n0 + w * kWarpCols, r0, &hd.full[it], policy);
       }
-      ptx::pdl_wait();
+      if (p.dep_flags != nullptr) {  // only the x-producing tiles of this split's k range
+        const long long step = *reinterpret_cast<const volatile long long*>(p.dep_step);
+        const unsigned target = static_cast<unsigned>(step + 1) * p.dep_per_step;
+        const int t0 = (row_begin * kKPerRow) / kColTile, t1 = (row_end * kKPerRow - 1) / kColTile;
+        for (int t = t0; t <= t1; ++t) {
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.dep_flags + t) : "memory");
+          } while (static_cast<int>(v - target) < 0);
+        }
+        ptx::fence_proxy_async_global();  // the TMA (async proxy) reads what the flags published
+      } else {
+        ptx::pdl_wait();
+      }
       for (int it = 0; it < pre; ++it) load_x(it, ring + it * kSB);
       int s = pre % stages;
       uint32_t phase = pre == stages ? 1u : 0u;
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     // ================= consumers
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
+    const bool flag_dep = kXS == 1 && p.dep_flags != nullptr;  // x by TMA after the producer's flag wait
     // LayerNorm-streaming: gamma / beta of this split's k range into smem (weights: before the wait)
     __half* sg = reinterpret_cast<__half*>(sx);
     __half* sb = sg + p.rows_per_split * kKPerRow;
@@ -192,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         reinterpret_cast<uint4*>(sb)[i] = b;
       }
     }
-    ptx::pdl_wait();
+    if (!flag_dep) ptx::pdl_wait();
 #ifdef DSINF_DIAG
     const unsigned long long t_rel = ptx::trace_release(p.trace, 32);
     const long long c_rel = ptx::clk();
@@ -306,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   }
 
   // ================= split-K reduction across the cluster (DSMEM) + epilogue
+  if (p.dep_flags != nullptr) ptx::pdl_wait();  // the epilogue's residual / outputs: whole previous grid
   if (nsplit > 1)
     ptx::cluster_sync();
   else
@@ -410,6 +425,13 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (want_stats) {
     __syncthreads();
     dev::stats_flush(p, es, (tile + split) % kStatStripes);
+  }
+  if (p.out_flags != nullptr) {  // column-tile counter for flag-granular consumers (DSINF_DOWN_FLAGS)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.out_flags + tile) : "memory");
+    }
   }
   if (p.push_n > 0) {  // publish the pushed partials: one system-scope release per destination rank
     __syncthreads();
@@ -698,6 +720,8 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   const bool xs = plan.x_stream != 0;
   const bool i8x = int8_weights && !plan.a16;  // int8 activations
   if (plan.a16 && p.pro != PRO_F16 && p.pro != PRO_LN) throw ConfigError("sbi_gemm: W8A16 takes fp16 x (PRO_F16 / PRO_LN)");
+  if (p.dep_flags != nullptr && !(xs && !plan.ln_stream && !i8x))
+    throw ConfigError("sbi_gemm: flag-granular dependencies need the fp16 / W8A16 x-streaming plan");
   if (plan.ln_stream) {
     if (p.pro != PRO_LN || p.ln_stats_in == nullptr || p.res_in == nullptr || p.ln_g == nullptr || p.ln_b == nullptr)
       throw ConfigError("sbi_gemm: LayerNorm-streaming needs PRO_LN with the producer's row sums");

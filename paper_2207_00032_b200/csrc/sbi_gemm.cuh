@@ -136,6 +136,15 @@ struct Params {
   unsigned long long* am_out;
   int am_valid;
   long long am_offset;
+  // Flag-granular dependency (x-streaming W8A16 / fp16 plans, TP = 1, DSINF_DOWN_FLAGS): instead of
+  // griddepcontrol.wait before its first x box, the producer waits until the x-producing GEMM's
+  // column-tile counters covering this CTA's k range reach (*dep_step + 1) * dep_per_step; the
+  // epilogue still waits for the whole previous grid.  out_flags: the producer side (+1 per CTA per
+  // column tile after its epilogue stores).
+  const unsigned* dep_flags;
+  unsigned dep_per_step;
+  const long long* dep_step;
+  unsigned* out_flags;
   unsigned long long* trace;  // launch timeline slot (ptx::trace_begin / trace_end) or null
   unsigned long long* cta_log;  // diagnostics: per-CTA [smid, start, release, prologue end, loop end, end] or null
 };

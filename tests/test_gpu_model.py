@@ -479,3 +479,30 @@ def test_layernorm_streaming_plan(dtype_bytes, batch, int8_act, monkeypatch):
     monkeypatch.setenv("DSINF_LN_STREAM", "1")
     run_parity(512, 2, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, int8_act=int8_act,
                oracle_int8_act=None if int8_act != capi.INT8_AUTO else (0x10f if batch <= 8 else 0x10e))
+
+
+@pytest.mark.parametrize("dtype_bytes,batch,int8_act", [(2, 1, 0), (2, 8, 0), (1, 1, capi.INT8_W8A16)])
+def test_down_flag_dependency(dtype_bytes, batch, int8_act, monkeypatch):
+    """DSINF_DOWN_FLAGS=1: MLP-down is PDL-launched and its producer waits only for the MLP-up column
+    tiles of its k range (monotonic per-tile counters, +1 per MLP-up CTA after its epilogue stores),
+    the epilogue for the whole MLP-up grid.  Same arithmetic: bit-identical logits and tokens over
+    many graph-replayed steps (the counters carry across steps), and against the oracle."""
+    rng = np.random.default_rng(41)
+    prompt = rng.integers(0, 1000, (batch, 6)).astype(np.int32)
+    outs = []
+    for df in ("0", "1"):
+        monkeypatch.setenv("DSINF_DOWN_FLAGS", df)
+        m = DecoderModel(512, 3, 8, 1000, dtype_bytes=dtype_bytes, batch=batch, max_ctx=40, seed=SEED,
+                         int8_act=int8_act)
+        m.set_prompt(prompt)
+        m.step(12)
+        torch.cuda.synchronize()
+        m.set_prompt(prompt)  # a second sequence on the same counters (re-captured graph)
+        m.step(20)
+        torch.cuda.synchronize()
+        outs.append((m.full_logits(), m.read_tokens()[1]))
+        m.close()
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][0], outs[1][0])
+    monkeypatch.setenv("DSINF_DOWN_FLAGS", "1")
+    run_parity(512, 2, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, int8_act=int8_act)
