@@ -357,6 +357,7 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
     sh.red = m.alloc_n<float>(2LL * m.t * B * h);
     sh.red_flag = m.alloc_n<unsigned long long>(2 * std::max<int64_t>(1, m.L));
     DSINF_CUDA_CHECK(cudaMemsetAsync(sh.red_flag, 0, 2 * std::max<int64_t>(1, m.L) * 8, s));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(sh.red, 0, 2LL * m.t * B * h * 4, s));  // TP_SLICE reads unpushed slots
   }
   if (m.fuse_ln) sh.lnstats = m.alloc_n<long long>((2 * m.L + 1) * gemm::kLnSlotWords);
   if (m.xs_ln || m.xs_lm) sh.xn = m.alloc_n<__half>(static_cast<int64_t>(B) * h);
@@ -652,6 +653,7 @@ struct Enqueuer {
     p.epi = gemm::EPI_F32;
     p.bias = nullptr;
     p.push_n = m.t;
+    p.push_gpu_scope = m.rt.tp_mode == DSINF_TP_LOCAL || m.rt.tp_mode == DSINF_TP_SLICE ? 1 : 0;
     for (int q = 0; q < m.t; ++q) {
       p.push_dst[q] = sh.peer_red[q] + (pt * m.t + sh.rank) * bh;
       p.push_flag[q] = sh.peer_flag[q] + pt * m.L + l;
@@ -1218,6 +1220,12 @@ struct Enqueuer {
 // rank) every rank exports CUDA-IPC handles of its slot and counter allocations, the handles are
 // all-gathered over the NCCL communicator, and each rank maps its peers' allocations (NVLink P2P).
 void map_reduction_peers(Model& m, cudaStream_t s) {
+  if (m.rt.tp_mode == DSINF_TP_SLICE) {  // every "peer" is this rank's own slot set
+    Shard& sh = m.shards[0];
+    sh.peer_red.assign(m.t, sh.red);
+    sh.peer_flag.assign(m.t, sh.red_flag);
+    return;
+  }
   if (m.rt.tp_mode != DSINF_TP_NCCL) {
     for (Shard& sh : m.shards) {
       sh.peer_red.clear();
@@ -1409,7 +1417,10 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // a fused all-reduce request (below) selects the slice plan: its slots are summed by the
       // per-CTA LayerNorm prologues
       const char* far_req = std::getenv("DSINF_FUSED_AR");
-      bool want_far = m->t > 1 && (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL) &&
+      // (TP_SLICE: the rank's pushes all land in its own slots and it is its own only signaller -- a
+      // timing model of the fused all-reduce's per-rank cost without the NVLink hop)
+      bool want_far = m->t > 1 &&
+                      (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_NCCL || rt->tp_mode == DSINF_TP_SLICE) &&
                       far_req != nullptr && std::atoi(far_req) != 0;
       if (rt->tp_mode == DSINF_TP_IPC && m->t > 1) want_far = true;  // the only exchange IPC mode has
       if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {

@@ -436,8 +436,17 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   if (p.push_n > 0) {  // publish the pushed partials: one system-scope release per destination rank
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      for (int q = 0; q < p.push_n; ++q) atomicAdd_system(p.push_flag[q], 1ull);
+      // one system-scope fence, then fire-and-forget reductions: returning atomics serialised one
+      // round trip per destination (t of them) at the end of every CTA, on the consumers' critical path
+      if (p.push_gpu_scope) {
+        __threadfence();
+        for (int q = 0; q < p.push_n; ++q)
+          asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p.push_flag[q]) : "memory");
+      } else {
+        __threadfence_system();
+        for (int q = 0; q < p.push_n; ++q)
+          asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p.push_flag[q]) : "memory");
+      }
     }
   }
   // keep our smem alive until the peers' DSMEM reads are done (their values are consumed before

@@ -128,6 +128,7 @@ struct Params {
   // fused all-reduce (producer side, EPI_F32): the partial [B][N] goes to push_dst[q] (rank q's slot
   // for this rank) for q < push_n, then each CTA adds 1 to every push_flag[q] (system scope)
   int push_n;
+  int push_gpu_scope;  // 1: every destination is on this GPU (TP_LOCAL / TP_SLICE): gpu-scope fence
   float* push_dst[8];
   unsigned long long* push_flag[8];
   // EPI_F32 without bias (LM head): greedy argmax fused into the epilogue -- per row the max of
