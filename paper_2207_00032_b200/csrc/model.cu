@@ -109,6 +109,7 @@ struct Shard {
   // rank's attn-out (point 0) / MLP-down (point 1) epilogue, and their arrival counters [2][L]
   float* red = nullptr;
   unsigned long long* red_flag = nullptr;
+  unsigned long long* push_done = nullptr;  // [2][L] gpu-local CTA counters of the last-CTA signalling
   // every rank's red / red_flag as addressable from this rank: the other on-device shards
   // (DSINF_TP_LOCAL) or CUDA-IPC mappings of the peer processes' allocations over NVLink (NCCL mode)
   std::vector<float*> peer_red;
@@ -156,6 +157,10 @@ struct dsinf_model {
   // TP > 1 without NCCL kernels between the GEMMs: the row-parallel GEMMs push their partials into
   // every rank's slots and signal a counter; the next LayerNorm prologue waits and sums the slots
   bool fused_ar = false;
+  // fused all-reduce signalling: gpu-scope fences when every destination is on this GPU (TP_LOCAL,
+  // TP_SLICE; DSINF_FAR_SYS=1 forces system scope for measurement); with system scope the grid's last
+  // CTA signals each rank once (DSINF_FAR_LASTCTA=0: every CTA signals)
+  bool far_gpu_scope = false, far_last_cta = false;
   long long* step_ctr = nullptr;  // decode steps taken (fused all-reduce counter targets)
   // DSINF_TP_IPC: argmax-key arrival counter (bumped by the peers' select kernels) and the peers'
   // key arrays / counters as mapped into this process; ipc_ready once dsinf_model_ipc_attach ran
@@ -358,6 +363,8 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
     sh.red_flag = m.alloc_n<unsigned long long>(2 * std::max<int64_t>(1, m.L));
     DSINF_CUDA_CHECK(cudaMemsetAsync(sh.red_flag, 0, 2 * std::max<int64_t>(1, m.L) * 8, s));
     DSINF_CUDA_CHECK(cudaMemsetAsync(sh.red, 0, 2LL * m.t * B * h * 4, s));  // TP_SLICE reads unpushed slots
+    sh.push_done = m.alloc_n<unsigned long long>(2 * std::max<int64_t>(1, m.L));
+    DSINF_CUDA_CHECK(cudaMemsetAsync(sh.push_done, 0, 2 * std::max<int64_t>(1, m.L) * 8, s));
   }
   if (m.fuse_ln) sh.lnstats = m.alloc_n<long long>((2 * m.L + 1) * gemm::kLnSlotWords);
   if (m.xs_ln || m.xs_lm) sh.xn = m.alloc_n<__half>(static_cast<int64_t>(B) * h);
@@ -636,7 +643,7 @@ struct Enqueuer {
     r.n = m.t;
     r.stride = bh;
     r.flag = sh.red_flag + pt * m.L + l;
-    r.per_step = static_cast<unsigned long long>(m.t) * ctas(pt == 0 ? sh.plan_o : sh.plan_down);
+    r.per_step = static_cast<unsigned long long>(m.t) * (m.far_last_cta ? 1 : ctas(pt == 0 ? sh.plan_o : sh.plan_down));
     return r;
   }
   void use_red(gemm::Params& p, const RedIn& r) const {
@@ -653,7 +660,12 @@ struct Enqueuer {
     p.epi = gemm::EPI_F32;
     p.bias = nullptr;
     p.push_n = m.t;
-    p.push_gpu_scope = m.rt.tp_mode == DSINF_TP_LOCAL || m.rt.tp_mode == DSINF_TP_SLICE ? 1 : 0;
+    p.push_gpu_scope = m.far_gpu_scope ? 1 : 0;
+    if (m.far_last_cta) {
+      p.push_done = sh.push_done + pt * m.L + l;
+      p.push_step = m.step_ctr;
+      p.push_ctas = static_cast<unsigned long long>(ctas(pt == 0 ? sh.plan_o : sh.plan_down));
+    }
     for (int q = 0; q < m.t; ++q) {
       p.push_dst[q] = sh.peer_red[q] + (pt * m.t + sh.rank) * bh;
       p.push_flag[q] = sh.peer_flag[q] + pt * m.L + l;
@@ -1451,6 +1463,13 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every
       // consumer CTA re-reads t slots), the win is hiding the NVLink exchange across GPUs
       m->fused_ar = want_far && !m->fuse_ln;
+      {
+        const char* fsys = std::getenv("DSINF_FAR_SYS");
+        const char* flast = std::getenv("DSINF_FAR_LASTCTA");
+        m->far_gpu_scope = (rt->tp_mode == DSINF_TP_LOCAL || rt->tp_mode == DSINF_TP_SLICE) &&
+                           !(fsys != nullptr && std::atoi(fsys) != 0);
+        m->far_last_cta = m->fused_ar && !m->far_gpu_scope && (flast == nullptr || std::atoi(flast) != 0);
+      }
     }
     if (rt->tp_mode == DSINF_TP_NCCL && m->t > 1) {
       require(nccl_comm != nullptr, "NCCL mode needs a communicator");

@@ -442,6 +442,18 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         __threadfence();
         for (int q = 0; q < p.push_n; ++q)
           asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p.push_flag[q]) : "memory");
+      } else if (p.push_done != nullptr) {
+        // every CTA's pushes ordered at gpu scope before its counter bump; the last CTA acquires them
+        // all, fences at system scope once and signals each destination rank once
+        __threadfence();
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.push_done) : "memory");
+        const unsigned long long step = static_cast<unsigned long long>(*reinterpret_cast<const volatile long long*>(p.push_step));
+        if (old + 1 == (step + 1) * p.push_ctas) {
+          __threadfence_system();
+          for (int q = 0; q < p.push_n; ++q)
+            asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p.push_flag[q]) : "memory");
+        }
       } else {
         __threadfence_system();
         for (int q = 0; q < p.push_n; ++q)

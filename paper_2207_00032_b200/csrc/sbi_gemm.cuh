@@ -131,6 +131,12 @@ struct Params {
   int push_gpu_scope;  // 1: every destination is on this GPU (TP_LOCAL / TP_SLICE): gpu-scope fence
   float* push_dst[8];
   unsigned long long* push_flag[8];
+  // system-scope pushes (cross-process / cross-GPU): each CTA bumps this gpu-local counter after a
+  // gpu-scope fence and only the grid's LAST CTA issues the system-scope fence and signals the t
+  // destinations (one signal per rank instead of one per CTA); null = every CTA signals
+  unsigned long long* push_done;
+  const long long* push_step;
+  unsigned long long push_ctas;
   // EPI_F32 without bias (LM head): greedy argmax fused into the epilogue -- per row the max of
   // pack(value, global column) over columns < am_valid, atomicMax'd into am_out[b] (zeroed per
   // step); ties resolve to the lowest column (moe.hpp:69-74).
