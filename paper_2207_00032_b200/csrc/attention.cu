@@ -131,9 +131,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
 // as attn_chunk / attention_kernel.
 constexpr int kTmaRows = 32;
 
+constexpr int kTmaMaxRing = 4;
 template <int TPP>
-__host__ __device__ constexpr size_t tma_ring_bytes(int d) {
-  return static_cast<size_t>(2) * 2 * kTmaRows * d * 2;
+__host__ __device__ constexpr size_t tma_ring_bytes(int d, int ring = 2) {
+  return static_cast<size_t>(ring) * 2 * kTmaRows * d * 2;
 }
 
 template <int TPP>
@@ -144,21 +145,21 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   const int d = p.d;
   const size_t stage_halves = static_cast<size_t>(2) * kTmaRows * d;  // K rows then V rows
   __half* ring = reinterpret_cast<__half*>(araw);
-  float* scratch = reinterpret_cast<float*>(araw + tma_ring_bytes<TPP>(d));
+  const int R = p.tma_ring;  // ring slots (2..kTmaMaxRing)
+  float* scratch = reinterpret_cast<float*>(araw + tma_ring_bytes<TPP>(d, R));
   float* so = scratch;       // [PPR][d]
   float* sm = so + PPR * d;  // [PPR]
   float* sl = sm + PPR;      // [PPR]
   float* co = sl + PPR;      // [d]
   float* cst = co + d;       // [2]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      araw + tma_ring_bytes<TPP>(d) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8);
+      araw + tma_ring_bytes<TPP>(d, R) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8);
   const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
   const int tid = threadIdx.x;
   ptx::trace_begin(p.trace);
   ptx::pdl_trigger();
   if (tid == 0) {
-    ptx::mbar_init(&bars[0], 1);
-    ptx::mbar_init(&bars[1], 1);
+    for (int r = 0; r < R; ++r) ptx::mbar_init(&bars[r], 1);
     ptx::fence_mbar_init();
   }
   ptx::pdl_wait();
@@ -173,16 +174,15 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   auto issue = [&](int st) {
     const int rows = min(kTmaRows, n - st * kTmaRows);
     const uint32_t bytes = static_cast<uint32_t>(rows) * d * 2;
-    __half* dst = ring + (st & 1) * stage_halves;
+    __half* dst = ring + (st % R) * stage_halves;
     const size_t src = kv_base + static_cast<size_t>(j0 + st * kTmaRows) * d;
-    ptx::mbar_arrive_expect_tx(&bars[st & 1], 2 * bytes);
-    ptx::bulk_g2s(dst, p.kc + src, bytes, &bars[st & 1], pol);
-    ptx::bulk_g2s(dst + static_cast<size_t>(kTmaRows) * d, p.vc + src, bytes, &bars[st & 1], pol);
+    ptx::mbar_arrive_expect_tx(&bars[st % R], 2 * bytes);
+    ptx::bulk_g2s(dst, p.kc + src, bytes, &bars[st % R], pol);
+    ptx::bulk_g2s(dst + static_cast<size_t>(kTmaRows) * d, p.vc + src, bytes, &bars[st % R], pol);
   };
   __syncthreads();  // barrier init visible
   if (tid == 0) {
-    if (nst > 0) issue(0);
-    if (nst > 1) issue(1);
+    for (int st = 0; st < min(R, nst); ++st) issue(st);
   }
   const int slot = tid / TPP, lane_in = tid % TPP;
   const int dim0 = lane_in * 8;
@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = 0.f;
   for (int st = 0; st < nst; ++st) {
-    ptx::mbar_wait(&bars[st & 1], static_cast<uint32_t>((st >> 1) & 1));
-    const __half* ks = ring + (st & 1) * stage_halves;
+    ptx::mbar_wait(&bars[st % R], static_cast<uint32_t>((st / R) & 1));
+    const __half* ks = ring + (st % R) * stage_halves;
     const __half* vs = ks + static_cast<size_t>(kTmaRows) * d;
     const int rows = min(kTmaRows, n - st * kTmaRows);
     float sc[kU];
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
       m = mn;
     }
     __syncthreads();  // every thread is done with this ring slot
-    if (tid == 0 && st + 2 < nst) issue(st + 2);
+    if (tid == 0 && st + R < nst) issue(st + R);
   }
   // merge the PPR position slots of this CTA (attn_chunk's tail)
   if (has_dims) {
@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
 }
 
 template <int TPP>
-size_t tma_smem_bytes(int d) {
-  return tma_ring_bytes<TPP>(d) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8 + 16;
+size_t tma_smem_bytes(int d, int ring) {
+  return tma_ring_bytes<TPP>(d, ring) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8 + 8 * kTmaMaxRing;
 }
 
 }  // namespace
@@ -305,9 +305,9 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   if (carveout_max()) {
     DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -336,12 +336,17 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
   const int tma = [] { const char* v = std::getenv("DSINF_ATTN_TMA"); return v ? std::atoi(v) : 1; }();  // read per enqueue
   if (tma && (reinterpret_cast<uintptr_t>(p.kc) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.vc) & 15) == 0) {
     p.kv_rows_cap = 0;
+    // ring slots: enough for a chunk's stages at the largest context, 2..4 (DSINF_ATTN_RING overrides)
+    const int max_st = ((p.max_seq + chunks - 1) / chunks + kTmaRows - 1) / kTmaRows;
+    const char* rv = std::getenv("DSINF_ATTN_RING");
+    p.tma_ring = rv ? std::max(2, std::min(kTmaMaxRing, std::atoi(rv))) : 2;
+    p.tma_ring = std::max(2, std::min(p.tma_ring, max_st));
     if (p.d <= 64)
-      launch_pdl(attention_tma_kernel<8>, grid, block, tma_smem_bytes<8>(p.d), s, pdl, p, cluster);
+      launch_pdl(attention_tma_kernel<8>, grid, block, tma_smem_bytes<8>(p.d, p.tma_ring), s, pdl, p, cluster);
     else if (p.d <= 128)
-      launch_pdl(attention_tma_kernel<16>, grid, block, tma_smem_bytes<16>(p.d), s, pdl, p, cluster);
+      launch_pdl(attention_tma_kernel<16>, grid, block, tma_smem_bytes<16>(p.d, p.tma_ring), s, pdl, p, cluster);
     else
-      launch_pdl(attention_tma_kernel<32>, grid, block, tma_smem_bytes<32>(p.d), s, pdl, p, cluster);
+      launch_pdl(attention_tma_kernel<32>, grid, block, tma_smem_bytes<32>(p.d, p.tma_ring), s, pdl, p, cluster);
     return;
   }
   // DSINF_ATTN_PREFETCH=1 (with DSINF_ATTN_TMA=0): K/V staging before the dependency wait (a chunk's

@@ -70,6 +70,7 @@ struct AttnParams {
   // shared memory BEFORE the dependency wait (they were written by earlier steps); only q and the
   // new position's K/V row are read after it.  Set by ops::attention.
   int kv_rows_cap;
+  int tma_ring;  // bulk-copy variant: K/V ring slots (set by ops::attention)
 };
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
