@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
     for (int r = 0; r < R; ++r) ptx::mbar_init(&bars[r], 1);
     ptx::fence_mbar_init();
   }
-  ptx::pdl_wait();
-  const int ctx = *p.pos + 1;
+  // the position counter and the K/V rows of earlier positions were written by earlier steps (the
+  // previous graph launch has completed): with p.early_kv the stages holding only such rows are
+  // requested before the wait on this step's QKV GEMM
+  const int ctx = *reinterpret_cast<const volatile int*>(p.pos) + 1;
   const int chunk = (ctx + C - 1) / C;
   const int j0 = c * chunk;
   const int j1 = min(ctx, j0 + chunk);
@@ -181,8 +183,12 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
     ptx::bulk_g2s(dst + static_cast<size_t>(kTmaRows) * d, p.vc + src, bytes, &bars[st % R], pol);
   };
   __syncthreads();  // barrier init visible
+  int issued = 0;
+  if (p.early_kv && tid == 0)
+    while (issued < min(R, nst) && j0 + (issued + 1) * kTmaRows <= ctx - 1) issue(issued++);  // rows < pos
+  ptx::pdl_wait();
   if (tid == 0) {
-    for (int st = 0; st < min(R, nst); ++st) issue(st);
+    for (int st = issued; st < min(R, nst); ++st) issue(st);
   }
   const int slot = tid / TPP, lane_in = tid % TPP;
   const int dim0 = lane_in * 8;
@@ -341,6 +347,8 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
     const char* rv = std::getenv("DSINF_ATTN_RING");
     p.tma_ring = rv ? std::max(2, std::min(kTmaMaxRing, std::atoi(rv))) : 2;
     p.tma_ring = std::max(2, std::min(p.tma_ring, max_st));
+    const char* ev = std::getenv("DSINF_ATTN_EARLY");
+    p.early_kv = ev != nullptr && std::atoi(ev) != 0;
     if (p.d <= 64)
       launch_pdl(attention_tma_kernel<8>, grid, block, tma_smem_bytes<8>(p.d, p.tma_ring), s, pdl, p, cluster);
     else if (p.d <= 128)

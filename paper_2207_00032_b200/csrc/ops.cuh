@@ -71,6 +71,7 @@ struct AttnParams {
   // new position's K/V row are read after it.  Set by ops::attention.
   int kv_rows_cap;
   int tma_ring;  // bulk-copy variant: K/V ring slots (set by ops::attention)
+  int early_kv;  // bulk-copy variant: stages of earlier positions requested before the dependency wait
 };
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
