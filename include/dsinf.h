@@ -372,6 +372,12 @@ int dsinf_nccl_get_unique_id(uint8_t id_out[128]);
 int dsinf_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
                            void** comm_out);
 int dsinf_nccl_comm_destroy(void* comm);
+/* Probe of the NCCL-mode all-reduce buffers: *symmetric = 1 when libnccl exports ncclMemAlloc /
+ * ncclCommWindowRegister (NCCL >= 2.27), in which case a `count`-float buffer is allocated with
+ * ncclMemAlloc and registered as an NCCL_WIN_COLL_SYMMETRIC window (as the model's per-layer
+ * all-reduce buffers are in DSINF_TP_NCCL; DSINF_NCCL_WINDOWS=0 disables that); a sum all-reduce of
+ * ones runs on it and *first_out receives element 0 (= the number of ranks).  Collective. */
+int dsinf_nccl_window_check(void* comm, int64_t count, int32_t* symmetric, float* first_out);
 
 /* ================================================================ model.hpp accounting */
 

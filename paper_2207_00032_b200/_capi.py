@@ -187,6 +187,7 @@ SIGNATURES = {
     "dsinf_model_destroy": (C.c_int, [vp]),
     "dsinf_model_ipc_handle": (C.c_int, [vp, vp, C.c_int64, C.POINTER(C.c_int64)]),
     "dsinf_model_ipc_attach": (C.c_int, [vp, vp, C.c_int64]),
+    "dsinf_nccl_window_check": (C.c_int, [vp, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     "dsinf_model_set_prompt": (C.c_int, [vp, P(i32), i64, vp]),
     "dsinf_model_set_prompt_device": (C.c_int, [vp, vp, i64, vp]),
     "dsinf_decode_step": (C.c_int, [vp, vp]),

@@ -197,10 +197,17 @@ struct dsinf_model {
   T* alloc_n(int64_t n) {
     return static_cast<T*>(alloc(static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T)));
   }
+  // NCCL mode: the per-layer all-reduce buffers in NCCL symmetric memory (ncclMemAlloc, registered as
+  // NCCL_WIN_COLL_SYMMETRIC windows) when the library has them; released before the communicator
+  std::vector<std::pair<void*, dsinf::nccl::Window>> nccl_windows;
   ~dsinf_model() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (auto& w : nccl_windows) {
+      dsinf::nccl::window_deregister(comm, w.second);
+      dsinf::nccl::mem_free(w.first);
+    }
     for (void* p : ipc_maps) cudaIpcCloseMemHandle(p);
     for (auto& a : allocs) cudaFree(a.p);
     if (cta_log) cudaFree(cta_log);
@@ -346,8 +353,20 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   const int B = m.B;
   sh.res[0] = m.alloc_n<float>(B * h);
   sh.res[1] = m.alloc_n<float>(B * h);
-  sh.d_attn = m.alloc_n<float>(B * h);
-  sh.d_mlp = m.alloc_n<float>(B * h);
+  const char* wv = std::getenv("DSINF_NCCL_WINDOWS");
+  if (m.rt.tp_mode == DSINF_TP_NCCL && m.t > 1 && !m.fused_ar && m.comm != nullptr && nccl::has_windows() &&
+      (wv == nullptr || std::atoi(wv) != 0)) {
+    // latency-bound B x h fp32 messages (16-786 KB): symmetric windows let NCCL use its symmetric-memory
+    // all-reduce kernels (collective registration, same order on every rank)
+    for (float** d : {&sh.d_attn, &sh.d_mlp}) {
+      void* p = nccl::mem_alloc(static_cast<size_t>(B * h) * 4);
+      m.nccl_windows.emplace_back(p, nccl::window_register(m.comm, p, static_cast<size_t>(B * h) * 4));
+      *d = static_cast<float*>(p);
+    }
+  } else {
+    sh.d_attn = m.alloc_n<float>(B * h);
+    sh.d_mlp = m.alloc_n<float>(B * h);
+  }
   sh.q = m.alloc_n<__half>(B * Hl * d);
   sh.a = m.alloc_n<__half>(B * Hl * d);
   sh.u = m.alloc_n<__half>(B * Fl);
@@ -1882,6 +1901,32 @@ int dsinf_nccl_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, 
 
 int dsinf_nccl_comm_destroy(void* comm) {
   return guarded([&] { nccl::destroy(static_cast<nccl::Comm>(comm)); });
+}
+
+int dsinf_nccl_window_check(void* comm, int64_t count, int32_t* symmetric, float* first_out) {
+  return guarded([&] {
+    require(comm && symmetric && first_out && count >= 1, "bad argument");
+    const auto c = static_cast<nccl::Comm>(comm);
+    *symmetric = nccl::has_windows() ? 1 : 0;
+    void* buf = nullptr;
+    nccl::Window w = nullptr;
+    if (*symmetric) {
+      buf = nccl::mem_alloc(static_cast<size_t>(count) * 4);
+      w = nccl::window_register(c, buf, static_cast<size_t>(count) * 4);
+    } else {
+      DSINF_CUDA_CHECK(cudaMalloc(&buf, static_cast<size_t>(count) * 4));
+    }
+    std::vector<float> ones(static_cast<size_t>(count), 1.0f);
+    DSINF_CUDA_CHECK(cudaMemcpy(buf, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice));
+    nccl::allreduce_sum_f32(static_cast<float*>(buf), static_cast<size_t>(count), c, nullptr);
+    DSINF_CUDA_CHECK(cudaMemcpy(first_out, buf, 4, cudaMemcpyDeviceToHost));
+    if (*symmetric) {
+      nccl::window_deregister(c, w);
+      nccl::mem_free(buf);
+    } else {
+      cudaFree(buf);
+    }
+  });
 }
 
 }  // extern "C"

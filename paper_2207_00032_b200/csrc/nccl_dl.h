@@ -25,5 +25,16 @@ void destroy(Comm c);
 void allreduce_sum_f32(float* buf, size_t count, Comm c, cudaStream_t s);
 void allgather_bytes(const void* send, void* recv, size_t bytes_per_rank, Comm c, cudaStream_t s);
 
+// Symmetric memory (NCCL >= 2.27: ncclMemAlloc + ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)):
+// the latency-bound per-layer all-reduce buffers registered as collective windows.  Optional symbols:
+// has_windows() is false on an older libnccl, and callers keep plain cudaMalloc buffers.
+typedef struct ncclWindow* Window;
+constexpr int kWinCollSymmetric = 0x01;
+bool has_windows();
+void* mem_alloc(size_t bytes);
+void mem_free(void* p);
+Window window_register(Comm c, void* buf, size_t bytes);  // collective over the communicator
+void window_deregister(Comm c, Window w);
+
 }  // namespace nccl
 }  // namespace dsinf
