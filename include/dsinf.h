@@ -126,7 +126,8 @@ int dsinf_quantize_weights_int8(const void* w_rowmajor_f16, int64_t N, int64_t K
  * recipe): every `group` (= 128) consecutive k of an output row share an fp16 scale
  * s = fp16(max|w| / 127) (fp32 divide, round to nearest; 1 for an all-zero group) and
  * q = clamp(rint(w / s), -127, 127) with an fp32 divide; packed with pack_M = 4 like the row mode,
- * group_scales_f16 [ceil(K/group)][N].  The W8A16 GEMM dequantises w = fp16(q * s) per group. */
+ * group_scales_f16 [ceil(K/group)][N].  The W8A16 GEMM computes y = sum_g s_g * sum_{k in g} q x
+ * (fp32 per-group partial sums folded with the group scale). */
 int dsinf_quantize_weights_int8_groups(const void* w_rowmajor_f16, int64_t N, int64_t K, int32_t group,
                                        int8_t* packed_i8, void* group_scales_f16, void* stream);
 /* Per-token activation quantisation (same formula, scale per row of x). */

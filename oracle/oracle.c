@@ -572,12 +572,12 @@ static int act_of(int int8_act, int g) { return (int8_act & 0x100) ? (int8_act >
  * (int8_act 1: weight-only, fp16 activations) */
 static void gemm8(int int8_act, const int8_t* W, const float* ws, int64_t N, int64_t K, const float* x16, int64_t B,
                   float* y, const float* gs) {
-  if (gs != NULL) { /* K-group weight-only: y = sum_k fp16(q s_group) x_k (fp64 sum; the GPU: fp32) */
+  if (gs != NULL) { /* K-group weight-only: y = sum_g s_g sum_{k in g} q x (fp64; the GPU: fp32 per group) */
 #pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; ++n)
       for (int64_t b = 0; b < B; ++b) {
         double a = 0.0;
-        for (int64_t k = 0; k < K; ++k) a += (double)f16r((float)W[n * K + k] * gs[(k / 128) * N + n]) * (double)x16[b * K + k];
+        for (int64_t k = 0; k < K; ++k) a += (double)W[n * K + k] * (double)gs[(k / 128) * N + n] * (double)x16[b * K + k];
         y[b * N + n] = (float)a;
       }
     return;

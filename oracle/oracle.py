@@ -182,16 +182,16 @@ def quant_groups(x, group=128):
 
 
 def dequant_groups(q, s16, group=128):
-    """The W8A16 K-group GEMM's effective weights: fp16(q * s) per element (fp32 product, one fp16
-    rounding -- what __hmul2 of the exact fp16 q and the fp16 scale computes)."""
+    """The K-group recipe's effective weights q * s (exact in fp64; the fp16 scale times an int8)."""
     R, K = q.shape
-    sc = np.repeat(s16.astype(np.float32).T, group, axis=1)[:, :K]
-    return (q.astype(np.float32) * sc).astype(np.float16).astype(np.float32)
+    sc = np.repeat(s16.astype(np.float64).T, group, axis=1)[:, :K]
+    return q.astype(np.float64) * sc
 
 
 def gemm_a16_groups(q, s16, x16, group=128):
-    """y[B][N] = sum_k fp16(q s) x in fp64, rounded to fp32 (the GPU accumulates in fp32)."""
-    w = dequant_groups(q, s16, group).astype(np.float64)
+    """y[B][N] = sum_g s_g * sum_{k in g} q x in fp64, rounded to fp32 (the GPU: each group's exact
+    int8 x fp16 products summed in fp32, times its fp16 scale, groups summed in fp32)."""
+    w = dequant_groups(q, s16, group)
     return (np.asarray(x16, dtype=np.float64) @ w.T).astype(np.float32)
 
 

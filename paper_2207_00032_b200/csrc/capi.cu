@@ -110,7 +110,7 @@ void run_gemm(const dsinf_gemm_args& a, cudaStream_t s) {
     const bool x_i8 = a.x_dtype == DSINF_DT_I8 || quant_once;
     const bool ready_x = !i8w || a16 || x_i8;  // GEMM-ready x (no on-the-fly quantisation)
     const bool xs = ready_x && gemm::prefer_x_stream(nb) && gemm::x_streamable(xb, K, K, i8w && !a16);
-    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs, a16);
+    const gemm::Plan plan = gemm::make_plan(N, K, nb, i8w, a.ksplit, xs, a16, false, false, a.group_size != 0);
     gemm::Params p{};
     p.w_scale = a.w_scales;
     p.w_gscale = a.group_size != 0 ? static_cast<const __half*>(a.w_group_scales) : nullptr;

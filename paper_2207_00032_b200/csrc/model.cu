@@ -393,14 +393,15 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   }
   if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
   const bool i8 = m.int8;
+  const bool kg = m.rt.int8_group != 0;
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
-                                m.ln_use(0), m.a16g(0));
+                                m.ln_use(0), m.a16g(0), kg);
   sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1), false,
-                              m.a16g(1));
+                              m.a16g(1), kg);
   sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2),
-                               m.a16g(2));
+                               m.a16g(2), kg);
   sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3), false,
-                                 m.a16g(3));
+                                 m.a16g(3), kg);
   if (m.down_flags) {
     for (LayerW& w : sh.layers) {
       w.up_flags = m.alloc_n<unsigned>(sh.plan_up.col_tiles);

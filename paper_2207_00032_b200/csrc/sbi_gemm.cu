@@ -206,6 +206,29 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
         reinterpret_cast<uint4*>(sb)[i] = b;
       }
     }
+    // K-group scales of this CTA's stages -> smem [stage][128 columns] (weights: before the wait)
+    const int x_region = kLN ? 2 * p.rows_per_split * kKPerRow * 2 : (kXS ? 0 : p.B * p.x_row_words * 4);
+    __half* sgs = reinterpret_cast<__half*>(reinterpret_cast<uint8_t*>(sx) + x_region);
+    if constexpr (kA16 != 0) {
+      if (p.w_gscale != nullptr) {
+        const int g0 = row_begin / kRowsPerStage;
+        for (int i = ctid; i < n_iters * (kColTile / 8); i += 128) {  // 8 columns (16 B) per item
+          const int it = i / (kColTile / 8), c8 = (i - it * (kColTile / 8)) * 8;
+          const int n = n0 + c8;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          const __half* src = p.w_gscale + static_cast<size_t>(g0 + it) * p.N + n;
+          if (n + 8 <= p.N && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            v = __ldg(reinterpret_cast<const uint4*>(src));
+          } else {
+            unsigned short h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int e = 0; e < 8; ++e)
+              if (n + e < p.N) h[e] = __half_as_ushort(src[e]);
+            v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          }
+          *reinterpret_cast<uint4*>(sgs + it * kColTile + c8) = v;
+        }
+      }
+    }
     if (!flag_dep) ptx::pdl_wait();
 #ifdef DSINF_DIAG
     const unsigned long long t_rel = ptx::trace_release(p.trace, 32);
@@ -285,10 +308,9 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     if constexpr (kA16) {
       const int g = lane >> 2, t = lane & 3;
       // K-group scales: stage i of this split is group row_begin / kRowsPerStage + i
-      const __half* gs = p.w_gscale == nullptr ? nullptr
-                                               : p.w_gscale + static_cast<size_t>(row_begin / kRowsPerStage) * p.N +
-                                                     n0 + cw * kWarpCols;
-      const int gs_valid = p.N - (n0 + cw * kWarpCols);
+      // K-group scales from the staged smem copy ([stage][128]; written before the consumer barrier)
+      const __half* gs = p.w_gscale == nullptr ? nullptr : sgs + cw * kWarpCols;
+      const int gs_valid = kWarpCols;  // out-of-range columns were staged as 0
       if constexpr (kXS) {  // x word pair 2 * (4 kk + t) of batch row r in the stage's two boxes
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int st, int, int kk, int bt) {
           const int r = bt * 8 + g;
@@ -296,14 +318,14 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
           const int w = 8 * kk + 2 * t, ww = w & 31;
           const uint8_t* xb = ring + st * kSB + kXOff + (w >> 5) * kBoxSlot;
           return *reinterpret_cast<const uint2*>(xb + r * 128 + (((ww >> 2) ^ (r & 7)) << 4) + (ww & 3) * 4);
-        }, 1, gs, p.N, gs_valid, ln_pre);
+        }, 1, gs, kColTile, gs_valid, ln_pre);
       } else {
         const int xrw = p.x_row_words;
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int, int it, int kk, int bt) {
           const int r = bt * 8 + g;
           if (r >= p.B) return make_uint2(0u, 0u);
           return *reinterpret_cast<const uint2*>(sx + r * xrw + it * 2 * kRowsPerStage + 8 * kk + 2 * t);
-        }, 1, gs, p.N, gs_valid);
+        }, 1, gs, kColTile, gs_valid);
       }
     } else if constexpr (kXS) {
       c.run_xs(ring, hd, stages, s, phase, n_iters, p.B, cw, lane, kSB, kXOff, ln_pre);
@@ -645,7 +667,7 @@ bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16, bool ln_stream,
-               bool a16_biased) {
+               bool a16_biased, bool k_groups) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   if (a16 && !int8_weights) throw ConfigError("sbi_gemm: W8A16 needs int8 weights");
   if (ln_stream && (!x_stream || (int8_weights && !a16)))
@@ -656,6 +678,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   Plan pl{};
   pl.x_stream = x_stream ? 1 : 0;
   pl.ln_stream = ln_stream ? 1 : 0;
+  pl.k_groups = k_groups && a16 ? 1 : 0;
   pl.a16 = a16 ? (a16_biased ? 2 : 1) : 0;
   pl.col_tiles = (N + kColTile - 1) / kColTile;
   pl.nb8 = B <= 8 ? 1 : 2;
@@ -668,9 +691,11 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   };
   // smem x slice of the non-streaming mode (the streaming mode keeps x in the ring stages)
   // (LayerNorm-streaming: the split's gamma and beta, fp16, in place of the slice)
+  // (+ the K-group scales of the CTA's stages: 128 fp16 per stage)
   auto x_bytes = [&](int rps) {
-    if (ln_stream) return static_cast<size_t>(2) * rps * m * 2;
-    return x_stream ? size_t{0} : static_cast<size_t>(B) * (xw * rps + 8) * 4;
+    const size_t gbytes = pl.k_groups ? static_cast<size_t>(rps / kRowsPerStage) * kColTile * 2 : 0;
+    if (ln_stream) return static_cast<size_t>(2) * rps * m * 2 + gbytes;
+    return (x_stream ? size_t{0} : static_cast<size_t>(B) * (xw * rps + 8) * 4) + gbytes;
   };
   auto valid = [&](int s) {
     const int rps = rps_for(s);
@@ -728,8 +753,8 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.rows_per_split = plan.rows_per_split;
   p.stages = plan.stages;
   p.a16 = plan.a16;
-  if (p.w_gscale != nullptr && !(int8_weights && plan.a16))
-    throw ConfigError("sbi_gemm: K-group scales need int8 weights on the W8A16 plan");
+  if (p.w_gscale != nullptr && !(int8_weights && plan.a16 && plan.k_groups))
+    throw ConfigError("sbi_gemm: K-group scales need int8 weights on a W8A16 plan made with k_groups");
   p.x_row_words = (plan.a16 ? 2 : 1) * plan.rows_per_split + 8;
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");

@@ -159,6 +159,7 @@ struct Params {
 struct Plan {
   int x_stream;  // 1: x streamed per stage by TMA (PRO_F16 / PRO_I8 only), no smem x slice
   int ln_stream;  // 1 (with x_stream): the residual is streamed and LayerNorm'd per stage (PRO_LN)
+  int k_groups;   // 1: smem for the CTA's K-group scales ([stage][128] fp16 after the x / gamma-beta region)
   int a16;       // W8A16 plan (int8 weights, fp16 x): 1 signed weight bytes, 2 biased (s + 128)
   int col_tiles;
   int ksplit;
@@ -174,8 +175,9 @@ void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 // Sets kernel attributes for every instantiation; call before graph capture.
 void configure();
 // a16_biased: the W8A16 weights are stored biased (s + 128 per byte; the decode model's own weights)
+// k_groups: W8A16 with K-group scales (the CTA's group scales are staged in shared memory)
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false, bool a16 = false,
-               bool ln_stream = false, bool a16_biased = false);
+               bool ln_stream = false, bool a16_biased = false, bool k_groups = false);
 // TMA descriptor of x for the x-streaming mode: `words` 32-bit words per row, `B` rows, row
 // stride ld_words (ld_words * 4 must be a multiple of 16 and x 16-byte aligned).
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words);

@@ -613,8 +613,9 @@ struct Consumer {
   // `step` > 1: this warp group consumes every step-th ring slot (the persistent step kernel's
   // interleaved consumer groups; stages % step == 0).
   // K-group scales (gs != nullptr): one int8 stage is one 128-k group; gs points at the group of
-  // the first stage for this warp's 32 columns ([group][gs_ld] fp16, gs_valid columns readable),
-  // and the weights dequantise to w = fp16(q * s_group) before the MMA (the row scale is then 1).
+  // the first stage for this warp's 32 columns ([group][gs_ld] fp16, gs_valid columns readable).
+  // Each group's exact int8 x fp16 products accumulate in fp32 (accg), then acc += s_group * accg
+  // per column at the stage end (the row scale is then 1).
   // `pre(s, it)` (optional) runs on every consumer thread right after stage s arrived, before its
   // MMAs (the LayerNorm-streaming plan normalises the stage's residual boxes there).
   struct NoPre {
@@ -647,8 +648,15 @@ struct Consumer {
           o[j][h] = __half2half2(c < gs_valid ? gs[static_cast<size_t>(i) * gs_ld + c] : __ushort_as_half(0));
         }
     };
+    float accg[kGroups ? 2 : 1][kGroups ? kNB8 : 1][4];  // this group's exact int8 x fp16 sums (fp32)
     if constexpr (kGroups) {
       if (n_iters > 0) load_gs(0, gsc);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int bt = 0; bt < kNB8; ++bt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) accg[j][bt][q] = 0.f;
     }
     for (int it = 0; it < n_iters; ++it) {
       if constexpr (kGroups) {
@@ -670,16 +678,25 @@ struct Consumer {
           uint32_t a0, a1, a2, a3;
           i8x4_to_h2x2<kA16 == 2>(wq[2 * j], a0, a2);
           i8x4_to_h2x2<kA16 == 2>(wq[2 * j + 1], a1, a3);
-          if constexpr (kGroups) {
-            a0 = h2_bits(__hmul2(bits_h2(a0), gsc[j][0]));
-            a2 = h2_bits(__hmul2(bits_h2(a2), gsc[j][0]));
-            a1 = h2_bits(__hmul2(bits_h2(a1), gsc[j][1]));
-            a3 = h2_bits(__hmul2(bits_h2(a3), gsc[j][1]));
+#pragma unroll
+          for (int bt = 0; bt < kNB8; ++bt) {
+            if constexpr (kGroups)
+              ptx::mma_f16(accg[j][bt], a0, a1, a2, a3, bx[bt].x, bx[bt].y);
+            else if constexpr (kA16)
+              ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, bx[bt].x, bx[bt].y);
           }
+        }
+      }
+      if constexpr (kGroups) {  // the stage is one 128-k group: acc += s_group x (sum q x) per column
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int bt = 0; bt < kNB8; ++bt)
-            if constexpr (kA16) ptx::mma_f16(acc[j][bt], a0, a1, a2, a3, bx[bt].x, bx[bt].y);
-        }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[j][bt][q] = fmaf(accg[j][bt][q], __low2float(gsc[j][q >> 1]), acc[j][bt][q]);
+              accg[j][bt][q] = 0.f;
+            }
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&hd.empty[s]);

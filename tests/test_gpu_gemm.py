@@ -183,8 +183,8 @@ def test_int8_group_quantisation_bit_exact(N, K):
                                           (1000, 300, 3, 0), (4096, 4096, 8, 0), (16384, 4096, 16, 0),
                                           (512, 4096, 2, 1), (512, 4096, 2, 4), (512, 4096, 2, 16)])
 def test_int8_group_w8a16_gemm(N, K, B, ksplit):
-    """W8A16 with K-group scales: y = sum_k fp16(q s_group) x_k, fp32 accumulation -- within
-    2e-3 * sum|w_eff x| + 1e-3 of the oracle's fp64 sum over the same fp16 effective weights, for
+    """W8A16 with K-group scales: y = sum_g s_g sum_{k in g} q_k x_k (each group's exact int8 x fp16
+    products in fp32, scaled per group) -- within 2e-3 * sum|q s x| + 1e-3 of the oracle's fp64 sum, for
     every split (a split boundary is a group boundary) and both x plans."""
     rng = np.random.default_rng(N * 7 + K + B)
     W = (rng.standard_normal((N, K)) * 0.05 * np.exp(rng.standard_normal((N, K)))).astype(np.float16)
