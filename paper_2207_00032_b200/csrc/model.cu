@@ -1000,6 +1000,7 @@ struct Enqueuer {
       ops::prefill_embed(pe, s);
       ++launches;
     }
+    const bool pf_pdl = std::getenv("DSINF_PREFILL_NOPDL") == nullptr;
     auto ln = [&](Shard& sh, const __half* g, const __half* b) {  // LayerNorm rows -> GEMM-ready x
       ops::PrepParams pp{};
       pp.mode = i8 ? ops::PREP_LN_I8 : ops::PREP_LN_F16;
@@ -1011,7 +1012,7 @@ struct Enqueuer {
       pp.out_scale = sh.pf.xs;
       pp.B = M;
       pp.K = h;
-      ops::row_prep(pp, s, false);
+      ops::row_prep(pp, s, pf_pdl);
       ++launches;
     };
     auto quant = [&](Shard& sh, const __half* x, int K) {  // int8: per-row quantisation of an fp16 activation
@@ -1023,7 +1024,7 @@ struct Enqueuer {
       pp.out_scale = sh.pf.xs;
       pp.B = M;
       pp.K = K;
-      ops::row_prep(pp, s, false);
+      ops::row_prep(pp, s, pf_pdl);
       ++launches;
     };
     auto gemm = [&](Shard& sh, tc::Params& p, const void* x, const void* w, const float* ws, int N, int K) {
@@ -1033,7 +1034,10 @@ struct Enqueuer {
       tc::make_maps(p, x, K * eb, w, K * eb, eb);
       p.x_scale = sh.pf.xs;
       p.w_scale = ws;
-      tc::launch(p, i8, s);
+      // split-K (one row tile) launches under PDL: the weight ring fills during the previous kernel's
+      // tail, except when this layer's row-major weights were just rewritten by the repack
+      p.w_early = sh.rm_per_layer ? 0 : 1;
+      tc::launch(p, i8, s, pf_pdl);
       ++launches;
     };
     // row-parallel output: t == 1 -> residual += y + bias in the epilogue; t > 1 -> partial, all-reduce,

@@ -10,6 +10,7 @@
 //               owns the 32 TMEM lanes of its quarter), dequantise / bias / GeLU / RoPE / residual,
 //               store straight to global.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -343,13 +344,24 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   if (warp == 1) tmem_dealloc(tmem, 2 * kBN);
 }
 
+#ifdef DSINF_DIAG
+// per-CTA phase stamps of the last split-K launch (`make DIAG=1`, tools/tc_stamps.py)
+__device__ unsigned long long g_tc_stamps[4096 * 8];
+#define TC_STAMP(k) (g_tc_stamps[blockIdx.x * 8 + (k)] = ptx::gtimer())
+#else
+#define TC_STAMP(k) ((void)0)
+#endif
+
 // Split-K mode for one row tile (M <= 128, the B = 1 prompt): the weights must stream at HBM rate,
 // so a 128-column tile is split over a cluster of `split` CTAs along K; each accumulates its K range
 // in TMEM, stages the partial tile in its (drained) ring smem, and after a cluster barrier rank r
 // sums the ranks' partials for column chunks r, r + split, ... through DSMEM (rank order) and runs
 // the fused epilogue on them.
-template <bool kInt8>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __grid_constant__ Params p) {
+template <bool kInt8, int kSBN>
+__global__ void __launch_bounds__(kThreads, kSBN == 128 ? 2 : 1) tc_gemm_splitk_kernel(const __grid_constant__ Params p) {
+  constexpr int kSStages = SplitCfg<kSBN>::kStagesS, kSStageBytes = SplitCfg<kSBN>::kStageBytesS;
+  constexpr int kSPartLd = SplitCfg<kSBN>::kPartLd;
+  constexpr int kQ = kSBN == 128 ? 2 : 4;  // ranks whose partial loads are in flight at once (register budget)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSStages * kSStageBytes);
@@ -363,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
   const int kps = (p.k_blocks + S - 1) / S;
   const int kb0 = rank * kps, kb1 = min(p.k_blocks, kb0 + kps);
   const int nk = max(0, kb1 - kb0);
+  if (threadIdx.x == 0) TC_STAMP(0);
   if (threadIdx.x == 0) {
     ptx::prefetch_tensormap(&p.amap);
     ptx::prefetch_tensormap(&p.bmap);
@@ -378,18 +391,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TC_STAMP(1);
   if (warp == 0) {
     if (lane == 0) {
-      ptx::pdl_wait();
       const uint64_t pol_a = ptx::policy_evict_last();
       const uint64_t pol_b = ptx::policy_evict_first();  // each weight byte is read once
+      // weights never depend on the previous kernel: the first ring stages stream before the wait
+      const int pre = p.w_early ? min(nk, kSStages) : 0;
+      for (int i = 0; i < pre; ++i) {
+        ptx::mbar_arrive_expect_tx(&full[i], kSStageBytes);
+        ptx::tma_load_2d(smem + i * kSStageBytes + kABytes, &p.bmap, (kb0 + i) * kBK, n0, &full[i], pol_b);
+      }
+      ptx::pdl_wait();
+      TC_STAMP(2);
       for (int i = 0; i < nk; ++i) {
         const int st = i % kSStages;
-        ptx::mbar_wait(&empty[st], ((i / kSStages) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[st], kSStageBytes);
         uint8_t* sa = smem + st * kSStageBytes;
+        if (i >= pre) {
+          ptx::mbar_wait(&empty[st], ((i / kSStages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[st], kSStageBytes);
+          ptx::tma_load_2d(sa + kABytes, &p.bmap, (kb0 + i) * kBK, n0, &full[st], pol_b);
+        }
         ptx::tma_load_2d(sa, &p.amap, (kb0 + i) * kBK, 0, &full[st], pol_a);
-        ptx::tma_load_2d(sa + kABytes, &p.bmap, (kb0 + i) * kBK, n0, &full[st], pol_b);
       }
     }
   } else if (warp == 1) {
@@ -401,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
         const int st = i % kSStages;
         ptx::mbar_wait(&full[st], (i / kSStages) & 1);
         tc_fence_after();
+        if (i == 0) TC_STAMP(3);
         const uint32_t sa = ptx::smem_u32(smem + st * kSStageBytes);
         const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
 #pragma unroll
@@ -409,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
                      (i | k) != 0 ? 1u : 0u);
         mma_commit(&empty[st]);
       }
+      TC_STAMP(4);
       mma_commit(acc_ready);
     }
   }
@@ -417,10 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
   const int quarter = warp & 3;
   const int row = quarter * 32 + lane;  // epilogue warps 2..5: TMEM lane quarter = warp % 4
   if (warp >= 2) {
+    ptx::pdl_wait();  // the epilogue reads / writes activations of the previous kernels
     if (nk > 0) {
       ptx::mbar_wait(acc_ready, 0);
       tc_fence_after();
     }
+    if (threadIdx.x == 64) TC_STAMP(5);
 #pragma unroll 1
     for (int c = 0; c < kSBN / 32; ++c) {
       uint32_t v[32];
@@ -437,45 +464,52 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_splitk_kernel(const __gri
   }
   tc_fence_before();
   ptx::cluster_sync();  // every rank's partial tile is in its smem
+  if (threadIdx.x == 64) TC_STAMP(6);
   if (warp >= 2 && row < p.M) {
     for (int c = rank; c < kSBN / 32; c += S) {
       if (n0 + c * 32 >= p.N) break;
       uint32_t v[32];
-      if constexpr (kInt8) {
-        int acc[32];
+      // sum of the S partials of this 32-column chunk, in the fixed order rank, rank + 1, ... (mod S):
+      // every rank starts on a different peer, so no CTA's shared memory serves the whole cluster at
+      // once; 16 columns x up to 4 ranks of loads in flight per round (deterministic: the chunk's
+      // owner and order never change)
+      uint32_t acc[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0;
-        for (int r = 0; r < S; ++r) {
-          const uint32_t base = ptx::map_shared_rank(part + row * kSPartLd + c * 32, r);
+      for (int j = 0; j < 32; ++j) acc[j] = 0u;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const uint4 u = ld_dsmem_u4(base + j * 4);
-            acc[j] += static_cast<int>(u.x);
-            acc[j + 1] += static_cast<int>(u.y);
-            acc[j + 2] += static_cast<int>(u.z);
-            acc[j + 3] += static_cast<int>(u.w);
-          }
+      for (int hh = 0; hh < 2; ++hh) {
+        for (int r0 = 0; r0 < S; r0 += 4) {
+          uint4 u[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (r0 + q < S) {
+              int peer = rank + r0 + q;
+              peer -= peer >= S ? S : 0;
+              const uint32_t base = ptx::map_shared_rank(part + row * kSPartLd + c * 32 + hh * 16, peer);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) u[q][j] = ld_dsmem_u4(base + j * 16);
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (r0 + q < S) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t w4[4] = {u[q][j].x, u[q][j].y, u[q][j].z, u[q][j].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  uint32_t& d = acc[hh * 16 + 4 * j + e];
+                  if constexpr (kInt8)
+                    d = static_cast<uint32_t>(static_cast<int>(d) + static_cast<int>(w4[e]));
+                  else
+                    d = __float_as_uint(__uint_as_float(d) + __uint_as_float(w4[e]));
+                }
+              }
+            }
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = static_cast<uint32_t>(acc[j]);
-      } else {
-        float acc[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        for (int r = 0; r < S; ++r) {  // rank order: deterministic
-          const uint32_t base = ptx::map_shared_rank(part + row * kSPartLd + c * 32, r);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const uint4 u = ld_dsmem_u4(base + j * 4);
-            acc[j] += __uint_as_float(u.x);
-            acc[j + 1] += __uint_as_float(u.y);
-            acc[j + 2] += __uint_as_float(u.z);
-            acc[j + 3] += __uint_as_float(u.w);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc[j]);
       }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = acc[j];
+      if (threadIdx.x == 64 && c == rank) TC_STAMP(7);
       epilogue32<kInt8>(p, row, n0 + c * 32, v);
     }
   }
@@ -515,6 +549,33 @@ void byte_map(CUtensorMap* map, const void* base, int rows, int row_bytes, int l
 
 int sm_count();
 
+void configure();
+
+// co-resident clusters of `sp` CTAs of the 256-column split-K kernel (cached per size)
+int split_clusters(int sp) {
+  static int cache[9] = {0};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache[sp] == 0) {
+    configure();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(sp * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = SplitCfg<256>::kSmem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = sp;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    DSINF_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, tc_gemm_splitk_kernel<false, 256>, &cfg));
+    cache[sp] = std::max(1, n);
+  }
+  return cache[sp];
+}
+
 void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld_bytes, int elem_bytes) {
   if (p.M < 1 || p.N < 1 || p.K < 1) throw ConfigError("tc_gemm: gemm shape dims must be positive");
   const int kbytes = p.K * elem_bytes;
@@ -522,16 +583,32 @@ void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld
   byte_map(&p.amap, x, p.M, kbytes, x_ld_bytes, kBM);
   const int m_tiles = (p.M + kBM - 1) / kBM;
   p.pair = m_tiles >= 2 && !std::getenv("DSINF_TC_NOPAIR");
-  // one row tile: split K over a cluster so that ~2 CTAs per SM stream the weights
+  // one row tile: split K over a cluster so that the weight stream fills every SM
   p.split = 1;
+  // measured (tools/tc_kscan.py, M = 128): the 256-column tile at one CTA per SM matches the 128-column
+  // tile on QKV / MLP-up and loses on the N = 4096 GEMMs (cluster packing leaves 96-132 CTAs), so 128
+  // is the default and DSINF_TC_SBN=256 selects the other
+  p.sbn = 128;
+  if (const char* v = std::getenv("DSINF_TC_SBN")) p.sbn = std::atoi(v) == 256 ? 256 : 128;
   if (m_tiles == 1 && !std::getenv("DSINF_TC_NOSPLIT")) {
-    const int n128 = (p.N + kSBN - 1) / kSBN;
-    // measured: clusters of up to 4 keep two CTAs per SM co-resident; 8-CTA clusters and second
-    // waves are slower
-    while (p.split < 4 && n128 * (2 * p.split) <= 2 * sm_count() && p.k_blocks >= 4 * (2 * p.split)) p.split *= 2;
+    const int nt = (p.N + p.sbn - 1) / p.sbn;
+    if (p.sbn == 128) {
+      // measured: clusters of up to 4 keep two CTAs per SM co-resident; 8-CTA clusters and second
+      // waves are slower
+      while (p.split < 4 && nt * (2 * p.split) <= 2 * sm_count() && p.k_blocks >= 4 * (2 * p.split)) p.split *= 2;
+    } else {
+      // one CTA per SM: the largest cluster (<= 8) whose nt clusters are co-resident in one wave
+      // (cudaOccupancyMaxActiveClusters: clusters are packed per GPC), >= 4 stages per CTA
+      p.split = 1;
+      for (int sp = 2; sp <= 8; ++sp)
+        if (p.k_blocks >= 4 * sp && nt <= split_clusters(sp)) p.split = sp;
+    }
     if (const char* v = std::getenv("DSINF_TC_SPLIT")) p.split = std::max(1, std::min(8, std::atoi(v)));
+    if (std::getenv("DSINF_TC_DEBUG"))
+      std::fprintf(stderr, "tc split-K N=%d K=%d: tile %d split %d clusters(split)=%d\n", p.N, p.K, p.sbn, p.split,
+                   p.sbn == 256 ? split_clusters(std::max(1, p.split)) : -1);
   }
-  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, (p.pair || p.split > 1) ? 128 : kBN);
+  byte_map(&p.bmap, w, p.N, kbytes, w_ld_bytes, p.pair || (p.split > 1 && p.sbn == 128) ? 128 : kBN);
 }
 
 void configure() {
@@ -539,10 +616,14 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmemBytes));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmemBytes));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(tc_gemm_splitk_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  auto split_attrs = [](auto kern, int smem) {
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  };
+  split_attrs(tc_gemm_splitk_kernel<false, 128>, SplitCfg<128>::kSmem);
+  split_attrs(tc_gemm_splitk_kernel<true, 128>, SplitCfg<128>::kSmem);
+  split_attrs(tc_gemm_splitk_kernel<false, 256>, SplitCfg<256>::kSmem);
+  split_attrs(tc_gemm_splitk_kernel<true, 256>, SplitCfg<256>::kSmem);
 }
 
 int sm_count() {
@@ -555,26 +636,36 @@ int sm_count() {
   return n;
 }
 
-void launch(const Params& p, bool int8, cudaStream_t s) {
+void launch(const Params& p, bool int8, cudaStream_t s, bool pdl) {
   const int m_tiles = (p.M + kBM - 1) / kBM, n_tiles = (p.N + kBN - 1) / kBN;
   if (p.split > 1) {
-    const int n128 = (p.N + kSBN - 1) / kSBN;
+    const int nt = (p.N + p.sbn - 1) / p.sbn;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(n128 * p.split);
+    cfg.gridDim = dim3(nt * p.split);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSSmemBytes;
+    cfg.dynamicSmemBytes = p.sbn == 128 ? SplitCfg<128>::kSmem : SplitCfg<256>::kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = p.split;
     attr.val.clusterDim.y = 1;
     attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    if (int8)
-      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<true>, p));
-    else
-      DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<false>, p));
+    cudaLaunchAttribute attrs[2] = {attr, {}};
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = pdl ? 2 : 1;
+    if (p.sbn == 128) {
+      if (int8)
+        DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<true, 128>, p));
+      else
+        DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<false, 128>, p));
+    } else {
+      if (int8)
+        DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<true, 256>, p));
+      else
+        DSINF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tc_gemm_splitk_kernel<false, 256>, p));
+    }
     return;
   }
   if (p.pair) {
@@ -608,3 +699,10 @@ void launch(const Params& p, bool int8, cudaStream_t s) {
 
 }  // namespace tc
 }  // namespace dsinf
+
+#ifdef DSINF_DIAG
+extern "C" int dsinf_debug_tc_stamps(unsigned long long* host, int n) {
+  if (n > 4096 * 8) n = 4096 * 8;
+  return cudaMemcpyFromSymbol(host, dsinf::tc::g_tc_stamps, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -28,11 +28,16 @@ constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 192;        // warp 0 TMA, warp 1 MMA issue + TMEM owner, warps 2..5 epilogue
 constexpr int kEpiThreads = 128;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-// split-K mode (small M): 128 x 128 tiles, 3 stages of 32 KB, two CTAs per SM
-constexpr int kSBN = 128, kSStages = 3;
-constexpr int kSStageBytes = kABytes + kSBN * kBK;
-constexpr int kSPartLd = kSBN + 4;  // fp32 / int32 partial row stride (floats)
-constexpr int kSSmemBytes = kSStages * kSStageBytes + 1024 + 256;
+// split-K mode (small M): 128 x kSBN tiles.  kSBN = 256: 4 stages of 48 KB, one CTA per SM (2/3 of
+// every stage is weights); kSBN = 128: 3 stages of 32 KB, two CTAs per SM.
+template <int kSBN>
+struct SplitCfg {
+  static constexpr int kStagesS = kSBN == 256 ? 4 : 3;
+  static constexpr int kStageBytesS = kABytes + kSBN * kBK;
+  static constexpr int kPartLd = kSBN + 4;  // fp32 / int32 partial row stride (floats)
+  static constexpr int kSmem = kStagesS * kStageBytesS + 1024 + 256;
+  static_assert(kBM * kPartLd * 4 <= kStagesS * kStageBytesS, "partial tile must fit the drained ring");
+};
 
 enum Epi : int {
   EPI_F32 = 0,       // out fp32 = y (+ bias)
@@ -49,8 +54,11 @@ struct Params {
   int k_blocks;                  // ceil(K * elem / 128)
   int pair;                      // cluster-pair mode (set by make_maps: >= 2 row tiles)
   int bf16;                      // 16-bit operands are bfloat16 (kind::f16 with BF16 A/B formats)
-  int split;                     // > 1: split-K mode for one row tile (M <= 128): 128-column tiles, a cluster of
-                                 // `split` CTAs per tile reduces its partials through DSMEM
+  int split;                     // > 1: split-K mode for one row tile (M <= 128): `sbn`-column tiles, a cluster
+                                 // of `split` CTAs per tile reduces its partials through DSMEM
+  int sbn;                       // split-K column tile: 128 (default) or 256
+  int w_early;                   // split-K under PDL: the first ring stages of W are issued before
+                                 // griddepcontrol.wait (W must not be written by the previous kernels)
   const float* x_scale;          // int8: [M]
   const float* w_scale;          // int8: [N]
   const __half* bias;            // optional [N]
@@ -68,7 +76,8 @@ struct Params {
 // Builds the two TMA maps (x and W viewed as byte matrices) and checks alignment.
 void make_maps(Params& p, const void* x, int x_ld_bytes, const void* w, int w_ld_bytes, int elem_bytes);
 void configure();
-void launch(const Params& p, bool int8, cudaStream_t s);
+// pdl: programmatic dependent launch (split-K mode only; the other modes ignore it)
+void launch(const Params& p, bool int8, cudaStream_t s, bool pdl = false);
 
 }  // namespace tc
 }  // namespace dsinf
