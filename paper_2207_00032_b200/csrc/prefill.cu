@@ -150,6 +150,17 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                : "r"(addr));
 }
 
+// 16-byte global -> shared copy without a register round trip (zero-filled when !valid), so a CTA's
+// whole tile load is in flight at once instead of one dependent L2 round trip per loop iteration
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ptx::smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 template <int D>
 __global__ void __launch_bounds__(kFThreads) prefill_attention_mma_kernel(const __grid_constant__ PrefillAttnParams p) {
   constexpr int LD = D + 8;       // smem row stride (halves)
@@ -165,12 +176,12 @@ __global__ void __launch_bounds__(kFThreads) prefill_attention_mma_kernel(const 
   const int hd = p.H * D;
   const int q0 = qb * kFQ;
   const int qn = min(kFQ, p.P - q0);
+#pragma unroll
   for (int i = threadIdx.x; i < kFQ * (D / 8); i += kFThreads) {
     const int r = i / (D / 8), c = (i - r * (D / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < qn) v = __ldcg(reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(b * p.P + q0 + r) * hd + head * D + c));
-    *reinterpret_cast<uint4*>(qs + r * LD + c) = v;
+    cp_async16(qs + r * LD + c, p.q + static_cast<size_t>(b * p.P + q0 + min(r, qn - 1)) * hd + head * D + c, r < qn);
   }
+  cp_async_wait_all();
   __syncthreads();
   // this warp's Q fragments (rows warp*16 .. +16)
   uint32_t qa[KS][4];
@@ -190,16 +201,14 @@ __global__ void __launch_bounds__(kFThreads) prefill_attention_mma_kernel(const 
   for (int t0 = 0; t0 <= last; t0 += kFK) {
     __syncthreads();
     const int tn = min(kFK, last + 1 - t0);
+#pragma unroll
     for (int i = threadIdx.x; i < kFK * (D / 8); i += kFThreads) {
       const int j = i / (D / 8), c = (i - j * (D / 8)) * 8;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-      if (j < tn) {
-        kv = __ldcg(reinterpret_cast<const uint4*>(p.kc + kv0 + static_cast<size_t>(t0 + j) * D + c));
-        vv = __ldcg(reinterpret_cast<const uint4*>(p.vc + kv0 + static_cast<size_t>(t0 + j) * D + c));
-      }
-      *reinterpret_cast<uint4*>(ks + j * LD + c) = kv;
-      *reinterpret_cast<uint4*>(vs + j * LD + c) = vv;
+      const size_t off = kv0 + static_cast<size_t>(t0 + min(j, tn - 1)) * D + c;
+      cp_async16(ks + j * LD + c, p.kc + off, j < tn);
+      cp_async16(vs + j * LD + c, p.vc + off, j < tn);
     }
+    cp_async_wait_all();
     __syncthreads();
     if (q0 + warp * 16 > last) continue;  // warp has no valid query rows (tail block)
     // S = Q K^T over 64 keys: 8 n-tiles of 8 keys
