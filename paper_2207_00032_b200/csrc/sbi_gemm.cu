@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
     // K-group scales of this CTA's stages -> smem [stage][128 columns] (weights: before the wait)
     const int x_region = kLN ? 2 * p.rows_per_split * kKPerRow * 2 : (kXS ? 0 : p.B * p.x_row_words * 4);
     __half* sgs = reinterpret_cast<__half*>(reinterpret_cast<uint8_t*>(sx) + x_region);
-    if constexpr (kA16 != 0) {
-      if (p.w_gscale != nullptr) {
+    if constexpr ((kA16 & 4) != 0) {
+      {
         const int g0 = row_begin / kRowsPerStage;
         for (int i = ctid; i < n_iters * (kColTile / 8); i += 128) {  // 8 columns (16 B) per item
           const int it = i / (kColTile / 8), c8 = (i - it * (kColTile / 8)) * 8;
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       const int g = lane >> 2, t = lane & 3;
       // K-group scales: stage i of this split is group row_begin / kRowsPerStage + i
       // K-group scales from the staged smem copy ([stage][128]; written before the consumer barrier)
-      const __half* gs = p.w_gscale == nullptr ? nullptr : sgs + cw * kWarpCols;
+      const __half* gs = (kA16 & 4) != 0 ? sgs + cw * kWarpCols : nullptr;
       const int gs_valid = kWarpCols;  // out-of-range columns were staged as 0
       if constexpr (kXS) {  // x word pair 2 * (4 kk + t) of batch row r in the stage's two boxes
         c.run_a16(ring, kSB, hd, stages, s, phase, n_iters, cw, lane, [&](int st, int, int kk, int bt) {
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
       }
       float2 ws = make_float2(0.f, 0.f);
       if constexpr (kInt8) {
-        if (kA16 && p.w_gscale != nullptr) {  // K-group scales were applied in the main loop
+        if ((kA16 & 4) != 0) {  // K-group scales were applied in the main loop
           ws = make_float2(1.f, 1.f);
         } else {
           ws.x = __ldg(p.w_scale + n);
@@ -635,6 +635,17 @@ void configure() {
   configure_one<true, 2, 1, 2>();
   configure_one<true, 1, 2, 2>();
   configure_one<true, 2, 2, 2>();
+  // W8A16 with K-group scales (kA16 | 4): signed (drop-in) and biased (model) weights
+  configure_one<true, 1, 0, 5>();
+  configure_one<true, 2, 0, 5>();
+  configure_one<true, 1, 1, 5>();
+  configure_one<true, 2, 1, 5>();
+  configure_one<true, 1, 0, 6>();
+  configure_one<true, 2, 0, 6>();
+  configure_one<true, 1, 1, 6>();
+  configure_one<true, 2, 1, 6>();
+  configure_one<true, 1, 2, 6>();
+  configure_one<true, 2, 2, 6>();
 }
 
 void make_x_map(CUtensorMap* map, const void* x, int words, int B, int ld_words) {
@@ -755,6 +766,7 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
   p.a16 = plan.a16;
   if (p.w_gscale != nullptr && !(int8_weights && plan.a16 && plan.k_groups))
     throw ConfigError("sbi_gemm: K-group scales need int8 weights on a W8A16 plan made with k_groups");
+  if (plan.k_groups && p.w_gscale == nullptr) throw ConfigError("sbi_gemm: a k_groups plan needs the K-group scales");
   p.x_row_words = (plan.a16 ? 2 : 1) * plan.rows_per_split + 8;
   p.ln_inv_k = 1.0 / static_cast<double>(p.K);
   if (p.B < 1 || p.B > kMaxB) throw ConfigError("sbi_gemm: batch must be 1..16 per launch");
@@ -785,7 +797,23 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
     make_x_map(&p.xmap, p.x, plan.a16 ? 2 * p.rows : p.rows, p.B, p.x_ld / (i8x ? 4 : 2));
   }
 #define DSINF_LAUNCH(I8, NB, XS, A16) launch_impl<I8, NB, XS, A16>(p, plan, stream, pdl)
-  if (plan.a16 == 2) {  // biased-weight W8A16
+  if (plan.k_groups) {  // W8A16 with K-group scales: kA16 = 5 (signed) / 6 (biased)
+    const int x = plan.ln_stream ? 2 : (xs ? 1 : 0);
+    if (plan.a16 == 2) {
+      if (plan.nb8 == 1) {
+        if (x == 2) DSINF_LAUNCH(true, 1, 2, 6); else if (x == 1) DSINF_LAUNCH(true, 1, 1, 6); else DSINF_LAUNCH(true, 1, 0, 6);
+      } else {
+        if (x == 2) DSINF_LAUNCH(true, 2, 2, 6); else if (x == 1) DSINF_LAUNCH(true, 2, 1, 6); else DSINF_LAUNCH(true, 2, 0, 6);
+      }
+    } else {
+      if (x == 2) throw ConfigError("sbi_gemm: LayerNorm-streaming K-group plans take biased weights");
+      if (plan.nb8 == 1) {
+        if (x == 1) DSINF_LAUNCH(true, 1, 1, 5); else DSINF_LAUNCH(true, 1, 0, 5);
+      } else {
+        if (x == 1) DSINF_LAUNCH(true, 2, 1, 5); else DSINF_LAUNCH(true, 2, 0, 5);
+      }
+    }
+  } else if (plan.a16 == 2) {  // biased-weight W8A16
     const int x = plan.ln_stream ? 2 : (xs ? 1 : 0);
     if (plan.nb8 == 1) {
       if (x == 2) DSINF_LAUNCH(true, 1, 2, 2); else if (x == 1) DSINF_LAUNCH(true, 1, 1, 2); else DSINF_LAUNCH(true, 1, 0, 2);
