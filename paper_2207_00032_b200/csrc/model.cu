@@ -628,10 +628,16 @@ struct Enqueuer {
 
   // DSINF_PDL_MASK bits: 0 qkv, 1 attention, 2 attn-out, 3 up, 4 down, 5 lm head, 6 the rest,
   // 7 row_prep.
-  // Default 0x8d: QKV, attn-out, MLP-up and row_prep launch early (their weight streams / launch
-  // latency overlap the small kernels before them); early dependents of the full-machine GEMMs
-  // (MLP-down, LM head after a GEMM) steal SM slots and measured slower.
-  int mask = [] { const char* v = std::getenv("DSINF_PDL_MASK"); return v ? static_cast<int>(std::strtol(v, nullptr, 0)) : 0x8d; }();
+  // Default 0xad: QKV, attn-out, MLP-up, the LM head and row_prep launch early (their weight
+  // streams / launch latency overlap the kernels before them; LM head: -2.7 us per step at B=1).
+  // MLP-down launches early only on the 3-stage W8A16 plans (INT8 at B <= 2: GPT-J B=1 1.775 ->
+  // 1.748 ms); elsewhere its early CTAs steal SM slots from MLP-up (int8 B=16 2.62 -> 2.79 ms).
+  // Attention early measured slower everywhere (tools/mask_sweep.sh, profiles/r2_pdl_mask_sweep.log).
+  int mask = [this] {
+    const char* v = std::getenv("DSINF_PDL_MASK");
+    if (v) return static_cast<int>(std::strtol(v, nullptr, 0));
+    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0);
+  }();
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
   int64_t pdl_launches = 0;
