@@ -97,6 +97,7 @@ struct Shard {
   float* xsc = nullptr;    // its per-token scales [B]
   long long* lnstats = nullptr;  // [2L+1][kLnSlotWords]: LayerNorm row sums from the producing epilogue
   unsigned* amax = nullptr;      // [2L][kAmaxSlotWords]: int8 activation row max from the producer
+  unsigned* head_ctr = nullptr;  // [L][Hl]: QKV attention-tail piece counters (m.attn_fuse; zero at rest)
   gemm::Plan plan_qkv{}, plan_o{}, plan_up{}, plan_down{}, plan_lm{};
   PrefillBufs pf;
   bool rm_ready = false;
@@ -154,6 +155,9 @@ struct dsinf_model {
   // TP = 1: the attn-out / MLP-down epilogues add the residual and emit the next LayerNorm's
   // row sums, so the LN prologues skip their full-row statistics pass (DSINF_FUSE_STATS=0: off)
   bool fuse_ln = false;
+  // QKV attention tail (Deep-Fusion region 2 in the QKV launch, LayerNorm-streaming plan): no
+  // standalone attention launch.  Opt-in (DSINF_ATTN_FUSE=1; DSINF_ATTN_FUSE_MAXB batch cap, 8)
+  bool attn_fuse = false;
   // TP > 1 without NCCL kernels between the GEMMs: the row-parallel GEMMs push their partials into
   // every rank's slots and signal a counter; the next LayerNorm prologue waits and sums the slots
   bool fused_ar = false;
@@ -392,6 +396,10 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
     sh.xsc = m.alloc_n<float>(B);
   }
   if (m.q8()) sh.amax = m.alloc_n<unsigned>(std::max<int64_t>(1, 2 * m.L) * gemm::kAmaxSlotWords);
+  if (m.attn_fuse) {
+    sh.head_ctr = m.alloc_n<unsigned>(std::max<int64_t>(1, m.L) * Hl);
+    DSINF_CUDA_CHECK(cudaMemsetAsync(sh.head_ctr, 0, std::max<int64_t>(1, m.L) * Hl * sizeof(unsigned), s));
+  }
   const bool i8 = m.int8;
   const bool kg = m.rt.int8_group != 0;
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
@@ -800,10 +808,18 @@ struct Enqueuer {
     p.heads = static_cast<int>(m.Hl);
     p.head_dim = static_cast<int>(m.d);
     p.max_seq = m.max_ctx;
+    if (m.attn_fuse) {  // the attention of every head runs in the tail of the cluster completing it
+      p.attn_tail = 1;
+      p.head_ctr = sh.head_ctr + static_cast<int64_t>(l) * m.Hl;
+      p.attn_out = sh.a;
+      p.attn_amax = amslot(sh, 2 * l);
+      p.attn_scale = 1.0f / std::sqrt(static_cast<float>(m.d));
+    }
     gemm_launch(p, sh.plan_qkv, m.int8, 0);
   }
 
   void k2_attn(Shard& sh, int l) {
+    if (m.attn_fuse) return;  // ran in the QKV launch's tail
     ops::AttnParams a{};
     const size_t layer_kv = static_cast<size_t>(m.B) * m.Hl * m.max_ctx * m.d;
     a.q = sh.q;
@@ -1488,6 +1504,14 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       m->down_flags = m->t == 1 && m->xs_od && !m->q8g(3) && dfv != nullptr && std::atoi(dfv) != 0;
       const bool ls_default = m->int8 ? m->B <= 2 : m->B <= 8;
       m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : ls_default);
+      {
+        const char* afv = std::getenv("DSINF_ATTN_FUSE");
+        const char* amb = std::getenv("DSINF_ATTN_FUSE_MAXB");
+        const int maxb = amb ? std::atoi(amb) : 8;
+        m->attn_fuse = m->ln_stream && !m->q8g(0) && rt->int8_group == 0 && !rt->use_step_kernel && m->B <= maxb &&
+                       m->d % 8 == 0 && m->d <= 256 && (m->int8 ? m->a16g(0) : true) &&
+                       afv != nullptr && std::atoi(afv) != 0;  // opt-in: measured slower (DESIGN 3.2)
+      }
       // fused all-reduce: on-device shards (DSINF_TP_LOCAL) or CUDA-IPC peer mappings across
       // processes; the per-CTA LayerNorm prologue path (slice plan) consumes the slots, the row_prep
       // path handles the LM head.  Opt-in (DSINF_FUSED_AR=1): on one device the explicit local reduction is cheaper (every

@@ -28,6 +28,7 @@
 #include "ptx.cuh"
 #include "sbi_gemm.cuh"
 #include "sbi_gemm_dev.cuh"
+#include "attn_dev.cuh"
 
 namespace dsinf {
 namespace gemm {
@@ -35,6 +36,134 @@ namespace gemm {
 namespace {
 
 using dev::Header;
+
+// ---------------------------------------------------------------- QKV attention tail (kXS == 3)
+// Deep-Fusion region 2 inside the QKV launch: the cluster whose epilogue
+// completes a head's q, k and v columns runs that head's decode attention (the standalone kernel's
+// online-softmax chunk, attn_dev.cuh, and its DSMEM chunk merge), so no attention launch and no
+// grid drain sit between QKV and attn-out.
+constexpr int kTailMaxHeads = 16;  // heads one column tile can complete (q/k/v sections, d >= 8)
+
+// column tiles overlapping columns [lo, hi) of the QKV output
+__device__ __forceinline__ int tiles_over(int lo, int hi) { return (hi - 1) / kColTile - lo / kColTile + 1; }
+
+// One (head, batch row): this CTA's context chunk, then the nsplit chunks merged through DSMEM
+// (merge_chunks_and_store's arithmetic, attention.cu) into attn_out.  Every thread of the CTA
+// calls it (the cluster barriers); the 128 consumer threads compute.
+template <int TPP>
+__device__ __forceinline__ void attn_tail_one(const Params& p, int head, int b, int split, int nsplit, float* scr, int ctx) {
+  constexpr int PPR = ops::dev::kAttnThreads / TPP;
+  ops::AttnParams a{};
+  a.q = p.q_out;
+  a.kc = p.k_cache;
+  a.vc = p.v_cache;
+  a.pos = p.pos;
+  a.B = p.B;
+  a.H = p.heads;
+  a.d = p.head_dim;
+  a.max_seq = p.max_seq;
+  a.scale = p.attn_scale;
+  const int d = p.head_dim;
+  const int tid = static_cast<int>(threadIdx.x) - 32;  // consumer index, < 0 on the producer warp
+  const int chunk = (ctx + nsplit - 1) / nsplit;
+  const int j0 = split * chunk, j1 = min(ctx, j0 + chunk);
+  if (tid >= 0) ops::dev::attn_chunk<TPP>(a, b, head, j0, j1, tid, scr, [] { dev::consumer_bar(); });
+  float* co = scr + PPR * d + 2 * PPR;
+  float* cst = co + d;
+  if (nsplit > 1)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
+  if (tid >= 0) {
+    // the ranks' (max, sum) re-read from DSMEM where needed: no per-rank register arrays (the
+    // kernel's register budget is the GEMM main loop's, 3 CTAs per SM)
+    float MM = -INFINITY;
+    for (int r = 0; r < nsplit; ++r) MM = fmaxf(MM, ptx::ld_dsmem_f2_nc(ptx::map_shared_rank(&cst[0], r)).x);
+    float LL = 0.f;
+    for (int r = 0; r < nsplit; ++r) {
+      const float2 v = ptx::ld_dsmem_f2_nc(ptx::map_shared_rank(&cst[0], r));
+      LL += (v.x == -INFINITY ? 0.f : expf(v.x - MM)) * v.y;
+    }
+    const float inv = 1.0f / LL;
+    const int hd = p.heads * d;
+    float amax = 0.f;
+    for (int i = split + nsplit * tid; i < d; i += nsplit * ops::dev::kAttnThreads) {
+      float acc = 0.f;
+      for (int r = 0; r < nsplit; ++r) {
+        const float mr = ptx::ld_dsmem_f2_nc(ptx::map_shared_rank(&cst[0], r)).x;
+        const float w = mr == -INFINITY ? 0.f : expf(mr - MM);
+        acc = fmaf(w, ptx::ld_dsmem_f_nc(ptx::map_shared_rank(&co[i], r)), acc);
+      }
+      const __half o = __float2half_rn(acc * inv);
+      p.attn_out[static_cast<size_t>(b) * hd + head * d + i] = o;
+      amax = fmaxf(amax, fabsf(__half2float(o)));
+    }
+    if (p.attn_amax != nullptr) {  // per-token int8 scale input of the attn-out GEMM
+      const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
+      if ((tid & 31) == 0 && mx != 0) atomicMax(p.attn_amax + ((head + split) % kStatStripes) * 32 + b, mx);
+    }
+  }
+  // peers' DSMEM reads of our partials are consumed before the scratch is reused
+  if (nsplit > 1)
+    ptx::cluster_sync_relaxed();
+  else
+    __syncthreads();
+}
+
+// After the epilogue: count this tile's (section, head) pieces; run the heads it completes.
+__device__ __forceinline__ void attn_tail(const Params& p, uint8_t* ring, int tile, int split, int nsplit) {
+  __shared__ int s_heads[kTailMaxHeads + 1];  // [0] = count (read by the peers through DSMEM)
+  if (nsplit > 1)
+    ptx::cluster_sync();  // every CTA's epilogue stores precede rank 0's release below
+  else
+    __syncthreads();
+  if (split == 0 && threadIdx.x == 0) {
+    const int d = p.head_dim, hd = p.heads * d, n0 = tile * kColTile;
+    int cnt = 0;
+    __threadfence();
+    for (int sec = 0; sec < 3; ++sec) {
+      const int lo = max(n0, sec * hd), hi = min(min(n0 + kColTile, p.N), (sec + 1) * hd);
+      if (lo >= hi) continue;
+      for (int h = (lo - sec * hd) / d; h <= (hi - 1 - sec * hd) / d; ++h) {
+        int need = 0;
+        for (int s2 = 0; s2 < 3; ++s2) need += tiles_over(s2 * hd + h * d, s2 * hd + (h + 1) * d);
+        const unsigned old = atomicAdd(p.head_ctr + h, 1u);
+        if (old + 1 == static_cast<unsigned>(need)) {
+          p.head_ctr[h] = 0u;  // every piece of this step arrived: reset for the next step
+          if (cnt < kTailMaxHeads) s_heads[1 + cnt++] = h;
+        }
+      }
+    }
+    __threadfence();  // acquire the other clusters' q / k / v stores before the peers read them
+    s_heads[0] = cnt;
+  }
+  if (nsplit > 1)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
+  // rank 0's head list (read per head below: no dynamically indexed local array)
+  auto list_at = [&](int i) {
+    return nsplit > 1 ? __float_as_int(ptx::ld_dsmem_f_nc(ptx::map_shared_rank(&s_heads[i], 0))) : s_heads[i];
+  };
+  const int cnt = list_at(0);
+  if (cnt == 0) {
+    if (nsplit > 1) ptx::cluster_sync_relaxed();  // rank 0's head list is read before it exits
+    return;
+  }
+  const int ctx = *p.pos + 1;
+  float* scr = reinterpret_cast<float*>(ring + 16 * 1024);  // past the split-K partials (<= 8.4 KB)
+  for (int i = 0; i < cnt; ++i) {
+    const int head = list_at(1 + i);
+    for (int b = 0; b < p.B; ++b) {
+      if (p.head_dim <= 64)
+        attn_tail_one<8>(p, head, b, split, nsplit, scr, ctx);
+      else if (p.head_dim <= 128)
+        attn_tail_one<16>(p, head, b, split, nsplit, scr, ctx);
+      else
+        attn_tail_one<32>(p, head, b, split, nsplit, scr, ctx);
+    }
+  }
+}
 
 // Dynamic smem (base rounded up to 1024 B for the 128B swizzle):
 //   [ring: stages x 16 KB] [header 1 KB] [x slice: B rows x x_row_words words]
@@ -45,9 +174,9 @@ using dev::Header;
 // kXS: 0 smem x slice, 1 x-streaming, 2 LayerNorm-streaming (fp32 residual boxes per stage,
 // normalised by the consumers into the stage's fp16 x boxes; fp16 or W8A16 weights).
 template <bool kInt8, int kNB8, int kXS, int kA16>
-__global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, kXS == 3 ? 3 : 1) sbi_gemm_kernel(const __grid_constant__ Params p) {
   static_assert(!kA16 || kInt8, "W8A16 needs int8 weights");
-  constexpr bool kLN = kXS == 2;
+  constexpr bool kLN = kXS >= 2;  // 3: LayerNorm-streaming + the QKV attention tail
   static_assert(!kLN || !kInt8 || kA16, "LayerNorm-streaming takes fp16 or W8A16 weights");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -485,7 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1) sbi_gemm_kernel(const __grid_cons
   }
   // keep our smem alive until the peers' DSMEM reads are done (their values are consumed before
   // they arrive, so no release ordering -- and no GPU-scope fence over our epilogue stores -- needed)
-  if (nsplit > 1) ptx::cluster_sync_relaxed();
+  if constexpr (kXS == 3) {
+    attn_tail(p, ring, tile, split, nsplit);  // its cluster barriers also keep our partials alive
+  } else {
+    if (nsplit > 1) ptx::cluster_sync_relaxed();
+  }
   ptx::trace_end(p.trace);
   if (clog && threadIdx.x == 0) clog[5] = ptx::gtimer();
 }
@@ -635,6 +768,11 @@ void configure() {
   configure_one<true, 2, 1, 2>();
   configure_one<true, 1, 2, 2>();
   configure_one<true, 2, 2, 2>();
+  // LayerNorm-streaming QKV with the attention tail (kXS = 3): fp16 and biased W8A16
+  configure_one<false, 1, 3, 0>();
+  configure_one<false, 2, 3, 0>();
+  configure_one<true, 1, 3, 2>();
+  configure_one<true, 2, 3, 2>();
   // W8A16 with K-group scales (kA16 | 4): signed (drop-in) and biased (model) weights
   configure_one<true, 1, 0, 5>();
   configure_one<true, 2, 0, 5>();
@@ -797,7 +935,17 @@ void launch(const Params& p_in, const Plan& plan, bool int8_weights, cudaStream_
     make_x_map(&p.xmap, p.x, plan.a16 ? 2 * p.rows : p.rows, p.B, p.x_ld / (i8x ? 4 : 2));
   }
 #define DSINF_LAUNCH(I8, NB, XS, A16) launch_impl<I8, NB, XS, A16>(p, plan, stream, pdl)
-  if (plan.k_groups) {  // W8A16 with K-group scales: kA16 = 5 (signed) / 6 (biased)
+  if (p.attn_tail) {  // QKV + attention tail: LayerNorm-streaming fp16 or biased W8A16 only
+    if (!plan.ln_stream || plan.k_groups || (plan.a16 != 0 && plan.a16 != 2) || (int8_weights && !plan.a16) ||
+        p.epi != EPI_QKV || p.head_ctr == nullptr || p.attn_out == nullptr || p.head_dim % 8 != 0 ||
+        p.head_dim > 256)
+      throw ConfigError("sbi_gemm: the attention tail needs the LayerNorm-streaming QKV plan (fp16 / biased W8A16)");
+    if (plan.a16) {
+      if (plan.nb8 == 1) DSINF_LAUNCH(true, 1, 3, 2); else DSINF_LAUNCH(true, 2, 3, 2);
+    } else {
+      if (plan.nb8 == 1) DSINF_LAUNCH(false, 1, 3, 0); else DSINF_LAUNCH(false, 2, 3, 0);
+    }
+  } else if (plan.k_groups) {  // W8A16 with K-group scales: kA16 = 5 (signed) / 6 (biased)
     const int x = plan.ln_stream ? 2 : (xs ? 1 : 0);
     if (plan.a16 == 2) {
       if (plan.nb8 == 1) {

@@ -123,6 +123,17 @@ struct Params {
   const float2* rope;  // [max_seq][head_dim/2] (cos, sin)
   const int* pos;
   int heads, head_dim, max_seq;
+  // EPI_QKV attention tail (Deep-Fusion region 2 inside the QKV launch, LayerNorm-streaming plan):
+  // after its epilogue a cluster bumps head_ctr[h] for every head its column tile touches (q, k or v
+  // section); the cluster completing a head runs that head's decode attention over positions
+  // 0..*pos, its nsplit CTAs splitting the context and merging through DSMEM, and writes attn_out
+  // [B][heads*head_dim] fp16 (+ attn_amax row max |out| stripes when non-null).  The standalone
+  // attention launch is skipped.  head_ctr: [heads] per layer, zero at rest (the completer resets).
+  int attn_tail;
+  unsigned* head_ctr;
+  __half* attn_out;
+  unsigned* attn_amax;
+  float attn_scale;
   long long* ln_stats_out;  // EPI_RESID: accumulate the new residual's row sums (slot, zeroed per step)
   unsigned* amax_out;       // EPI_F16 / EPI_GELU_F16: accumulate row max |out|
   // fused all-reduce (producer side, EPI_F32): the partial [B][N] goes to push_dst[q] (rank q's slot

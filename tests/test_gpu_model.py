@@ -506,3 +506,33 @@ def test_down_flag_dependency(dtype_bytes, batch, int8_act, monkeypatch):
     assert np.array_equal(outs[0][0], outs[1][0])
     monkeypatch.setenv("DSINF_DOWN_FLAGS", "1")
     run_parity(512, 2, 8, 1000, batch=batch, dtype_bytes=dtype_bytes, int8_act=int8_act)
+
+
+@pytest.mark.parametrize("hidden,heads,dtype_bytes,batch,int8_act", [(512, 4, 2, 1, 0), (512, 8, 2, 3, 0),
+                                                                     (768, 8, 2, 1, 0),
+                                                                     (512, 4, 1, 1, capi.INT8_W8A16),
+                                                                     (512, 8, 1, 2, capi.INT8_W8A16)])
+def test_qkv_attention_tail(hidden, heads, dtype_bytes, batch, int8_act, monkeypatch):
+    """DSINF_ATTN_FUSE=1: decode attention runs in the tail of the QKV launch (the cluster completing a
+    head's q / k / v column tiles attends for it, its K splits merging the context chunks through
+    DSMEM); one launch per layer fewer, same tokens as the standalone attention and the oracle.  Head
+    dims 128, 64 and 96 (768 / 8: tiles straddle heads)."""
+    rng = np.random.default_rng(53)
+    prompt = rng.integers(0, 1000, (batch, 5)).astype(np.int32)
+    outs, launches = [], []
+    for f in ("0", "1"):
+        monkeypatch.setenv("DSINF_ATTN_FUSE", f)
+        m = DecoderModel(hidden, 3, heads, 1000, dtype_bytes=dtype_bytes, batch=batch, max_ctx=40, seed=SEED,
+                         int8_act=int8_act)
+        m.set_prompt(prompt)
+        m.step(20)  # graph replays: the head counters must return to zero every step
+        torch.cuda.synchronize()
+        outs.append((m.full_logits(), m.read_tokens()[1]))
+        launches.append(m.get_info().kernels_per_step)
+        m.close()
+    (la, ha), (lb, hb) = outs
+    assert launches[0] - launches[1] == 3, launches
+    assert np.array_equal(ha, hb)
+    assert float(np.abs(la - lb).max()) <= 2e-3 * float(np.abs(la).max()) + 1e-3
+    monkeypatch.setenv("DSINF_ATTN_FUSE", "1")
+    run_parity(hidden, 2, heads, 1000, batch=batch, dtype_bytes=dtype_bytes, int8_act=int8_act)
