@@ -416,8 +416,12 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
       DSINF_CUDA_CHECK(cudaMemsetAsync(w.up_flags, 0, sizeof(unsigned) * sh.plan_up.col_tiles, s));
     }
   }
+  // LM head ring depth (DSINF_LM_STAGES; 0 = the plan's own): 2 at B <= 8, where the shallower ring
+  // fits more CTAs per SM (GPT-J int8 B=1 1.738 -> 1.724 ms, fp16 2.531 -> 2.521, fp16 B=8 2.811 ->
+  // 2.797; B=16 neutral; profiles/r2_lm_stages_sweep.log)
+  const int lm_stages = [&] { const char* v = std::getenv("DSINF_LM_STAGES"); return v ? std::atoi(v) : (B <= 8 ? 2 : 0); }();
   sh.plan_lm = gemm::make_plan(static_cast<int>(m.Vl), static_cast<int>(h), B, false, 0, m.xs_lm, false,
-                               m.ln_stream && m.xs_lm);
+                               m.ln_stream && m.xs_lm, false, false, lm_stages);
 }
 
 // Row-major copies of the layer GEMM weights for the tensor-core prefill (same synthetic values;

@@ -816,7 +816,7 @@ bool x_streamable(const void* x, int x_ld, int K, bool int8_x) {
 // so that the whole grid is ONE wave of co-resident clusters (every CTA starts streaming at
 // once, no tail wave) and reduces the split in-cluster.
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream, bool a16, bool ln_stream,
-               bool a16_biased, bool k_groups) {
+               bool a16_biased, bool k_groups, int stage_cap) {
   if (N < 1 || K < 1 || B < 1 || B > kMaxB) throw ConfigError("sbi_gemm: bad shape");
   if (a16 && !int8_weights) throw ConfigError("sbi_gemm: W8A16 needs int8 weights");
   if (ln_stream && (!x_stream || (int8_weights && !a16)))
@@ -853,7 +853,8 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   };
   // ring depth: 4 stages; W8A16 at B <= 2 takes 3 (GPT-J int8 B=1 1.868 -> 1.838 ms; B=8: 2.187 -> 2.237
   // and B=16: 2.587 -> 2.747 with 3, so larger batches keep 4).  DSINF_STAGES overrides.
-  const int max_stages = std::max(1, std::min(kMaxStages, env_int("DSINF_STAGES", a16 && B <= 2 ? 3 : 4)));
+  int max_stages = std::max(1, std::min(kMaxStages, env_int("DSINF_STAGES", a16 && B <= 2 ? 3 : 4)));
+  if (stage_cap > 0) max_stages = std::min(max_stages, stage_cap);
   const int cap_per_sm = env_int("DSINF_CTA_PER_SM", 0);
   auto smem_for = [&](int s, int* stages_out) {
     const int rps = rps_for(s);
