@@ -402,14 +402,23 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   }
   const bool i8 = m.int8;
   const bool kg = m.rt.int8_group != 0;
+  // per-GEMM ring depth requests (DSINF_STAGES_{QKV,O,UP,DOWN}; 0 = the plan's own).  Measured
+  // defaults at TP = 1, h >= 4096 (GPT-J; profiles/r2_stage_sweep.log): QKV 3 stages for fp16 (B=1
+  // 2.520 -> 2.501 ms, B=8 2.797 -> 2.752, B=16 with MLP-up 2: 3.154 -> 3.123) and W8A16 at B = 8
+  // (2.185 -> 2.148); the LayerNorm-streaming W8A16 MLP-up 4 stages at B <= 2 (B=1 1.723 -> 1.685,
+  // B=2 1.808 -> 1.777).  GPT-2 (h 1600) keeps the plan's own depths (both measured slower there).
+  const bool big = m.t == 1 && h >= 4096;
+  auto st_req = [](const char* name, int dflt) { const char* v = std::getenv(name); return v ? std::atoi(v) : dflt; };
+  const int qkv_st = big && (!i8 || (m.a16g(0) && B > 2 && B <= 8)) ? 3 : 0;
+  const int up_st = big && i8 && m.a16g(2) && m.ln_use(2) && B <= 2 ? 4 : (big && !i8 && B > 8 ? 2 : 0);
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
-                                m.ln_use(0), m.a16g(0), kg);
+                                m.ln_use(0), m.a16g(0), kg, st_req("DSINF_STAGES_QKV", qkv_st));
   sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1), false,
-                              m.a16g(1), kg);
+                              m.a16g(1), kg, st_req("DSINF_STAGES_O", 0));
   sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2),
-                               m.a16g(2), kg);
+                               m.a16g(2), kg, st_req("DSINF_STAGES_UP", up_st));
   sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3), false,
-                                 m.a16g(3), kg);
+                                 m.a16g(3), kg, st_req("DSINF_STAGES_DOWN", 0));
   if (m.down_flags) {
     for (LayerW& w : sh.layers) {
       w.up_flags = m.alloc_n<unsigned>(sh.plan_up.col_tiles);

@@ -854,7 +854,7 @@ Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_
   // ring depth: 4 stages; W8A16 at B <= 2 takes 3 (GPT-J int8 B=1 1.868 -> 1.838 ms; B=8: 2.187 -> 2.237
   // and B=16: 2.587 -> 2.747 with 3, so larger batches keep 4).  DSINF_STAGES overrides.
   int max_stages = std::max(1, std::min(kMaxStages, env_int("DSINF_STAGES", a16 && B <= 2 ? 3 : 4)));
-  if (stage_cap > 0) max_stages = std::min(max_stages, stage_cap);
+  if (stage_cap > 0) max_stages = std::min(kMaxStages, stage_cap);  // per-GEMM ring depth request
   const int cap_per_sm = env_int("DSINF_CTA_PER_SM", 0);
   auto smem_for = [&](int s, int* stages_out) {
     const int rps = rps_for(s);

@@ -187,7 +187,7 @@ void make_weight_map(CUtensorMap* map, const void* w_packed, int N, int rows);
 void configure();
 // a16_biased: the W8A16 weights are stored biased (s + 128 per byte; the decode model's own weights)
 // k_groups: W8A16 with K-group scales (the CTA's group scales are staged in shared memory)
-// stage_cap > 0: at most that many ring stages (the LM head's plan)
+// stage_cap > 0: that many ring stages (at most; per-GEMM request from the model)
 Plan make_plan(int N, int K, int B, bool int8_weights, int forced_split, bool x_stream = false, bool a16 = false,
                bool ln_stream = false, bool a16_biased = false, bool k_groups = false, int stage_cap = 0);
 // TMA descriptor of x for the x-streaming mode: `words` 32-bit words per row, `B` rows, row
