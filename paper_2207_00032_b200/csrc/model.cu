@@ -657,7 +657,10 @@ struct Enqueuer {
   int mask = [this] {
     const char* v = std::getenv("DSINF_PDL_MASK");
     if (v) return static_cast<int>(std::strtol(v, nullptr, 0));
-    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0);
+    // small fp16 layers (h < 4096, TP = 1, B <= 8: GPT-2 1.5B) leave room for early MLP-down and
+    // attention CTAs: B=1 1.642 -> 1.593 ms, B=8 1.843 -> 1.796 (profiles/r2_gpt2_sweep.log)
+    const bool small16 = !m.int8 && m.h < 4096 && m.t == 1 && m.B <= 8;
+    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0) | (small16 ? 0x12 : 0);
   }();
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
