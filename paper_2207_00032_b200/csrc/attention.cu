@@ -193,12 +193,15 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   const int slot = tid / TPP, lane_in = tid % TPP;
   const int dim0 = lane_in * 8;
   const bool has_dims = dim0 < d;
+  // scores in the log2 domain (q pre-scaled by log2(e)): exp2f is one MUFU.EX2, expf a longer sequence;
+  // the CTA's (max, sum) go back to the natural domain before the chunk merge
+  constexpr float kLog2e = 1.4426950408889634f;
   float q[8];
   if (has_dims) {
     const uint4 qu = __ldcg(reinterpret_cast<const uint4*>(p.q + static_cast<size_t>(b) * p.H * d + head * d + dim0));
     dev::h8_to_f(qu, q);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] *= p.scale;
+    for (int i = 0; i < 8; ++i) q[i] *= p.scale * kLog2e;
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[i] = 0.f;
@@ -206,51 +209,95 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   float m = -INFINITY, l = 0.f, o[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) o[i] = 0.f;
+  const bool all_dims = TPP * 8 == d;  // every lane owns 8 dims (d = 64 / 128 / 256)
+  int rs = 0;                          // ring slot and its parity, advanced per stage
+  uint32_t rph = 0;
   for (int st = 0; st < nst; ++st) {
-    ptx::mbar_wait(&bars[st % R], static_cast<uint32_t>((st / R) & 1));
-    const __half* ks = ring + (st % R) * stage_halves;
+    ptx::mbar_wait(&bars[rs], rph);
+    const __half* ks = ring + rs * stage_halves;
     const __half* vs = ks + static_cast<size_t>(kTmaRows) * d;
     const int rows = min(kTmaRows, n - st * kTmaRows);
-    float sc[kU];
-    float mt = -INFINITY;
+    if (rows == kTmaRows && all_dims) {
+      // full stage, every lane with dims: no per-position predicates
+      float sc[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int r = u * PPR + slot;
-      float sdot = 0.f;
-      if (r < rows && has_dims) {
+      for (int u = 0; u < kU; ++u) {
         float kf[8];
-        dev::h8_to_f(*reinterpret_cast<const uint4*>(ks + static_cast<size_t>(r) * d + dim0), kf);
+        dev::h8_to_f(*reinterpret_cast<const uint4*>(ks + static_cast<size_t>(u * PPR + slot) * d + dim0), kf);
+        float sdot = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) sdot = fmaf(q[i], kf[i], sdot);
+        sc[u] = sdot;
       }
 #pragma unroll
-      for (int off = TPP / 2; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
-      sc[u] = r < rows ? sdot : -INFINITY;
-      mt = fmaxf(mt, sc[u]);
-    }
-    if (mt != -INFINITY) {
+      for (int off = TPP / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < kU; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], off);
+      float mt = sc[0];
+#pragma unroll
+      for (int u = 1; u < kU; ++u) mt = fmaxf(mt, sc[u]);
       const float mn = fmaxf(m, mt);
-      const float corr = expf(m - mn);
+      const float corr = exp2f(m - mn);  // m = -inf on the first stage: 0
       l *= corr;
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] *= corr;
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        if (sc[u] == -INFINITY) continue;
-        const float pj = expf(sc[u] - mn);
+        const float pj = exp2f(sc[u] - mn);
         l += pj;
-        if (has_dims) {
-          float vf[8];
-          dev::h8_to_f(*reinterpret_cast<const uint4*>(vs + static_cast<size_t>(u * PPR + slot) * d + dim0), vf);
+        float vf[8];
+        dev::h8_to_f(*reinterpret_cast<const uint4*>(vs + static_cast<size_t>(u * PPR + slot) * d + dim0), vf);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i]);
-        }
+        for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i]);
       }
       m = mn;
+    } else {
+      float sc[kU];
+      float mt = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int r = u * PPR + slot;
+        float sdot = 0.f;
+        if (r < rows && has_dims) {
+          float kf[8];
+          dev::h8_to_f(*reinterpret_cast<const uint4*>(ks + static_cast<size_t>(r) * d + dim0), kf);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sdot = fmaf(q[i], kf[i], sdot);
+        }
+#pragma unroll
+        for (int off = TPP / 2; off > 0; off >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, off);
+        sc[u] = r < rows ? sdot : -INFINITY;
+        mt = fmaxf(mt, sc[u]);
+      }
+      if (mt != -INFINITY) {
+        const float mn = fmaxf(m, mt);
+        const float corr = exp2f(m - mn);
+        l *= corr;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] *= corr;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (sc[u] == -INFINITY) continue;
+          const float pj = exp2f(sc[u] - mn);
+          l += pj;
+          if (has_dims) {
+            float vf[8];
+            dev::h8_to_f(*reinterpret_cast<const uint4*>(vs + static_cast<size_t>(u * PPR + slot) * d + dim0), vf);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = fmaf(pj, vf[i], o[i]);
+          }
+        }
+        m = mn;
+      }
     }
     __syncthreads();  // every thread is done with this ring slot
     if (tid == 0 && st + R < nst) issue(st + R);
+    if (++rs == R) {
+      rs = 0;
+      rph ^= 1u;
+    }
   }
+  m = m == -INFINITY ? m : m * 0.69314718055994531f;  // back to the natural-log domain
   // merge the PPR position slots of this CTA (attn_chunk's tail)
   if (has_dims) {
 #pragma unroll
