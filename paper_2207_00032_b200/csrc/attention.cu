@@ -25,7 +25,7 @@ using dev::kAttnThreads;
 // Merge the C chunk partials of (b, head) across the cluster through DSMEM and write the output
 // row (and the int8 row max).  co / cst: this CTA's partial (unnormalised output, max, sum).
 __device__ __forceinline__ void merge_chunks_and_store(const AttnParams& p, float* co, float* cst, int head, int b,
-                                                       int c, int C, int tid) {
+                                                       int c, int C, int tid, int nthreads = kAttnThreads) {
   const int d = p.d;
   // merge the C chunks of this (b, head) across the cluster
   if (C > 1)
@@ -60,7 +60,7 @@ __device__ __forceinline__ void merge_chunks_and_store(const AttnParams& p, floa
   const float inv = 1.0f / LL;
   const int hd = p.H * d;
   float amax = 0.f;
-  for (int i = c + C * tid; i < d; i += C * kAttnThreads) {
+  for (int i = c + C * tid; i < d; i += C * nthreads) {
     float part[kMaxC];
 #pragma unroll
     for (int r = 0; r < kMaxC; ++r)
@@ -137,9 +137,15 @@ __host__ __device__ constexpr size_t tma_ring_bytes(int d, int ring = 2) {
   return static_cast<size_t>(ring) * 2 * kTmaRows * d * 2;
 }
 
-template <int TPP>
-__global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __grid_constant__ AttnParams p) {
-  constexpr int PPR = kAttnThreads / TPP;  // positions scored in parallel
+// NT threads per CTA: 128 (default), or 256 (DSINF_ATTN_NT; twice the warps per SM, measured slower)
+template <int TPP, int NT>
+__host__ __device__ constexpr size_t tma_scratch_floats(int d) {
+  return static_cast<size_t>(NT / TPP) * d + 2 * (NT / TPP) + d + 4;
+}
+
+template <int TPP, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 4 : 1) attention_tma_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int PPR = NT / TPP;  // positions scored in parallel
   constexpr int kU = kTmaRows / PPR;       // positions per thread per stage
   extern __shared__ __align__(128) uint8_t araw[];
   const int d = p.d;
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   float* co = sl + PPR;      // [d]
   float* cst = co + d;       // [2]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      araw + tma_ring_bytes<TPP>(d, R) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8);
+      araw + tma_ring_bytes<TPP>(d, R) + (tma_scratch_floats<TPP, NT>(d) * 4 + 7) / 8 * 8);
   const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
   const int tid = threadIdx.x;
   ptx::trace_begin(p.trace);
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
   __syncthreads();
   float M = -INFINITY;
   for (int sidx = 0; sidx < PPR; ++sidx) M = fmaxf(M, sm[sidx]);
-  for (int i = tid; i < d; i += kAttnThreads) {
+  for (int i = tid; i < d; i += NT) {
     float acc = 0.f;
     for (int sidx = 0; sidx < PPR; ++sidx) {
       const float w = sm[sidx] == -INFINITY ? 0.f : expf(sm[sidx] - M);
@@ -325,12 +331,31 @@ __global__ void __launch_bounds__(kAttnThreads) attention_tma_kernel(const __gri
     cst[1] = L;
   }
   __syncthreads();
-  merge_chunks_and_store(p, co, cst, head, b, c, C, tid);
+  merge_chunks_and_store(p, co, cst, head, b, c, C, tid, NT);
 }
 
-template <int TPP>
+template <int TPP, int NT>
 size_t tma_smem_bytes(int d, int ring) {
-  return tma_ring_bytes<TPP>(d, ring) + (dev::attn_scratch_floats<TPP>(d) * 4 + 7) / 8 * 8 + 8 * kTmaMaxRing;
+  return tma_ring_bytes<TPP>(d, ring) + (tma_scratch_floats<TPP, NT>(d) * 4 + 7) / 8 * 8 + 8 * kTmaMaxRing;
+}
+
+template <int TPP, int NT>
+void configure_tma() {
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<TPP, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<TPP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  if (carveout_max())
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<TPP, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+
+template <int NT>
+void launch_tma(const AttnParams& p, dim3 grid, dim3 cluster, cudaStream_t s, bool pdl) {
+  const dim3 block(NT);
+  if (p.d <= 64)
+    launch_pdl(attention_tma_kernel<8, NT>, grid, block, tma_smem_bytes<8, NT>(p.d, p.tma_ring), s, pdl, p, cluster);
+  else if (p.d <= 128)
+    launch_pdl(attention_tma_kernel<16, NT>, grid, block, tma_smem_bytes<16, NT>(p.d, p.tma_ring), s, pdl, p, cluster);
+  else
+    launch_pdl(attention_tma_kernel<32, NT>, grid, block, tma_smem_bytes<32, NT>(p.d, p.tma_ring), s, pdl, p, cluster);
 }
 
 }  // namespace
@@ -355,17 +380,12 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-  if (carveout_max()) {
-    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_tma_kernel<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  }
+  configure_tma<8, 128>();
+  configure_tma<16, 128>();
+  configure_tma<32, 128>();
+  configure_tma<8, 256>();
+  configure_tma<16, 256>();
+  configure_tma<32, 256>();
   // the K/V staging area (<= 48 KB) on top of the softmax scratch
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -396,12 +416,14 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
     p.tma_ring = std::max(2, std::min(p.tma_ring, max_st));
     const char* ev = std::getenv("DSINF_ATTN_EARLY");
     p.early_kv = ev != nullptr && std::atoi(ev) != 0;
-    if (p.d <= 64)
-      launch_pdl(attention_tma_kernel<8>, grid, block, tma_smem_bytes<8>(p.d, p.tma_ring), s, pdl, p, cluster);
-    else if (p.d <= 128)
-      launch_pdl(attention_tma_kernel<16>, grid, block, tma_smem_bytes<16>(p.d, p.tma_ring), s, pdl, p, cluster);
+    // DSINF_ATTN_NT=256: 256 threads per CTA (measured slower at B = 8 / 16: GPT-J int8 B=16 attention
+    // 13.8 -> 15.5 us per layer, fp16 B=8 10.8 -> 12.8; profiles/r2_attn_fastpath_ab.log)
+    const char* ntv = std::getenv("DSINF_ATTN_NT");
+    const int nt = ntv ? std::atoi(ntv) : 128;
+    if (nt == 256)
+      launch_tma<256>(p, grid, cluster, s, pdl);
     else
-      launch_pdl(attention_tma_kernel<32>, grid, block, tma_smem_bytes<32>(p.d, p.tma_ring), s, pdl, p, cluster);
+      launch_tma<128>(p, grid, cluster, s, pdl);
     return;
   }
   // DSINF_ATTN_PREFETCH=1 (with DSINF_ATTN_TMA=0): K/V staging before the dependency wait (a chunk's
