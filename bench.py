@@ -302,9 +302,9 @@ def run_reference(args, preset, rank, world):
 
 def auto_act(batch, tp):
     """The per-GEMM INT8 activation modes DSINF_INT8_AUTO picks (model.cu, dsinf_model_create)."""
-    if batch <= 8:
+    if batch <= 8 or tp == 1:
         return "w8a16"
-    return "w8a8 qkv + w8a16 attn_out/mlp" if tp == 1 else "w8a8"
+    return "w8a8"
 
 
 def workload_config(args, preset, world):

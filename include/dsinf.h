@@ -140,8 +140,8 @@ int dsinf_quantize_activations_int8(const void* x_f16, int64_t B, int64_t K, int
  *        per-output-row dequant -- no activation quantisation on the decode critical path. */
 #define DSINF_INT8_W8A8 0
 #define DSINF_INT8_W8A16 1
-#define DSINF_INT8_AUTO 2 /* runtime config only (measured): W8A16 for batch <= 8; above, W8A8 QKV +
-                             W8A16 attn-out / MLP at TP = 1 and W8A8 everywhere at TP > 1 */
+#define DSINF_INT8_AUTO 2 /* runtime config only (measured): W8A16 at TP = 1 and for batch <= 8; W8A8
+                             everywhere at TP > 1 and batch > 8 */
 
 #define DSINF_EPI_NONE 0
 #define DSINF_EPI_GELU 1 /* tanh GeLU after the bias */

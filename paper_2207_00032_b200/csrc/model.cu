@@ -404,12 +404,12 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   const bool kg = m.rt.int8_group != 0;
   // per-GEMM ring depth requests (DSINF_STAGES_{QKV,O,UP,DOWN}; 0 = the plan's own).  Measured
   // defaults at TP = 1, h >= 4096 (GPT-J; profiles/r2_stage_sweep.log): QKV 3 stages for fp16 (B=1
-  // 2.520 -> 2.501 ms, B=8 2.797 -> 2.752, B=16 with MLP-up 2: 3.154 -> 3.123) and W8A16 at B = 8
-  // (2.185 -> 2.148); the LayerNorm-streaming W8A16 MLP-up 4 stages at B <= 2 (B=1 1.723 -> 1.685,
+  // 2.520 -> 2.501 ms, B=8 2.797 -> 2.752, B=16 with MLP-up 2: 3.154 -> 3.123) and W8A16 at B > 2
+  // (B=8 2.185 -> 2.148; B=16 W8A16 QKV 2.602 -> 2.508, profiles/r2_b16_sweep.log); the LayerNorm-streaming W8A16 MLP-up 4 stages at B <= 2 (B=1 1.723 -> 1.685,
   // B=2 1.808 -> 1.777).  GPT-2 (h 1600) keeps the plan's own depths (both measured slower there).
   const bool big = m.t == 1 && h >= 4096;
   auto st_req = [](const char* name, int dflt) { const char* v = std::getenv(name); return v ? std::atoi(v) : dflt; };
-  const int qkv_st = big && (!i8 || (m.a16g(0) && B > 2 && B <= 8)) ? 3 : 0;
+  const int qkv_st = big && (!i8 || (m.a16g(0) && B > 2)) ? 3 : 0;
   const int up_st = big && i8 && m.a16g(2) && m.ln_use(2) && B <= 2 ? 4 : (big && !i8 && B > 8 ? 2 : 0);
   sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
                                 m.ln_use(0), m.a16g(0), kg, st_req("DSINF_STAGES_QKV", qkv_st));
@@ -660,7 +660,9 @@ struct Enqueuer {
     // small fp16 layers (h < 4096, TP = 1, B <= 8: GPT-2 1.5B) leave room for early MLP-down and
     // attention CTAs: B=1 1.642 -> 1.593 ms, B=8 1.843 -> 1.796 (profiles/r2_gpt2_sweep.log)
     const bool small16 = !m.int8 && m.h < 4096 && m.t == 1 && m.B <= 8;
-    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0) | (small16 ? 0x12 : 0);
+    // INT8 at B > 8 (W8A16 since the tuning pass): attention early too (GPT-J B=16 2.502 -> 2.476 ms)
+    const bool i8big = m.int8 && m.B > 8 && m.t == 1;
+    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0) | (small16 ? 0x12 : 0) | (i8big ? 0x02 : 0);
   }();
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
@@ -1470,7 +1472,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
     // DSINF_A16_MASK overrides for experiments.
     if (m->int8) {
       if (rt->int8_act == DSINF_INT8_W8A16) m->a16_mask = 0xf;
-      else if (rt->int8_act == DSINF_INT8_AUTO) m->a16_mask = rt->batch <= 8 ? 0xf : (m->t == 1 ? 0xe : 0x0);
+      else if (rt->int8_act == DSINF_INT8_AUTO) m->a16_mask = rt->batch <= 8 || m->t == 1 ? 0xf : 0x0;  // W8A16 QKV at B=16 with 3 stages: 2.587 -> 2.508 ms
       if (const char* am = std::getenv("DSINF_A16_MASK")) m->a16_mask = static_cast<int>(std::strtol(am, nullptr, 0)) & 0xf;
     }
     m->a16 = m->a16_mask != 0;

@@ -77,11 +77,11 @@ def gpu_run(hidden, layers, heads, vocab, *, dtype, batch, prompts, tp=1):
 
 
 def auto_mask(batch, tp):
-    """The oracle image of DSINF_INT8_AUTO (model.cu dsinf_model_create): W8A16 everywhere up to
-    B = 8; at B = 16 W8A8 QKV + W8A16 the rest at TP = 1, W8A8 everywhere at TP > 1."""
-    if batch <= 8:
+    """The oracle image of DSINF_INT8_AUTO (model.cu dsinf_model_create): W8A16 everywhere at TP = 1
+    and up to B = 8; W8A8 everywhere at TP > 1 and B = 16."""
+    if batch <= 8 or tp == 1:
         return 0x10f
-    return 0x10e if tp == 1 else 0x100
+    return 0x100
 
 
 def compare(name, dtype, tokens, glog, olog, spread=None):
