@@ -334,6 +334,170 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 4 : 1) attention_tma_kernel(co
   merge_chunks_and_store(p, co, cst, head, b, c, C, tid, NT);
 }
 
+// Tensor-core variant (DSINF_ATTN_MMA=1; d in {64, 96, 128}): the bulk-copy ring with K/V rows
+// landing at a padded stride (d + 8 halves: the mma fragment loads are conflict-free), scores
+// S = K q on mma.m16n8k16 (q in column 0 of B; warps 0-1 take 16 positions each), the online softmax
+// on 32 lanes (one position each), and O += P V on mma (P in row 0 of A; each warp 32 dims, V
+// fragments by ldmatrix.trans).  q and P are rounded to fp16 for the MMAs, accumulation is fp32.
+// row padding in halves: 8 = conflict-free fragment loads but one bulk copy per row (measured 2x
+// slower: the single issuing thread serialises 64 copies per stage); 0 = two bulk copies per stage
+constexpr int kMmaPad = 0;
+__device__ __forceinline__ uint32_t ptx_pack_h2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void att_ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__host__ __device__ constexpr size_t mma_stage_halves(int d) { return static_cast<size_t>(2) * kTmaRows * (d + kMmaPad); }
+size_t mma_smem_bytes(int d) {
+  // ring (2 stages) + q (d halves) + raw scores [32] + co [d] + cst [2] + 2 barriers
+  return 2 * mma_stage_halves(d) * 2 + static_cast<size_t>(d) * 2 + 32 * 4 + static_cast<size_t>(d) * 4 + 16 + 16;
+}
+
+__global__ void __launch_bounds__(128) attention_mma_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ __align__(128) uint8_t araw[];
+  const int d = p.d, SP = d + kMmaPad;
+  const size_t stage_halves = mma_stage_halves(d);
+  __half* ring = reinterpret_cast<__half*>(araw);
+  __half* sq = ring + 2 * stage_halves;
+  float* ssc = reinterpret_cast<float*>(sq + d);
+  float* co = ssc + 32;
+  float* cst = co + d;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cst + 4) + 0);
+  const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  ptx::trace_begin(p.trace);
+  ptx::pdl_trigger();
+  if (tid == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_mbar_init();
+  }
+  const int ctx = *reinterpret_cast<const volatile int*>(p.pos) + 1;
+  const int chunk = (ctx + C - 1) / C;
+  const int j0 = c * chunk;
+  const int j1 = min(ctx, j0 + chunk);
+  const int n = max(0, j1 - j0);
+  const int nst = (n + kTmaRows - 1) / kTmaRows;
+  const size_t kv_base = (static_cast<size_t>(b) * p.H + head) * p.max_seq * d;
+  const uint64_t pol = ptx::policy_evict_first();
+  auto issue = [&](int st) {  // one bulk copy per K and V row into the padded stage
+    const int rows = min(kTmaRows, n - st * kTmaRows);
+    const uint32_t bytes = static_cast<uint32_t>(d) * 2;
+    __half* dst = ring + (st & 1) * stage_halves;
+    const size_t src = kv_base + static_cast<size_t>(j0 + st * kTmaRows) * d;
+    ptx::mbar_arrive_expect_tx(&bars[st & 1], 2 * bytes * rows);
+    if (kMmaPad == 0) {  // contiguous rows: one bulk copy each for K and V
+      ptx::bulk_g2s(dst, p.kc + src, bytes * rows, &bars[st & 1], pol);
+      ptx::bulk_g2s(dst + kTmaRows * SP, p.vc + src, bytes * rows, &bars[st & 1], pol);
+    } else {
+      for (int r = 0; r < rows; ++r) {
+        ptx::bulk_g2s(dst + r * SP, p.kc + src + static_cast<size_t>(r) * d, bytes, &bars[st & 1], pol);
+        ptx::bulk_g2s(dst + (kTmaRows + r) * SP, p.vc + src + static_cast<size_t>(r) * d, bytes, &bars[st & 1], pol);
+      }
+    }
+  };
+  __syncthreads();  // barrier init visible
+  ptx::pdl_wait();
+  if (tid == 0) {
+    if (nst > 0) issue(0);
+    if (nst > 1) issue(1);
+  }
+  constexpr float kLog2e = 1.4426950408889634f;
+  for (int i = tid; i < d; i += 128)
+    sq[i] = __float2half_rn(__half2float(__ldcg(p.q + static_cast<size_t>(b) * p.H * d + head * d + i)) * p.scale * kLog2e);
+  __syncthreads();
+  float m = -INFINITY, l = 0.f;
+  float o[4][4];  // this warp's 32 dims: 4 n-tiles (row 0 of the accumulator is the output)
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
+  const bool pv_warp = warp * 32 < d;
+  for (int st = 0; st < nst; ++st) {
+    ptx::mbar_wait(&bars[st & 1], static_cast<uint32_t>((st >> 1) & 1));
+    const __half* ks = ring + (st & 1) * stage_halves;
+    const __half* vs = ks + kTmaRows * SP;
+    const int rows = min(kTmaRows, n - st * kTmaRows);
+    if (rows < kTmaRows) {  // rows past the context hold stale bytes: zero their V (P is 0 there)
+      __half* vz = const_cast<__half*>(vs);
+      for (int i = tid; i < (kTmaRows - rows) * d; i += 128) vz[(rows + i / d) * SP + i % d] = __ushort_as_half(0);
+    }
+    if (warp < 2) {  // S[16 positions] = K q, k over d in steps of 16
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+      const __half* kr = ks + (warp * 16) * SP;
+      for (int k0 = 0; k0 < d; k0 += 16) {
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(kr + g * SP + k0 + 2 * t);
+        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(kr + (g + 8) * SP + k0 + 2 * t);
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(kr + g * SP + k0 + 8 + 2 * t);
+        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(kr + (g + 8) * SP + k0 + 8 + 2 * t);
+        const uint32_t b0 = g == 0 ? *reinterpret_cast<const uint32_t*>(sq + k0 + 2 * t) : 0u;
+        const uint32_t b1 = g == 0 ? *reinterpret_cast<const uint32_t*>(sq + k0 + 8 + 2 * t) : 0u;
+        ptx::mma_f16(sacc, a0, a1, a2, a3, b0, b1);
+      }
+      if (t == 0) {  // column 0: positions g and g + 8 of this warp's 16
+        ssc[warp * 16 + g] = sacc[0];
+        ssc[warp * 16 + g + 8] = sacc[2];
+      }
+    }
+    __syncthreads();
+    // online softmax: lane j owns position j of the stage (every warp computes the same values)
+    const float sj = lane < rows ? ssc[lane] : -INFINITY;
+    float mt = sj;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+    const float mn = fmaxf(m, mt);
+    const float corr = exp2f(m - mn);
+    const float pj = lane < rows ? exp2f(sj - mn) : 0.f;
+    float ps = pj;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+    l = l * corr + ps;
+    m = mn;
+    if (pv_warp) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[nt][e] *= corr;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {  // 16 positions per k step
+        const float p0 = __shfl_sync(0xffffffffu, pj, kk * 16 + 2 * t);
+        const float p1 = __shfl_sync(0xffffffffu, pj, kk * 16 + 2 * t + 1);
+        const float p2 = __shfl_sync(0xffffffffu, pj, kk * 16 + 8 + 2 * t);
+        const float p3 = __shfl_sync(0xffffffffu, pj, kk * 16 + 8 + 2 * t + 1);
+        const uint32_t pa0 = g == 0 ? ptx_pack_h2(p0, p1) : 0u;
+        const uint32_t pa2 = g == 0 ? ptx_pack_h2(p2, p3) : 0u;
+        const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+        for (int n2 = 0; n2 < 2; ++n2) {
+          uint32_t b0, b1, b2, b3;
+          att_ldsm_x4_t(ptx::smem_u32(vs + key * SP + warp * 32 + n2 * 16 + (lane >> 4) * 8), b0, b1, b2, b3);
+          ptx::mma_f16(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
+          ptx::mma_f16(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
+        }
+      }
+    }
+    __syncthreads();  // the ring slot and the raw scores are free
+    if (tid == 0 && st + 2 < nst) issue(st + 2);
+  }
+  if (pv_warp && g == 0) {
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      co[warp * 32 + nt * 8 + 2 * t] = o[nt][0];
+      co[warp * 32 + nt * 8 + 2 * t + 1] = o[nt][1];
+    }
+  }
+  if (tid == 0) {
+    cst[0] = m == -INFINITY ? m : m * 0.69314718055994531f;  // natural-log domain for the merge
+    cst[1] = l;
+  }
+  __syncthreads();
+  merge_chunks_and_store(p, co, cst, head, b, c, C, tid, 128);
+}
+
 template <int TPP, int NT>
 size_t tma_smem_bytes(int d, int ring) {
   return tma_ring_bytes<TPP>(d, ring) + (tma_scratch_floats<TPP, NT>(d) * 4 + 7) / 8 * 8 + 8 * kTmaMaxRing;
@@ -380,6 +544,10 @@ void configure() {
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_mma_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  if (carveout_max())
+    DSINF_CUDA_CHECK(cudaFuncSetAttribute(attention_mma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   configure_tma<8, 128>();
   configure_tma<16, 128>();
   configure_tma<32, 128>();
@@ -418,6 +586,11 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
     p.early_kv = ev != nullptr && std::atoi(ev) != 0;
     // DSINF_ATTN_NT=256: 256 threads per CTA (measured slower at B = 8 / 16: GPT-J int8 B=16 attention
     // 13.8 -> 15.5 us per layer, fp16 B=8 10.8 -> 12.8; profiles/r2_attn_fastpath_ab.log)
+    const char* mmv = std::getenv("DSINF_ATTN_MMA");
+    if (mmv != nullptr && std::atoi(mmv) != 0 && (p.d == 64 || p.d == 96 || p.d == 128)) {
+      launch_pdl(attention_mma_kernel, grid, dim3(128), mma_smem_bytes(p.d), s, pdl, p, cluster);
+      return;
+    }
     const char* ntv = std::getenv("DSINF_ATTN_NT");
     const int nt = ntv ? std::atoi(ntv) : 128;
     if (nt == 256)
