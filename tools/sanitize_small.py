@@ -22,6 +22,22 @@ for dt, B, tp in [(2, 1, 1), (1, 3, 1), (2, 5, 1), (1, 8, 1), (2, 2, 2)]:
     m.step(7)
     torch.cuda.synchronize()
     m.close()
+# round-2 paths: full 32-position attention stages (one context chunk per (row, head)), the QKV
+# attention tail, the tensor-core attention stage, INT8 K-group W8A16 and INT8 AUTO at B = 16
+for env, kw in [({"DSINF_ATTN_CTAS": "1"}, dict(dtype_bytes=2, batch=2)),
+                ({"DSINF_ATTN_FUSE": "1"}, dict(dtype_bytes=2, batch=1)),
+                ({"DSINF_ATTN_FUSE": "1"}, dict(dtype_bytes=1, batch=2, int8_act=capi.INT8_W8A16)),
+                ({"DSINF_ATTN_MMA": "1", "DSINF_ATTN_CTAS": "1"}, dict(dtype_bytes=2, batch=2)),
+                ({}, dict(dtype_bytes=1, batch=1, int8_act=capi.INT8_W8A16, int8_group=128)),
+                ({}, dict(dtype_bytes=1, batch=16, int8_act=capi.INT8_AUTO))]:
+    os.environ.update(env)
+    m = DecoderModel(512, 2, 4, 1000, max_ctx=80, use_cuda_graph=False, **kw)
+    m.set_prompt(rng.integers(0, 1000, (kw["batch"], 40)).astype(np.int32))
+    m.step(44)
+    torch.cuda.synchronize()
+    m.close()
+    for k in env:
+        del os.environ[k]
 dev = torch.device("cuda")
 w = (torch.randn(640, 320, device=dev) * 0.05).half()
 x = torch.randn(3, 320, device=dev).half()
