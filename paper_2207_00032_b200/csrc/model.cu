@@ -409,15 +409,17 @@ void build_shard(Model& m, Shard& sh, cudaStream_t s) {
   // B=2 1.808 -> 1.777).  GPT-2 (h 1600) keeps the plan's own depths (both measured slower there).
   const bool big = m.t == 1 && h >= 4096;
   auto st_req = [](const char* name, int dflt) { const char* v = std::getenv(name); return v ? std::atoi(v) : dflt; };
+  // per-GEMM K-split requests (DSINF_KSPLIT_{QKV,O,UP,DOWN}; 0 = the plan's one-wave choice)
+  auto ks_req = [](const char* name) { const char* v = std::getenv(name); return v ? std::atoi(v) : 0; };
   const int qkv_st = big && (!i8 || (m.a16g(0) && B > 2)) ? 3 : 0;
   const int up_st = big && i8 && m.a16g(2) && m.ln_use(2) && B <= 2 ? 4 : (big && !i8 && B > 8 ? 2 : 0);
-  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(0),
+  sh.plan_qkv = gemm::make_plan(static_cast<int>(3 * Hl * d), static_cast<int>(h), B, i8, ks_req("DSINF_KSPLIT_QKV"), m.xs_ln, m.a16g(0),
                                 m.ln_use(0), m.a16g(0), kg, st_req("DSINF_STAGES_QKV", qkv_st));
-  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, 0, m.xs_od, m.a16g(1), false,
+  sh.plan_o = gemm::make_plan(static_cast<int>(h), static_cast<int>(Hl * d), B, i8, ks_req("DSINF_KSPLIT_O"), m.xs_od, m.a16g(1), false,
                               m.a16g(1), kg, st_req("DSINF_STAGES_O", 0));
-  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, 0, m.xs_ln, m.a16g(2), m.ln_use(2),
+  sh.plan_up = gemm::make_plan(static_cast<int>(Fl), static_cast<int>(h), B, i8, ks_req("DSINF_KSPLIT_UP"), m.xs_ln, m.a16g(2), m.ln_use(2),
                                m.a16g(2), kg, st_req("DSINF_STAGES_UP", up_st));
-  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, 0, m.xs_od, m.a16g(3), false,
+  sh.plan_down = gemm::make_plan(static_cast<int>(h), static_cast<int>(Fl), B, i8, ks_req("DSINF_KSPLIT_DOWN"), m.xs_od, m.a16g(3), false,
                                  m.a16g(3), kg, st_req("DSINF_STAGES_DOWN", 0));
   if (m.down_flags) {
     for (LayerW& w : sh.layers) {
