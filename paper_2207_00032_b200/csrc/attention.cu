@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 4 : 1) attention_tma_kernel(co
   const int head = blockIdx.x, b = blockIdx.y, c = blockIdx.z, C = gridDim.z;
   const int tid = threadIdx.x;
   ptx::trace_begin(p.trace);
-  ptx::pdl_trigger();
+  if (!p.late_trigger) ptx::pdl_trigger();
   if (tid == 0) {
     for (int r = 0; r < R; ++r) ptx::mbar_init(&bars[r], 1);
     ptx::fence_mbar_init();
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 4 : 1) attention_tma_kernel(co
   if (p.early_kv && tid == 0)
     while (issued < min(R, nst) && j0 + (issued + 1) * kTmaRows <= ctx - 1) issue(issued++);  // rows < pos
   ptx::pdl_wait();
+  if (p.late_trigger) ptx::pdl_trigger();  // dependents launch once our inputs are complete
   if (tid == 0) {
     for (int st = issued; st < min(R, nst); ++st) issue(st);
   }
@@ -584,6 +585,8 @@ void attention(const AttnParams& p_in, int chunks, cudaStream_t s, bool pdl) {
     p.tma_ring = std::max(2, std::min(p.tma_ring, max_st));
     const char* ev = std::getenv("DSINF_ATTN_EARLY");
     p.early_kv = ev != nullptr && std::atoi(ev) != 0;
+    const char* ltv = std::getenv("DSINF_ATTN_LATE_TRIGGER");  // overrides the model's choice
+    if (ltv != nullptr) p.late_trigger = std::atoi(ltv) != 0;
     // DSINF_ATTN_NT=256: 256 threads per CTA (measured slower at B = 8 / 16: GPT-J int8 B=16 attention
     // 13.8 -> 15.5 us per layer, fp16 B=8 10.8 -> 12.8; profiles/r2_attn_fastpath_ab.log)
     const char* mmv = std::getenv("DSINF_ATTN_MMA");

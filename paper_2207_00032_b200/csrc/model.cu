@@ -158,6 +158,11 @@ struct dsinf_model {
   // QKV attention tail (Deep-Fusion region 2 in the QKV launch, LayerNorm-streaming plan): no
   // standalone attention launch.  Opt-in (DSINF_ATTN_FUSE=1; DSINF_ATTN_FUSE_MAXB batch cap, 8)
   bool attn_fuse = false;
+  // attention PDL-launched with its dependents released after its own dependency wait (and MLP-down
+  // early): fp16 at h <= 4096 and INT8 at h < 4096, TP = 1 (GPT-J fp16 B=1 2.501 -> 2.458 ms, B=8
+  // 2.707 -> 2.670; GPT-2 int8 B=8 1.818 -> 1.764; slower for GPT-J INT8 and NeoX fp16;
+  // profiles/r2_attn_late_trigger.log)
+  bool attn_late = false;
   // TP > 1 without NCCL kernels between the GEMMs: the row-parallel GEMMs push their partials into
   // every rank's slots and signal a counter; the next LayerNorm prologue waits and sums the slots
   bool fused_ar = false;
@@ -664,7 +669,8 @@ struct Enqueuer {
     const bool small16 = !m.int8 && m.h < 4096 && m.t == 1 && m.B <= 8;
     // INT8 at B > 8 (W8A16 since the tuning pass): attention early too (GPT-J B=16 2.502 -> 2.476 ms)
     const bool i8big = m.int8 && m.B > 8 && m.t == 1;
-    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0) | (small16 ? 0x12 : 0) | (i8big ? 0x02 : 0);
+    return 0xad | (m.a16g(3) && m.B <= 2 ? 0x10 : 0) | (small16 ? 0x12 : 0) | (i8big ? 0x02 : 0) |
+           (m.attn_late ? 0x12 : 0);
   }();
   bool P(int bit) const { return pdl && ((mask >> bit) & 1); }
 
@@ -854,6 +860,7 @@ struct Enqueuer {
     a.scale = 1.0f / std::sqrt(static_cast<float>(m.d));
     a.amax_out = amslot(sh, 2 * l);
     a.trace = tslot(DSINF_LK_ATTN);
+    a.late_trigger = m.attn_late ? 1 : 0;
     ops::attention(a, m.attn_chunks, s, P(1));
     ++launches;
   }
@@ -1524,6 +1531,7 @@ int dsinf_model_create(const dsinf_model_config* cfg, const dsinf_runtime_config
       m->down_flags = m->t == 1 && m->xs_od && !m->q8g(3) && dfv != nullptr && std::atoi(dfv) != 0;
       const bool ls_default = m->int8 ? m->B <= 2 : m->B <= 8;
       m->ln_stream = m->fuse_ln && m->xs_ln && m->h % 8 == 0 && (lsv ? std::atoi(lsv) != 0 : ls_default);
+      m->attn_late = m->t == 1 && (m->int8 ? m->h < 4096 : m->h <= 4096);
       {
         const char* afv = std::getenv("DSINF_ATTN_FUSE");
         const char* amb = std::getenv("DSINF_ATTN_FUSE_MAXB");

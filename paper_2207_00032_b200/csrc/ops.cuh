@@ -72,6 +72,7 @@ struct AttnParams {
   int kv_rows_cap;
   int tma_ring;  // bulk-copy variant: K/V ring slots (set by ops::attention)
   int early_kv;  // bulk-copy variant: stages of earlier positions requested before the dependency wait
+  int late_trigger;  // bulk-copy variant: release dependents after the dependency wait, not at kernel start
 };
 int attention_chunks(int B, int H);
 // Sets kernel attributes (dynamic smem, non-portable clusters); call before graph capture.
